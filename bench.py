@@ -1,0 +1,398 @@
+"""Benchmark: circuit time-to-solution and effective HBM GB/s per part-pass.
+
+One step = one full simulation of the BASELINE config circuit (every part
+of its partition, one kernel pass each) on a state already resident in HBM.
+``value`` = algorithmic part-pass bytes of all ranks / step time, where a
+part-pass moves 2 x 2^l x 16 B (read + write of a rank's shard, SURVEY.md
+§8(d)); ``ms_per_step`` is the circuit time-to-solution (partitioning, done
+once on the host, is reported separately). ``e2e`` is the same metric
+through the public API with the initial state in pinned host memory and the
+final state read back every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--strategy dfs]
+    python bench.py --impl reference ...   # the CPU port of the reference path
+
+Under torchrun (N > 1) the state is sharded over the N ranks (n + log2 N
+qubits, weak scaling) and layout switches run over NCCL.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "circuit time-to-solution and effective HBM GB/s per part-pass at 1/2/4/8 B200"
+UNIT = "GB/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def _traffic_from_profiles(config: str, strategy: str):
+    """Per-launch DRAM bytes of the part kernel from the committed ncu
+    summary of this workload (profiles/*_ncu_summary.json), else None."""
+    for f in sorted((ROOT / "profiles").glob("*ncu_summary.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+        except Exception:
+            continue
+        if d.get("workload") == f"{config}/{strategy}" and d.get("dram_bytes_per_launch"):
+            return float(d["dram_bytes_per_launch"])
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm, smax, power = [], [], []
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+                power.append(float(r[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, r[3:7]):
+                if v.strip().lower() in ("active", "1"):
+                    reasons.add(name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def build_workload(config: str, strategy: str, extra_bits: int = 0):
+    from paper_2205_06973_b200 import build_dag, configs, partition_dagp, partition_dfs, partition_nat
+
+    cfg = configs.CONFIGS[config.split("@")[0]]
+    name = config
+    if extra_bits:
+        name = f"{config.split('@')[0]}@{cfg.num_qubits + extra_bits}"
+    circuit = configs.build(name)
+    t0 = time.perf_counter()
+    fn = {"nat": partition_nat, "dfs": partition_dfs, "dagp": partition_dagp}[strategy]
+    part = fn(build_dag(circuit), cfg.limit)
+    t_part = time.perf_counter() - t0
+    return cfg, circuit, part, t_part
+
+
+# --------------------------------------------------------------------------- CPU reference arm
+
+def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup, quiet=False):
+    """The reference path's CPU restatement (oracle/sv_oracle.c, all host
+    threads) on a bounded sample of fixings of every part."""
+    import numpy as np
+
+    from oracle import c_oracle
+
+    c_oracle.lib()
+    threads = c_oracle.threads()
+    n = circuit.num_qubits
+    # calibrate: fixings per part so that one step takes ~target seconds
+    target = args.cpu_step_seconds
+    psi = np.zeros(1 << n, dtype=np.complex128)
+    psi[0] = 1.0
+    slots = [c_oracle.part_slots(circuit, p.gate_indices, p.qubits) for p in part.parts]
+    def make_plan(frac):
+        return [(pos, ops, sl, max(1, min(1 << (n - len(pos)), int((1 << (n - len(pos))) * frac))))
+                for pos, ops, sl in slots]
+
+    def timed(plan):
+        t0 = time.perf_counter()
+        for pos, ops, sl, k in plan:
+            c_oracle.run_part(psi, pos, ops, sl, 0, k)
+        return time.perf_counter() - t0
+
+    frac = 1e-4
+    while True:  # grow the sample until a pass is long enough to time
+        dt = timed(make_plan(frac))
+        if dt > 0.25 or frac >= 1.0:
+            break
+        frac = min(1.0, frac * 8)
+    frac = min(1.0, frac * target / dt)
+    plan = make_plan(frac)
+
+    def step():
+        b = 0
+        for pos, ops, sl, k in plan:
+            c_oracle.run_part(psi, pos, ops, sl, 0, k)
+            b += 2 * (k << len(pos)) * 16
+        return b
+
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    nbytes = 0
+    for _ in range(steps):
+        nbytes += step()
+    dt = time.perf_counter() - t0
+    value = nbytes / dt / 1e9
+    sample_amps = sum(k << len(pos) for pos, _, _, k in plan)
+    sample = (f"{config_label(args)}: each step runs every one of the {len(plan)} parts over "
+              f"{sample_amps / (1 << n) / len(plan):.4%} of its fixings ({sample_amps} amplitude updates "
+              f"per step, fixings 0..k-1 of each part) with {threads} threads; GB/s = 2 x 16 B x "
+              f"amplitudes / time, the same algorithmic count as the GPU arm")
+    full_s = (len(plan) * (1 << n) * 32) / (value * 1e9)
+    return {
+        "value": value, "threads": threads, "sample": sample, "ms_per_step": dt / steps * 1e3,
+        "projected_time_to_solution_s": full_s,
+    }
+
+
+def config_label(args):
+    return f"{args.config}/{args.strategy}"
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
+    import numpy as np
+    import torch
+
+    from paper_2205_06973_b200.hier import HierarchicalRun, execute_hierarchical
+    from paper_2205_06973_b200.statevec import allocate, init_basis
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    n = circuit.num_qubits
+    dist = world > 1
+    if dist:
+        from paper_2205_06973_b200.multi import ShardedRun
+
+        run = ShardedRun(circuit, part, int(math.log2(world)), device=dev)
+        n_local = run.n_local
+    else:
+        run = HierarchicalRun(circuit, part, device=dev)
+        n_local = n
+    num_parts = part.num_parts
+    bytes_per_pass = 2 * (1 << n_local) * 16
+    state = allocate(n_local, "complex128", dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(timed_events=None):
+        if rank == 0 or not dist:
+            init_basis(state, 0)
+        else:
+            state.zero_()
+        if timed_events is not None:
+            timed_events.append(torch.cuda.Event(enable_timing=True))
+            timed_events[-1].record(stream)
+        if dist:
+            run.run(state, events=timed_events)
+        elif timed_events is None:
+            run.program.run(state)
+        else:
+            for i in range(num_parts):
+                run.program.run(state, i, 1)
+                timed_events.append(torch.cuda.Event(enable_timing=True))
+                timed_events[-1].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
+    clocks = ClockSampler(dev.index if dev.index is not None else 0)
+    clocks.start()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    marks = []
+    torch.cuda.synchronize()
+    start.record(stream)
+    for _ in range(args.steps):
+        ev = []
+        one_step(ev)
+        marks.append(ev)
+    stop.record(stream)
+    torch.cuda.synchronize()
+    total_ms = start.elapsed_time(stop)
+    clk = clocks.stop()
+    # per-launch durations of the part kernel (events between launches)
+    durs = []
+    for ev in marks:
+        durs += [ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)]
+    # only the part kernels sit between the events when not distributed
+    if dist:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = world * num_parts * bytes_per_pass / (ms_step / 1e3) / 1e9
+
+    # e2e through the public API: host initial state in, host state out
+    e2e = None
+    if not dist and not args.no_e2e:
+        host_in = torch.zeros(1 << n, dtype=torch.complex128).pin_memory()
+        host_in[0] = 1.0
+        host_out = torch.empty_like(host_in).pin_memory()
+        from paper_2205_06973_b200.statevec import StateVector
+
+        def e2e_step():
+            st = StateVector(n, state)
+            state.copy_(host_in, non_blocking=True)
+            run.program.run(st.data)
+            host_out.copy_(state, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / args.steps
+        assert abs(float(host_out.abs().pow(2).sum()) - 1.0) < 1e-9
+        e2e = {"value": num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
+               "ms_per_step": e_ms, "h2d_bytes_per_step": (1 << n) * 16, "d2h_bytes_per_step": (1 << n) * 16,
+               "path": "public API: initial state from pinned host -> HierarchicalRun.program.run (all parts) "
+                       "-> final state to pinned host"}
+
+    info = [run.program.info(i) for i in range(num_parts)] if not dist else run.part_infos()
+    return {
+        "ms_step": ms_step, "value": value, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
+        "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
+        "comm": run.comm_summary() if dist else None,
+    }
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--strategy", default="dfs", choices=["nat", "dfs", "dagp"])
+    ap.add_argument("--cpu-step-seconds", type=float, default=4.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as tdist
+
+        if args.impl == "reference":
+            if rank != 0:
+                return 0
+            world = 1
+        else:
+            tdist.init_process_group("nccl")
+    extra = int(math.log2(world)) if world > 1 else 0
+    cfg, circuit, part, t_part = build_workload(args.config, args.strategy, extra)
+    n = circuit.num_qubits
+    config = {"workload": f"{args.config}: {cfg.description}" + (f", scaled to {n} qubits" if extra else ""),
+              "num_qubits": n, "limit": cfg.limit, "strategy": args.strategy, "parts": part.num_parts,
+              "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
+              "state_bytes_per_gpu": (1 << (n - extra)) * 16,
+              "l2_policy": "inputs larger than L2: the state (>= 1 GiB) exceeds the 126 MB L2",
+              "partition_seconds_host": round(t_part, 4), "parallelism": f"qubit-sharded x{world}" if world > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        r = cpu_arm(args, cfg, circuit, part, t_part, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
+                                 "sample": r["sample"]},
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "projected_time_to_solution_s": r["projected_time_to_solution_s"]}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    g = gpu_arm(args, cfg, circuit, part, t_part, rank, world)
+    if rank != 0:
+        return 0
+    peak, peak_kind = _peaks()
+    durs = g["durations_ms"]
+    avg_ms = sum(durs) / len(durs) if durs else g["ms_step"] / g["num_parts"]
+    achieved = g["bytes_per_pass"] / (avg_ms / 1e3) / 1e9
+    traffic = _traffic_from_profiles(args.config, args.strategy)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "kernel": "hs_part_kernel (one launch = one part-pass)",
+                "algorithmic_bytes_per_launch": g["bytes_per_pass"],
+                "avg_launch_ms": avg_ms,
+                "per_part_gbs": [g["bytes_per_pass"] / (d / 1e3) / 1e9 for d in durs[: g["num_parts"]]]}
+    infos = g["info"]
+    flops = sum(i["fp_ops_per_amp"] for i in infos) * (1 << g["n_local"])
+    line = {"metric": METRIC, "value": g["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": g["ms_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
+            "config": config, "roofline": roofline, "clocks": g["clocks"],
+            "gpu_launches": args.steps * g["num_parts"] + (args.steps * g["num_parts"] if g["e2e"] else 0),
+            "e2e": g["e2e"],
+            "time_to_solution_ms": g["ms_step"],
+            "fp64_flops_per_step_paper_count": flops,
+            "phases_per_part": [i["phases"] for i in infos],
+            "comm": g["comm"]}
+    if not args.no_cpu_baseline and world == 1:
+        r = cpu_arm(args, cfg, circuit, part, t_part, 2, 1)
+        line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
+                                "sample": r["sample"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

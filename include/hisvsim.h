@@ -1,0 +1,169 @@
+/*
+ * hisvsim.h — C ABI of the B200-native part-pass engine (libhisvsim.so).
+ *
+ * The reference (HiSVSIM `hisim` 0.1.0) is pure Python/numpy and has no FFI;
+ * its drop-in boundary is the Python function layer. Each
+ * entry point below replaces one reference function on the hot path:
+ *
+ *   hs_part_apply      ~ hisim.hier.run_part          (pkg/src/hisim/hier.py:220-244)
+ *                        incl. apply_op per gate      (pkg/src/hisim/statevec.py:241-261)
+ *   hs_program_create  ~ hisim.hier.remap_part over all parts (hier.py:181-217),
+ *                        planned once, uploaded once
+ *   hs_program_run     ~ the part loop of execute_hierarchical (hier.py:342-368)
+ *                        / _run_on_buffers (pkg/src/hisim/dist.py:454-482)
+ *   hs_state_init_basis~ hisim.statevec.zero_state    (statevec.py:151-167)
+ *   hs_bit_permute     ~ RedistributionPlan.apply, the local half
+ *                        (dist.py:261-268; layout_positions dist.py:151-166)
+ *   hs_pack_segments / hs_unpack_segments
+ *                      ~ the remote half of RedistributionPlan.apply: gather the
+ *                        amplitudes bound for each peer into contiguous
+ *                        segments for the NCCL all-to-all, and scatter back
+ *   hs_max_abs_diff    ~ hisim.hier.verify_against_flat (hier.py:422-436)
+ *
+ * Conventions (same as the reference):
+ *   - amplitude index is little-endian: bit i of the index is qubit/position i;
+ *   - a part is given by its staged positions (strictly ascending, the
+ *     QubitSlotMap of hier.py:49-77) and its gates in program order with
+ *     operands as slots into that list (ExecutablePart.op_slots), controls
+ *     first and target last (qasm.py:78-88);
+ *   - gate kinds are numbered in hisim.qasm.GateKind declaration order.
+ *
+ * Ownership: the caller owns every state buffer (device memory, e.g. a torch
+ * tensor); the library never allocates or frees it. Programs and scratch are
+ * owned by their handles. All launches are stream-ordered and asynchronous on
+ * the stream passed in (NULL = legacy default stream). No C++ exception
+ * crosses this boundary: every call returns an hs_status and the message of
+ * the last failure on the calling thread is available from hs_last_error().
+ */
+#ifndef HISVSIM_H
+#define HISVSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_ABI_VERSION 1
+#define HS_MAX_STAGED 24
+
+/* status codes; the Python shim maps them onto the hisim error taxonomy */
+typedef enum {
+  HS_OK = 0,
+  HS_ERR_INVALID = 1,    /* ValueError: bad shape / position / operand      */
+  HS_ERR_CAPACITY = 2,   /* QubitCountOutOfRangeError: does not fit          */
+  HS_ERR_CUDA = 3,       /* DeviceError: CUDA runtime failure                */
+  HS_ERR_TOO_WIDE = 4,   /* PartTooWideForLayoutError-like: tile > on-chip   */
+  HS_ERR_UNSUPPORTED = 5 /* gate kind or dtype not supported                 */
+} hs_status;
+
+typedef enum { HS_C128 = 0, HS_C64 = 1 } hs_dtype;
+
+/* hisim.qasm.GateKind, declaration order (qasm.py:26-47) */
+typedef enum {
+  HS_H = 0, HS_X, HS_Y, HS_Z, HS_S, HS_T, HS_SDG, HS_TDG,
+  HS_RX, HS_RY, HS_RZ, HS_U1, HS_U3,
+  HS_CX, HS_CZ, HS_CRZ, HS_CRY, HS_SWAP, HS_CCX,
+  HS_NUM_KINDS
+} hs_gate_kind;
+
+/* one GateOp in slot coordinates (ExecutablePart.ops[i] + op_slots[i]) */
+typedef struct {
+  int32_t kind;      /* hs_gate_kind */
+  int32_t num_slots; /* arity: 1, 2 or 3 */
+  int32_t slots[3];  /* controls first, target last */
+  int32_t reserved;
+  double params[3];  /* radians, reference parameter order */
+} hs_gate;
+
+/* one part: staged positions + a window into the gate array */
+typedef struct {
+  int32_t num_staged;            /* w */
+  int32_t staged[HS_MAX_STAGED]; /* strictly ascending, < n_local */
+  int32_t gate_offset;
+  int32_t num_gates;
+} hs_part;
+
+/* what the planner made of a part (for traces / reports / tests) */
+typedef struct {
+  int32_t tile_bits;      /* T: positions staged per CTA tile (w + fill) */
+  int32_t tile_pos[32];   /* ascending physical positions of the tile */
+  int32_t reg_bits;       /* register bits per thread */
+  int32_t phases;         /* register phases (SMEM exchanges) */
+  int32_t instructions;   /* device instructions incl. phase markers */
+  int32_t dense_gates, perm_gates, diag_gates, swaps_relabelled;
+  int64_t tiles;          /* CTA tiles per launch = batch * 2^(n_local - T) */
+  double fp_ops_per_amp;  /* diagnostic real FLOPs per amplitude */
+} hs_part_info;
+
+typedef struct hs_engine hs_engine;
+typedef struct hs_program hs_program;
+
+const char* hs_last_error(void);
+int hs_abi_version(void);
+
+/* engine: binds a CUDA device; holds launch configuration */
+int hs_engine_create(int device, hs_engine** out);
+int hs_engine_destroy(hs_engine* eng);
+/* SMs and the max tile bits per dtype chosen for this device */
+int hs_engine_query(hs_engine* eng, int* num_sms, int* tile_bits_c128, int* tile_bits_c64);
+
+/* plan + upload a whole part sequence for buffers of batch x 2^n_local */
+int hs_program_create(hs_engine* eng, int n_local, int dtype,
+                      const hs_part* parts, int num_parts,
+                      const hs_gate* gates, int num_gates, hs_program** out);
+int hs_program_destroy(hs_program* prog);
+int hs_program_num_parts(hs_program* prog);
+int hs_program_part_info(hs_program* prog, int part, hs_part_info* out);
+/* device instructions of one part, copied to host (test/debug); returns the
+ * count via *count; buf may be NULL to query the size in bytes */
+int hs_program_dump(hs_program* prog, int part, void* buf, size_t buf_bytes,
+                    int* count, size_t* instr_bytes);
+/* launch parts [first, first+count) in order on `stream` over `batch`
+ * contiguous rows of 2^n_local amplitudes each */
+int hs_program_run(hs_program* prog, void* state, int64_t batch,
+                   int first, int count, void* stream);
+/* same, but records the launches into a CUDA graph on first use and
+ * replays it afterwards (state pointer and batch must not change) */
+int hs_program_run_graph(hs_program* prog, void* state, int64_t batch, void* stream);
+
+/* host-only planning of one part (no CUDA call; usable without a GPU):
+ * writes the PartLaunch header + device instructions into buf (NULL to
+ * query *bytes), and the plan summary into *info */
+int hs_plan_part(int n_local, int dtype, int tile_bits, const int32_t* staged, int w,
+                 const hs_gate* gates, int num_gates, void* buf, size_t buf_bytes,
+                 size_t* bytes, hs_part_info* info);
+
+/* one-shot run_part: plan, upload, launch, free (synchronizes the stream) */
+int hs_part_apply(hs_engine* eng, void* state, int64_t batch, int n_local, int dtype,
+                  const int32_t* staged, int w, const hs_gate* gates, int num_gates,
+                  void* stream);
+
+/* |index> : zero the buffer and write 1 at `index` (per row when batch>1 use
+ * row 0 only: the buffer is treated as one state of batch*2^n_local) */
+int hs_state_init_basis(void* state, int64_t num_amps, int dtype, int64_t index, void* stream);
+
+/* out[perm(i)] = in[i] where bit j of i moves to bit dst_of[j];
+ * out-of-place, num_bits <= 40 */
+int hs_bit_permute(const void* in, void* out, int num_bits, int dtype,
+                   const int32_t* dst_of, void* stream);
+
+/* max |a - b| over n amplitudes of `dtype`, b given as complex128 (the
+ * oracle's type); result written to *host_result after a stream sync */
+int hs_max_abs_diff(const void* a, int dtype, const void* b_c128, int64_t n,
+                    double* host_result, void* stream);
+
+/* Pack for a qubit-remap all-to-all: with `num_seg_bits` local positions
+ * seg_pos[] whose values name a destination segment, copy src into dst so
+ * that all amplitudes of segment k are contiguous (segment-major, inner
+ * order = remaining bits ascending). unpack is the inverse. */
+int hs_pack_segments(const void* src, void* dst, int num_bits, int dtype,
+                     const int32_t* seg_pos, int num_seg_bits, void* stream);
+int hs_unpack_segments(const void* src, void* dst, int num_bits, int dtype,
+                       const int32_t* seg_pos, int num_seg_bits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HISVSIM_H */

@@ -1,0 +1,365 @@
+// C-ABI implementation (include/hisvsim.h): engine and program handles,
+// status codes + thread-local last error, stream-ordered launches.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "hs_common.h"
+
+namespace hs {
+cudaError_t prepare_kernels(int smem_optin);
+cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void* psi, int n_local,
+                        int64_t batch, int num_sms, cudaStream_t stream);
+cudaError_t launch_set_basis(void* psi, int dtype, int64_t index, cudaStream_t s);
+cudaError_t launch_bit_permute(const void* in, void* out, int nbits, int dtype, const int32_t* dst_of,
+                               int num_sms, cudaStream_t s);
+cudaError_t launch_segments(bool pack, const void* in, void* out, int nbits, int dtype,
+                            const int32_t* seg_pos, int nseg, int num_sms, cudaStream_t s);
+cudaError_t launch_maxdiff(const void* a, int dtype, const void* b, int64_t n, unsigned long long* dres,
+                           int num_sms, cudaStream_t s);
+}  // namespace hs
+
+using namespace hs;
+
+struct hs_engine {
+  int device = 0;
+  int num_sms = 0;
+  int smem_optin = 0;
+  int tile_c128 = 12;
+  int tile_c64 = 13;
+  unsigned long long* d_scratch = nullptr;  // reductions
+};
+
+struct hs_program {
+  hs_engine* eng = nullptr;
+  int n_local = 0;
+  int dtype = 0;
+  std::vector<PartPlan> plans;
+  Instr* d_prog = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  void* graph_state = nullptr;
+  int64_t graph_batch = 0;
+  cudaStream_t graph_stream = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(HS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                               cudaGetErrorString(e) + ")");
+}
+
+#define HS_CUDA(call, what)                         \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+int tile_for(const hs_engine* eng, int dtype) {
+  return dtype == HS_C128 ? eng->tile_c128 : eng->tile_c64;
+}
+
+int check_dtype(int dtype) {
+  if (dtype != HS_C128 && dtype != HS_C64) return fail(HS_ERR_UNSUPPORTED, "dtype must be HS_C128 or HS_C64");
+  return HS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+int hs_abi_version(void) { return HS_ABI_VERSION; }
+
+int hs_engine_create(int device, hs_engine** out) {
+  if (!out) return fail(HS_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  int count = 0;
+  HS_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  if (device < 0 || device >= count)
+    return fail(HS_ERR_INVALID, "device " + std::to_string(device) + " outside 0.." + std::to_string(count - 1));
+  HS_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  int major = 0;
+  HS_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device), "attr");
+  if (major != 10) return fail(HS_ERR_UNSUPPORTED, "libhisvsim is built for sm_100a (B200) only");
+  std::unique_ptr<hs_engine> eng(new (std::nothrow) hs_engine);
+  if (!eng) return fail(HS_ERR_CAPACITY, "out of host memory");
+  eng->device = device;
+  HS_CUDA(cudaDeviceGetAttribute(&eng->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+  HS_CUDA(cudaDeviceGetAttribute(&eng->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
+  HS_CUDA(prepare_kernels(eng->smem_optin), "cudaFuncSetAttribute");
+  HS_CUDA(cudaMalloc(&eng->d_scratch, 64), "cudaMalloc scratch");
+  *out = eng.release();
+  return HS_OK;
+}
+
+int hs_engine_destroy(hs_engine* eng) {
+  if (!eng) return HS_OK;
+  cudaSetDevice(eng->device);
+  if (eng->d_scratch) cudaFree(eng->d_scratch);
+  delete eng;
+  return HS_OK;
+}
+
+int hs_engine_query(hs_engine* eng, int* num_sms, int* tile_c128, int* tile_c64) {
+  if (!eng) return fail(HS_ERR_INVALID, "engine is NULL");
+  if (num_sms) *num_sms = eng->num_sms;
+  if (tile_c128) *tile_c128 = eng->tile_c128;
+  if (tile_c64) *tile_c64 = eng->tile_c64;
+  return HS_OK;
+}
+
+int hs_program_create(hs_engine* eng, int n_local, int dtype, const hs_part* parts, int num_parts,
+                      const hs_gate* gates, int num_gates, hs_program** out) {
+  if (!eng || !out) return fail(HS_ERR_INVALID, "engine/out is NULL");
+  *out = nullptr;
+  if (int s = check_dtype(dtype)) return s;
+  if (num_parts < 0 || (num_parts > 0 && !parts)) return fail(HS_ERR_INVALID, "bad part array");
+  std::unique_ptr<hs_program> prog(new (std::nothrow) hs_program);
+  if (!prog) return fail(HS_ERR_CAPACITY, "out of host memory");
+  prog->eng = eng;
+  prog->n_local = n_local;
+  prog->dtype = dtype;
+  prog->plans.resize(num_parts);
+  size_t total = 0;
+  for (int i = 0; i < num_parts; ++i) {
+    const hs_part& p = parts[i];
+    if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates)
+      return fail(HS_ERR_INVALID, "part " + std::to_string(i) + ": gate window outside the gate array");
+    std::string err;
+    int s = plan_part(n_local, dtype, tile_for(eng, dtype), p.staged, p.num_staged, gates + p.gate_offset,
+                      p.num_gates, prog->plans[i], err);
+    if (s != HS_OK) return fail(s, "part " + std::to_string(i) + ": " + err);
+    prog->plans[i].launch.prog_offset = (int64_t)total;
+    total += prog->plans[i].prog.size();
+  }
+  if (total) {
+    HS_CUDA(cudaSetDevice(eng->device), "cudaSetDevice");
+    std::vector<Instr> all;
+    all.reserve(total);
+    for (auto& pl : prog->plans) all.insert(all.end(), pl.prog.begin(), pl.prog.end());
+    HS_CUDA(cudaMalloc(&prog->d_prog, total * sizeof(Instr)), "cudaMalloc program");
+    HS_CUDA(cudaMemcpy(prog->d_prog, all.data(), total * sizeof(Instr), cudaMemcpyHostToDevice),
+            "cudaMemcpy program");
+  }
+  *out = prog.release();
+  return HS_OK;
+}
+
+int hs_program_destroy(hs_program* prog) {
+  if (!prog) return HS_OK;
+  cudaSetDevice(prog->eng->device);
+  if (prog->graph) cudaGraphExecDestroy(prog->graph);
+  if (prog->d_prog) cudaFree(prog->d_prog);
+  delete prog;
+  return HS_OK;
+}
+
+int hs_program_num_parts(hs_program* prog) { return prog ? (int)prog->plans.size() : -1; }
+
+int hs_program_part_info(hs_program* prog, int part, hs_part_info* out) {
+  if (!prog || !out) return fail(HS_ERR_INVALID, "program/out is NULL");
+  if (part < 0 || part >= (int)prog->plans.size()) return fail(HS_ERR_INVALID, "part index out of range");
+  *out = prog->plans[part].info;
+  return HS_OK;
+}
+
+int hs_program_dump(hs_program* prog, int part, void* buf, size_t buf_bytes, int* count,
+                    size_t* instr_bytes) {
+  if (!prog) return fail(HS_ERR_INVALID, "program is NULL");
+  if (part < 0 || part >= (int)prog->plans.size()) return fail(HS_ERR_INVALID, "part index out of range");
+  const PartPlan& pl = prog->plans[part];
+  if (count) *count = (int)pl.prog.size();
+  if (instr_bytes) *instr_bytes = sizeof(Instr);
+  // layout: PartLaunch header followed by the instructions
+  const size_t need = sizeof(PartLaunch) + pl.prog.size() * sizeof(Instr);
+  if (!buf) return HS_OK;
+  if (buf_bytes < need) return fail(HS_ERR_INVALID, "dump buffer too small");
+  std::memcpy(buf, &pl.launch, sizeof(PartLaunch));
+  std::memcpy((char*)buf + sizeof(PartLaunch), pl.prog.data(), pl.prog.size() * sizeof(Instr));
+  return HS_OK;
+}
+
+static int run_range(hs_program* prog, void* state, int64_t batch, int first, int count, cudaStream_t s) {
+  hs_engine* eng = prog->eng;
+  for (int i = first; i < first + count; ++i) {
+    const PartPlan& pl = prog->plans[i];
+    HS_CUDA(launch_part(prog->dtype, pl.launch, prog->d_prog, state, prog->n_local, batch, eng->num_sms, s),
+            "part kernel launch");
+  }
+  return HS_OK;
+}
+
+int hs_program_run(hs_program* prog, void* state, int64_t batch, int first, int count, void* stream) {
+  if (!prog || !state) return fail(HS_ERR_INVALID, "program/state is NULL");
+  if (batch < 1) return fail(HS_ERR_INVALID, "batch must be >= 1");
+  if (first < 0 || count < 0 || first + count > (int)prog->plans.size())
+    return fail(HS_ERR_INVALID, "part range outside the program");
+  HS_CUDA(cudaSetDevice(prog->eng->device), "cudaSetDevice");
+  return run_range(prog, state, batch, first, count, (cudaStream_t)stream);
+}
+
+int hs_program_run_graph(hs_program* prog, void* state, int64_t batch, void* stream) {
+  if (!prog || !state) return fail(HS_ERR_INVALID, "program/state is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  HS_CUDA(cudaSetDevice(prog->eng->device), "cudaSetDevice");
+  if (prog->graph && (prog->graph_state != state || prog->graph_batch != batch)) {
+    cudaGraphExecDestroy(prog->graph);
+    prog->graph = nullptr;
+  }
+  if (!prog->graph) {
+    cudaStream_t cap = s;
+    bool own = false;
+    if (!cap) {  // cannot capture the legacy stream
+      HS_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "cudaStreamCreate");
+      own = true;
+    }
+    HS_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+    int st = run_range(prog, state, batch, 0, (int)prog->plans.size(), cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap, &g);
+    if (st != HS_OK) { if (g) cudaGraphDestroy(g); if (own) cudaStreamDestroy(cap); return st; }
+    if (e != cudaSuccess) { if (own) cudaStreamDestroy(cap); return cuda_fail(e, "end capture"); }
+    e = cudaGraphInstantiate(&prog->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (own) cudaStreamDestroy(cap);
+    if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+    prog->graph_state = state;
+    prog->graph_batch = batch;
+  }
+  HS_CUDA(cudaGraphLaunch(prog->graph, s), "graph launch");
+  return HS_OK;
+}
+
+int hs_plan_part(int n_local, int dtype, int tile_bits, const int32_t* staged, int w, const hs_gate* gates,
+                 int num_gates, void* buf, size_t buf_bytes, size_t* bytes, hs_part_info* info) {
+  if (int s = check_dtype(dtype)) return s;
+  if (num_gates < 0 || (num_gates > 0 && !gates) || (w > 0 && !staged)) return fail(HS_ERR_INVALID, "bad arrays");
+  if (tile_bits < 1 || tile_bits > MAX_TILE) return fail(HS_ERR_INVALID, "tile_bits outside [1, 13]");
+  PartPlan plan;
+  std::string err;
+  int s = plan_part(n_local, dtype, tile_bits, staged, w, gates, num_gates, plan, err);
+  if (s != HS_OK) return fail(s, err);
+  const size_t need = sizeof(PartLaunch) + plan.prog.size() * sizeof(Instr);
+  if (bytes) *bytes = need;
+  if (info) *info = plan.info;
+  if (!buf) return HS_OK;
+  if (buf_bytes < need) return fail(HS_ERR_INVALID, "plan buffer too small");
+  plan.launch.prog_offset = 0;
+  std::memcpy(buf, &plan.launch, sizeof(PartLaunch));
+  std::memcpy((char*)buf + sizeof(PartLaunch), plan.prog.data(), plan.prog.size() * sizeof(Instr));
+  return HS_OK;
+}
+
+int hs_part_apply(hs_engine* eng, void* state, int64_t batch, int n_local, int dtype, const int32_t* staged,
+                  int w, const hs_gate* gates, int num_gates, void* stream) {
+  if (!eng || !state) return fail(HS_ERR_INVALID, "engine/state is NULL");
+  hs_part part;
+  std::memset(&part, 0, sizeof(part));
+  if (w < 0 || w > HS_MAX_STAGED) return fail(HS_ERR_INVALID, "staged count outside [0, 24]");
+  part.num_staged = w;
+  for (int j = 0; j < w; ++j) part.staged[j] = staged[j];
+  part.gate_offset = 0;
+  part.num_gates = num_gates;
+  hs_program* prog = nullptr;
+  int s = hs_program_create(eng, n_local, dtype, &part, 1, gates, num_gates, &prog);
+  if (s != HS_OK) return s;
+  s = hs_program_run(prog, state, batch, 0, 1, stream);
+  if (s == HS_OK) {
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) s = cuda_fail(e, "stream sync");
+  }
+  hs_program_destroy(prog);
+  return s;
+}
+
+int hs_state_init_basis(void* state, int64_t num_amps, int dtype, int64_t index, void* stream) {
+  if (!state) return fail(HS_ERR_INVALID, "state is NULL");
+  if (int s = check_dtype(dtype)) return s;
+  if (index < 0 || index >= num_amps) return fail(HS_ERR_INVALID, "basis index outside the state");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t amp = dtype == HS_C128 ? 16 : 8;
+  HS_CUDA(cudaMemsetAsync(state, 0, amp * (size_t)num_amps, s), "cudaMemsetAsync");
+  HS_CUDA(launch_set_basis(state, dtype, index, s), "set basis");
+  return HS_OK;
+}
+
+static int sms_of_current() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+int hs_bit_permute(const void* in, void* out, int num_bits, int dtype, const int32_t* dst_of, void* stream) {
+  if (!in || !out || !dst_of) return fail(HS_ERR_INVALID, "NULL argument");
+  if (in == out) return fail(HS_ERR_INVALID, "hs_bit_permute is out-of-place");
+  if (int s = check_dtype(dtype)) return s;
+  if (num_bits < 0 || num_bits > 40) return fail(HS_ERR_INVALID, "num_bits outside [0, 40]");
+  uint64_t seen = 0;
+  for (int b = 0; b < num_bits; ++b) {
+    if (dst_of[b] < 0 || dst_of[b] >= num_bits || (seen >> dst_of[b] & 1))
+      return fail(HS_ERR_INVALID, "dst_of is not a permutation");
+    seen |= 1ull << dst_of[b];
+  }
+  HS_CUDA(launch_bit_permute(in, out, num_bits, dtype, dst_of, sms_of_current(), (cudaStream_t)stream),
+          "bit permute");
+  return HS_OK;
+}
+
+static int segments(bool pack, const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos,
+                    int nseg, void* stream) {
+  if (!src || !dst || (nseg && !seg_pos)) return fail(HS_ERR_INVALID, "NULL argument");
+  if (src == dst) return fail(HS_ERR_INVALID, "pack/unpack are out-of-place");
+  if (int s = check_dtype(dtype)) return s;
+  if (nseg < 0 || nseg > 8 || num_bits < nseg || num_bits > 40)
+    return fail(HS_ERR_INVALID, "segment bits outside range");
+  for (int k = 0; k < nseg; ++k) {
+    if (seg_pos[k] < 0 || seg_pos[k] >= num_bits) return fail(HS_ERR_INVALID, "segment position outside state");
+    if (k && seg_pos[k] <= seg_pos[k - 1]) return fail(HS_ERR_INVALID, "segment positions not ascending");
+  }
+  HS_CUDA(launch_segments(pack, src, dst, num_bits, dtype, seg_pos, nseg, sms_of_current(), (cudaStream_t)stream),
+          "segment kernel");
+  return HS_OK;
+}
+
+int hs_pack_segments(const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos, int nseg,
+                     void* stream) {
+  return segments(true, src, dst, num_bits, dtype, seg_pos, nseg, stream);
+}
+
+int hs_unpack_segments(const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos, int nseg,
+                       void* stream) {
+  return segments(false, src, dst, num_bits, dtype, seg_pos, nseg, stream);
+}
+
+int hs_max_abs_diff(const void* a, int dtype, const void* b_c128, int64_t n, double* host_result, void* stream) {
+  if (!a || !b_c128 || !host_result) return fail(HS_ERR_INVALID, "NULL argument");
+  if (int s = check_dtype(dtype)) return s;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* d = nullptr;
+  HS_CUDA(cudaMallocAsync((void**)&d, sizeof(unsigned long long), s), "cudaMallocAsync");
+  HS_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s), "memset");
+  if (n > 0) HS_CUDA(launch_maxdiff(a, dtype, b_c128, n, d, sms_of_current(), s), "maxdiff");
+  unsigned long long bits = 0;
+  HS_CUDA(cudaMemcpyAsync(&bits, d, sizeof(bits), cudaMemcpyDeviceToHost, s), "memcpy");
+  HS_CUDA(cudaFreeAsync(d, s), "cudaFreeAsync");
+  HS_CUDA(cudaStreamSynchronize(s), "sync");
+  double r;
+  std::memcpy(&r, &bits, sizeof(r));
+  *host_result = r;
+  return HS_OK;
+}
+
+}  // extern "C"

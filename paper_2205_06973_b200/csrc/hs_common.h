@@ -1,0 +1,68 @@
+// Internal definitions shared by the planner (host C++) and the part kernels.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hisvsim.h"
+
+namespace hs {
+
+// Device instruction opcodes of a part program.
+enum : uint16_t {
+  I_PHASE = 1,  // write registers back (previous map), barrier, load with a new map
+  I_DENSE = 2,  // 2x2 on register bit k, predicated on controls
+  I_PERM = 3,   // X-type exchange on register bit k, predicated on controls
+  I_DIAG = 4,   // diag(d0, d1) on a target bit (register k or tid-mask), predicated
+};
+
+// DIAG flags
+enum : uint8_t { F_D0_ONE = 1, F_D1_ONE = 2, F_SIGN = 4 };
+
+constexpr uint8_t K_NONE = 0xFF;
+constexpr int MAX_RB = 4;       // register bits per thread
+constexpr int MAX_TILE = 13;    // tile bits the kernels support
+constexpr int MAX_NPOS = 12;    // non-register tile bits (T - RB)
+
+// One device instruction, 96 bytes. Location bits are positions inside the
+// CTA tile (0..T-1) in the current storage labelling.
+struct alignas(16) Instr {
+  uint16_t op;
+  uint8_t k;       // register index of the target (DENSE/PERM/DIAG) or K_NONE
+  uint8_t flags;
+  uint32_t creg;   // controls that are register bits: mask over register index
+  uint32_t ctid;   // controls that are thread bits: mask over tile location bits
+  uint32_t qtid;   // DIAG target as a tile-location mask when not a register bit
+  uint8_t rpos[MAX_RB];    // PHASE: location of register bit k
+  uint8_t npos[MAX_NPOS];  // PHASE: location of thread-index bit m
+  double m[8];     // DENSE: m00 m01 m10 m11 (re, im); DIAG: d0, d1
+};
+static_assert(sizeof(Instr) == 96, "Instr layout");
+
+// Everything a part launch needs besides the instruction array.
+struct PartLaunch {
+  int64_t prog_offset;  // into the program's device instruction buffer
+  int32_t nprog;
+  int32_t T;            // tile bits
+  int32_t RB;           // register bits
+  int32_t fin_sync;     // barrier needed before the final store
+  uint8_t tpos[16];     // ascending physical positions of the tile
+  uint8_t fin_rpos[MAX_RB];
+  uint8_t fin_npos[MAX_NPOS];
+};
+
+struct PartPlan {
+  PartLaunch launch;
+  std::vector<Instr> prog;
+  hs_part_info info;
+};
+
+// Plan one part. Returns HS_OK or an error code with `err` filled.
+int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w,
+              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err);
+
+// 2x2 base matrix of a gate kind (controls handled by masking), row-major
+// complex: m[0..7] = m00 re/im, m01, m10, m11. Mirrors statevec.py:33-98.
+bool base_matrix(int kind, const double* params, double m[8]);
+
+}  // namespace hs

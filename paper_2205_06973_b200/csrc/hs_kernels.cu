@@ -1,0 +1,477 @@
+// sm_100a kernels of the part-pass engine.
+//
+// hs_part_kernel: one pass of a part over the state (hisim.hier.run_part,
+// hier.py:220-244, with statevec.apply_op per gate, statevec.py:172-261).
+// A persistent grid walks CTA tiles; a tile is every amplitude whose free
+// (non-tile) bits spell one value. Per tile:
+//   1. cp.async 16/8-byte loads of the 2^T amplitudes into shared memory
+//      (tile bits ascending, so the low tile bits give contiguous runs),
+//   2. the part program: PHASE instructions move amplitudes between shared
+//      memory and registers (each thread then owns 2^RB amplitudes whose
+//      register bits are the phase's targets); DENSE/PERM/DIAG instructions
+//      update registers in place,
+//   3. the last phase's registers go back to shared memory in natural tile
+//      order (undoing SWAP relabels), then coalesced stores to HBM.
+// Shared memory slots are XOR-swizzled so phase exchanges are conflict-free.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hs_common.h"
+
+namespace hs {
+
+template <typename R> struct Cx;
+template <> struct Cx<double> { using T = double2; };
+template <> struct Cx<float> { using T = float2; };
+
+// XOR swizzle (linear over GF(2)): fold the higher index bits into the bits
+// that select the 16B (c128) / 8B (c64) bank group inside a 128B row
+template <typename R> __device__ __forceinline__ uint32_t swz(uint32_t s);
+template <> __device__ __forceinline__ uint32_t swz<double>(uint32_t s) {
+  return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9) ^ (s >> 12)) & 7u);
+}
+template <> __device__ __forceinline__ uint32_t swz<float>(uint32_t s) {
+  return s ^ (((s >> 4) ^ (s >> 8) ^ (s >> 12)) & 15u);
+}
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+struct KParams {
+  void* psi;
+  const Instr* prog;
+  int64_t ntiles;      // batch * 2^(n_local - T)
+  int32_t nprog;
+  int32_t n_local;
+  int32_t T;
+  int32_t fin_sync;
+  uint8_t tpos[16];
+  uint8_t fin_rpos[MAX_RB];
+  uint8_t fin_npos[MAX_NPOS];
+};
+
+// address offset of tile index 0 of tile `t`: insert zero bits at the tile
+// positions of the low (n_local - T) bits, rows above n_local
+__device__ __forceinline__ uint64_t tile_base(uint64_t t, const KParams& p) {
+  const int fb = p.n_local - p.T;
+  uint64_t row = t >> fb;
+  uint64_t f = t & ((uint64_t(1) << fb) - 1);
+  for (int b = 0; b < p.T; ++b) {
+    uint64_t lo = f & ((uint64_t(1) << p.tpos[b]) - 1);
+    f = ((f ^ lo) << 1) | lo;
+  }
+  return (row << p.n_local) | f;
+}
+
+__device__ __forceinline__ uint32_t deposit(uint32_t x, const uint8_t* pos, int cnt) {
+  uint32_t r = 0;
+  for (int m = 0; m < cnt; ++m) r |= ((x >> m) & 1u) << pos[m];
+  return r;
+}
+
+template <typename C, typename R>
+__device__ __forceinline__ C cmul(C a, R br, R bi) {
+  C r;
+  r.x = fma(a.x, br, -a.y * bi);
+  r.y = fma(a.x, bi, a.y * br);
+  return r;
+}
+
+// ---- register-bit gate bodies (K compile-time so registers stay registers)
+
+template <typename R, int RB, int K>
+__device__ __forceinline__ void dense_k(typename Cx<R>::T* a, const R* m, uint32_t creg) {
+#pragma unroll
+  for (int i = 0; i < (1 << RB); ++i) {
+    if (i & (1 << K)) continue;
+    if ((uint32_t(i) & creg) != creg) continue;
+    const int j = i | (1 << K);
+    typename Cx<R>::T x = a[i], y = a[j], u, v;
+    u.x = fma(m[0], x.x, fma(-m[1], x.y, fma(m[2], y.x, -m[3] * y.y)));
+    u.y = fma(m[0], x.y, fma(m[1], x.x, fma(m[2], y.y, m[3] * y.x)));
+    v.x = fma(m[4], x.x, fma(-m[5], x.y, fma(m[6], y.x, -m[7] * y.y)));
+    v.y = fma(m[4], x.y, fma(m[5], x.x, fma(m[6], y.y, m[7] * y.x)));
+    a[i] = u;
+    a[j] = v;
+  }
+}
+
+template <typename R, int RB, int K>
+__device__ __forceinline__ void perm_k(typename Cx<R>::T* a, uint32_t creg) {
+#pragma unroll
+  for (int i = 0; i < (1 << RB); ++i) {
+    if (i & (1 << K)) continue;
+    if ((uint32_t(i) & creg) != creg) continue;
+    const int j = i | (1 << K);
+    typename Cx<R>::T t = a[i];
+    a[i] = a[j];
+    a[j] = t;
+  }
+}
+
+template <typename R, int RB, int K>
+__device__ __forceinline__ void diag_k(typename Cx<R>::T* a, const R* d, uint32_t creg, int flags) {
+#pragma unroll
+  for (int i = 0; i < (1 << RB); ++i) {
+    if ((uint32_t(i) & creg) != creg) continue;
+    if (i & (1 << K)) {
+      if (flags & F_SIGN) { a[i].x = -a[i].x; a[i].y = -a[i].y; }
+      else if (!(flags & F_D1_ONE)) a[i] = cmul(a[i], d[2], d[3]);
+    } else {
+      if (!(flags & F_D0_ONE)) a[i] = cmul(a[i], d[0], d[1]);
+    }
+  }
+}
+
+template <typename R, int RB>
+__device__ __forceinline__ void diag_uniform(typename Cx<R>::T* a, R dr, R di, uint32_t creg) {
+#pragma unroll
+  for (int i = 0; i < (1 << RB); ++i) {
+    if ((uint32_t(i) & creg) != creg) continue;
+    a[i] = cmul(a[i], dr, di);
+  }
+}
+
+template <typename R, int RB>
+__device__ __forceinline__ void negate_uniform(typename Cx<R>::T* a, uint32_t creg) {
+#pragma unroll
+  for (int i = 0; i < (1 << RB); ++i) {
+    if ((uint32_t(i) & creg) != creg) continue;
+    a[i].x = -a[i].x;
+    a[i].y = -a[i].y;
+  }
+}
+
+template <typename R, int RB>
+__device__ __forceinline__ void exec_instr(typename Cx<R>::T* a, const Instr& in, uint32_t tdep) {
+  if ((tdep & in.ctid) != in.ctid) return;  // a thread-bit control is 0 for all my amplitudes
+  R m[8];
+  if (in.op == I_DENSE) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) m[q] = (R)in.m[q];
+    switch (in.k) {
+      case 0: dense_k<R, RB, 0>(a, m, in.creg); break;
+      case 1: if (RB > 1) dense_k<R, RB, (RB > 1 ? 1 : 0)>(a, m, in.creg); break;
+      case 2: if (RB > 2) dense_k<R, RB, (RB > 2 ? 2 : 0)>(a, m, in.creg); break;
+      case 3: if (RB > 3) dense_k<R, RB, (RB > 3 ? 3 : 0)>(a, m, in.creg); break;
+    }
+  } else if (in.op == I_PERM) {
+    switch (in.k) {
+      case 0: perm_k<R, RB, 0>(a, in.creg); break;
+      case 1: if (RB > 1) perm_k<R, RB, (RB > 1 ? 1 : 0)>(a, in.creg); break;
+      case 2: if (RB > 2) perm_k<R, RB, (RB > 2 ? 2 : 0)>(a, in.creg); break;
+      case 3: if (RB > 3) perm_k<R, RB, (RB > 3 ? 3 : 0)>(a, in.creg); break;
+    }
+  } else {  // I_DIAG
+#pragma unroll
+    for (int q = 0; q < 4; ++q) m[q] = (R)in.m[q];
+    if (in.k == K_NONE) {
+      const bool one = (tdep & in.qtid) != 0;
+      if (one) {
+        if (in.flags & F_SIGN) negate_uniform<R, RB>(a, in.creg);
+        else if (!(in.flags & F_D1_ONE)) diag_uniform<R, RB>(a, m[2], m[3], in.creg);
+      } else if (!(in.flags & F_D0_ONE)) {
+        diag_uniform<R, RB>(a, m[0], m[1], in.creg);
+      }
+      return;
+    }
+    switch (in.k) {
+      case 0: diag_k<R, RB, 0>(a, m, in.creg, in.flags); break;
+      case 1: if (RB > 1) diag_k<R, RB, (RB > 1 ? 1 : 0)>(a, m, in.creg, in.flags); break;
+      case 2: if (RB > 2) diag_k<R, RB, (RB > 2 ? 2 : 0)>(a, m, in.creg, in.flags); break;
+      case 3: if (RB > 3) diag_k<R, RB, (RB > 3 ? 3 : 0)>(a, m, in.creg, in.flags); break;
+    }
+  }
+}
+
+// slot of register i given the phase's swizzled thread base and per-bit
+// swizzled register contributions (swizzle is linear, bits are disjoint)
+template <int RB>
+__device__ __forceinline__ uint32_t reg_slot(uint32_t st, const uint32_t* ub, int i) {
+  uint32_t s = st;
+#pragma unroll
+  for (int k = 0; k < RB; ++k)
+    if (i & (1 << k)) s ^= ub[k];
+  return s;
+}
+
+template <typename R, int RB>
+__device__ __forceinline__ void phase_map(const uint8_t* rpos, const uint8_t* npos, int T,
+                                          uint32_t& tdep, uint32_t& st, uint32_t* ub) {
+  tdep = deposit(threadIdx.x, npos, T - RB);
+  st = swz<R>(tdep);
+#pragma unroll
+  for (int k = 0; k < RB; ++k) ub[k] = swz<R>(1u << rpos[k]);
+}
+
+template <typename R, int RB>
+__global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512, 2)
+hs_part_kernel(const KParams p) {
+  using C = typename Cx<R>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* sm = reinterpret_cast<C*>(smem_raw);
+  C* psi = reinterpret_cast<C*>(p.psi);
+  const uint32_t tid = threadIdx.x;
+  const int T = p.T;
+  const int lowbits = T - RB;  // thread bits of the canonical load order
+  // global offset of tile index s = tid + (j << lowbits)
+  uint64_t ga_tid = 0;
+  for (int b = 0; b < lowbits; ++b) ga_tid |= uint64_t((tid >> b) & 1u) << p.tpos[b];
+  uint64_t ga_hi[RB];
+#pragma unroll
+  for (int k = 0; k < RB; ++k) ga_hi[k] = uint64_t(1) << p.tpos[lowbits + k];
+
+  for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    const uint64_t base = tile_base((uint64_t)t, p) | ga_tid;
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+      uint64_t off = base;
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (j & (1 << k)) off |= ga_hi[k];
+      const uint32_t s = tid + (uint32_t(j) << lowbits);
+      cp_async(&sm[swz<R>(s)], &psi[off], sizeof(C));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    C a[1 << RB];
+    uint32_t tdep = 0, st = 0, ub[RB];
+    bool loaded = false;
+    for (int pc = 0; pc < p.nprog; ++pc) {
+      const Instr& in = p.prog[pc];
+      if (in.op == I_PHASE) {
+        if (loaded) {
+#pragma unroll
+          for (int i = 0; i < (1 << RB); ++i) sm[reg_slot<RB>(st, ub, i)] = a[i];
+          __syncthreads();
+        }
+        phase_map<R, RB>(in.rpos, in.npos, T, tdep, st, ub);
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) a[i] = sm[reg_slot<RB>(st, ub, i)];
+        loaded = true;
+      } else {
+        exec_instr<R, RB>(a, in, tdep);
+      }
+    }
+    if (p.fin_sync) __syncthreads();
+    phase_map<R, RB>(p.fin_rpos, p.fin_npos, T, tdep, st, ub);
+#pragma unroll
+    for (int i = 0; i < (1 << RB); ++i) sm[reg_slot<RB>(st, ub, i)] = a[i];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+      uint64_t off = base;
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (j & (1 << k)) off |= ga_hi[k];
+      const uint32_t s = tid + (uint32_t(j) << lowbits);
+      psi[off] = sm[swz<R>(s)];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+
+struct KernelSlot {
+  const void* fn;
+  int max_blocks_per_sm[MAX_TILE + 1];
+};
+
+template <typename R, int RB>
+static const void* kfn() { return reinterpret_cast<const void*>(&hs_part_kernel<R, RB>); }
+
+static const void* kernel_for(int dtype, int RB) {
+  if (dtype == HS_C128) {
+    switch (RB) {
+      case 1: return kfn<double, 1>();
+      case 2: return kfn<double, 2>();
+      case 3: return kfn<double, 3>();
+      default: return kfn<double, 4>();
+    }
+  }
+  switch (RB) {
+    case 1: return kfn<float, 1>();
+    case 2: return kfn<float, 2>();
+    case 3: return kfn<float, 3>();
+    default: return kfn<float, 4>();
+  }
+}
+
+cudaError_t prepare_kernels(int smem_optin) {
+  for (int dt = 0; dt < 2; ++dt)
+    for (int rb = 1; rb <= MAX_RB; ++rb) {
+      cudaError_t e = cudaFuncSetAttribute(kernel_for(dt, rb),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
+}
+
+cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void* psi,
+                        int n_local, int64_t batch, int num_sms, cudaStream_t stream) {
+  KParams p;
+  p.psi = psi;
+  p.prog = dprog + L.prog_offset;
+  p.nprog = L.nprog;
+  p.n_local = n_local;
+  p.T = L.T;
+  p.fin_sync = L.fin_sync;
+  p.ntiles = batch << (n_local - L.T);
+  for (int b = 0; b < 16; ++b) p.tpos[b] = L.tpos[b];
+  for (int k = 0; k < MAX_RB; ++k) p.fin_rpos[k] = L.fin_rpos[k];
+  for (int m = 0; m < MAX_NPOS; ++m) p.fin_npos[m] = L.fin_npos[m];
+  const size_t amp = (dtype == HS_C128) ? 16 : 8;
+  const size_t smem = amp << L.T;
+  const int threads = 1 << (L.T - L.RB);
+  const void* fn = kernel_for(dtype, L.RB);
+  int per_sm = 1;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > p.ntiles) grid = p.ntiles;
+  void* args[] = {&p};
+  return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(threads), args, smem, stream);
+}
+
+// ------------------------------------------------------------ utility kernels
+
+__global__ void set_basis_kernel(void* psi, int dtype, int64_t index) {
+  if (dtype == HS_C128) reinterpret_cast<double2*>(psi)[index] = make_double2(1.0, 0.0);
+  else reinterpret_cast<float2*>(psi)[index] = make_float2(1.0f, 0.0f);
+}
+
+cudaError_t launch_set_basis(void* psi, int dtype, int64_t index, cudaStream_t s) {
+  set_basis_kernel<<<1, 1, 0, s>>>(psi, dtype, index);
+  return cudaGetLastError();
+}
+
+struct PermParams {
+  int8_t dst_of[48];
+  int32_t nbits;
+};
+
+template <typename C>
+__global__ void bit_permute_kernel(const C* __restrict__ in, C* __restrict__ out, PermParams p) {
+  const uint64_t n = uint64_t(1) << p.nbits;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t o = 0;
+    for (int b = 0; b < p.nbits; ++b) o |= ((i >> b) & 1ull) << p.dst_of[b];
+    out[o] = in[i];
+  }
+}
+
+cudaError_t launch_bit_permute(const void* in, void* out, int nbits, int dtype, const int32_t* dst_of,
+                               int num_sms, cudaStream_t s) {
+  PermParams p;
+  p.nbits = nbits;
+  for (int b = 0; b < nbits; ++b) p.dst_of[b] = (int8_t)dst_of[b];
+  const uint64_t n = uint64_t(1) << nbits;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
+  if (dtype == HS_C128)
+    bit_permute_kernel<double2><<<(unsigned)blocks, 256, 0, s>>>((const double2*)in, (double2*)out, p);
+  else
+    bit_permute_kernel<float2><<<(unsigned)blocks, 256, 0, s>>>((const float2*)in, (float2*)out, p);
+  return cudaGetLastError();
+}
+
+// segment pack: amplitude i goes to segment seg(i) (its bits at seg_pos),
+// at inner index = the other bits of i compressed, ascending
+struct SegParams {
+  int8_t seg_pos[8];
+  int32_t nseg;
+  int32_t nbits;
+};
+
+__device__ __forceinline__ void seg_split(uint64_t i, const SegParams& p, uint64_t& seg, uint64_t& inner) {
+  seg = 0;
+  inner = i;
+  // remove seg bits from the highest position down so lower ones stay valid
+  for (int k = p.nseg - 1; k >= 0; --k) {
+    int q = p.seg_pos[k];
+    seg |= ((i >> q) & 1ull) << k;
+    uint64_t lo = inner & ((1ull << q) - 1);
+    inner = ((inner >> (q + 1)) << q) | lo;
+  }
+}
+
+template <typename C, bool PACK>
+__global__ void seg_kernel(const C* __restrict__ in, C* __restrict__ out, SegParams p) {
+  const uint64_t n = uint64_t(1) << p.nbits;
+  const int inner_bits = p.nbits - p.nseg;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t seg, inner;
+    seg_split(i, p, seg, inner);
+    const uint64_t packed = (seg << inner_bits) | inner;
+    if (PACK) out[packed] = in[i];
+    else out[i] = in[packed];
+  }
+}
+
+cudaError_t launch_segments(bool pack, const void* in, void* out, int nbits, int dtype,
+                            const int32_t* seg_pos, int nseg, int num_sms, cudaStream_t s) {
+  SegParams p;
+  p.nbits = nbits;
+  p.nseg = nseg;
+  for (int k = 0; k < nseg; ++k) p.seg_pos[k] = (int8_t)seg_pos[k];
+  const uint64_t n = uint64_t(1) << nbits;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
+  if (dtype == HS_C128) {
+    if (pack) seg_kernel<double2, true><<<(unsigned)blocks, 256, 0, s>>>((const double2*)in, (double2*)out, p);
+    else seg_kernel<double2, false><<<(unsigned)blocks, 256, 0, s>>>((const double2*)in, (double2*)out, p);
+  } else {
+    if (pack) seg_kernel<float2, true><<<(unsigned)blocks, 256, 0, s>>>((const float2*)in, (float2*)out, p);
+    else seg_kernel<float2, false><<<(unsigned)blocks, 256, 0, s>>>((const float2*)in, (float2*)out, p);
+  }
+  return cudaGetLastError();
+}
+
+// max |a - b|: non-negative doubles order like their bit patterns
+template <typename C>
+__global__ void maxdiff_kernel(const C* __restrict__ a, const double2* __restrict__ b, int64_t n,
+                               unsigned long long* result) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double dx = (double)a[i].x - b[i].x, dy = (double)a[i].y - b[i].y;
+    double d = sqrt(dx * dx + dy * dy);
+    if (!(d <= m)) m = d;  // NaN propagates as "bigger"
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    double other = __shfl_xor_sync(0xffffffffu, m, o);
+    if (!(other <= m)) m = other;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long bits = (m != m) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(m);
+    atomicMax(result, bits);
+  }
+}
+
+cudaError_t launch_maxdiff(const void* a, int dtype, const void* b, int64_t n,
+                           unsigned long long* dres, int num_sms, cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  if (blocks < 1) blocks = 1;
+  if (dtype == HS_C128)
+    maxdiff_kernel<double2><<<(unsigned)blocks, 256, 0, s>>>((const double2*)a, (const double2*)b, n, dres);
+  else
+    maxdiff_kernel<float2><<<(unsigned)blocks, 256, 0, s>>>((const float2*)a, (const double2*)b, n, dres);
+  return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,329 @@
+// Part planner: turns one part (staged positions + gates in slot
+// coordinates, i.e. hisim.hier.ExecutablePart, hier.py:159-217) into a
+// device program for the part kernel.
+//
+// The CTA tile is the part's staged positions plus the lowest other
+// positions ("ride-along" bits, processed as extra fixings) up to the tile
+// width, so small parts still read long contiguous runs. Inside a tile the
+// gates run out of registers: each thread owns 2^RB amplitudes whose index
+// bits (the "register bits") change from phase to phase through a shared
+// memory exchange. A phase is a maximal group of gates, reordered only across
+// commuting gates, whose non-diagonal targets fit the phase's register bits.
+// Diagonal gates and controls never need a register bit: a thread knows the
+// value of every other tile bit of its amplitudes. SWAP costs nothing: it
+// relabels where two qubits live and the final store writes the tile back in
+// natural order.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "hs_common.h"
+
+namespace hs {
+
+bool base_matrix(int kind, const double* p, double m[8]) {
+  const double r2 = 1.0 / std::sqrt(2.0);
+  auto set = [&](double a, double b, double c, double d, double e, double f, double g,
+                 double h) {
+    m[0] = a; m[1] = b; m[2] = c; m[3] = d; m[4] = e; m[5] = f; m[6] = g; m[7] = h;
+  };
+  switch (kind) {
+    case HS_H: set(r2, 0, r2, 0, r2, 0, -r2, 0); return true;
+    case HS_X: case HS_CX: case HS_CCX: set(0, 0, 1, 0, 1, 0, 0, 0); return true;
+    case HS_Y: set(0, 0, 0, -1, 0, 1, 0, 0); return true;
+    case HS_Z: case HS_CZ: set(1, 0, 0, 0, 0, 0, -1, 0); return true;
+    case HS_S: set(1, 0, 0, 0, 0, 0, 0, 1); return true;
+    case HS_SDG: set(1, 0, 0, 0, 0, 0, 0, -1); return true;
+    case HS_T: set(1, 0, 0, 0, 0, 0, std::cos(0.25 * M_PI), std::sin(0.25 * M_PI)); return true;
+    case HS_TDG: set(1, 0, 0, 0, 0, 0, std::cos(0.25 * M_PI), -std::sin(0.25 * M_PI)); return true;
+    case HS_RX: {
+      double c = std::cos(p[0] / 2), s = std::sin(p[0] / 2);
+      set(c, 0, 0, -s, 0, -s, c, 0);
+      return true;
+    }
+    case HS_RY: case HS_CRY: {
+      double c = std::cos(p[0] / 2), s = std::sin(p[0] / 2);
+      set(c, 0, -s, 0, s, 0, c, 0);
+      return true;
+    }
+    case HS_RZ: case HS_CRZ:
+      set(std::cos(-0.5 * p[0]), std::sin(-0.5 * p[0]), 0, 0, 0, 0, std::cos(0.5 * p[0]),
+          std::sin(0.5 * p[0]));
+      return true;
+    case HS_U1: set(1, 0, 0, 0, 0, 0, std::cos(p[0]), std::sin(p[0])); return true;
+    case HS_U3: {
+      double c = std::cos(p[0] / 2), s = std::sin(p[0] / 2);
+      double phi = p[1], lam = p[2];
+      set(c, 0, -std::cos(lam) * s, -std::sin(lam) * s, std::cos(phi) * s, std::sin(phi) * s,
+          std::cos(phi + lam) * c, std::sin(phi + lam) * c);
+      return true;
+    }
+    default: return false;
+  }
+}
+
+namespace {
+
+enum Cls { C_DENSE, C_PERM, C_DIAG, C_SWAP };
+
+int arity_of(int kind) {
+  switch (kind) {
+    case HS_CX: case HS_CZ: case HS_CRZ: case HS_CRY: case HS_SWAP: return 2;
+    case HS_CCX: return 3;
+    default: return (kind >= 0 && kind < HS_NUM_KINDS) ? 1 : -1;
+  }
+}
+
+struct Gate {
+  Cls cls;
+  int tgt;      // tile-logical bit (SWAP: first operand)
+  int other;    // SWAP: second operand
+  int ctl[2];
+  int nctl;
+  double m[8];
+  uint32_t nd;  // tile-logical bits touched non-diagonally
+  uint32_t d;   // tile-logical bits touched diagonally (controls, diag targets)
+};
+
+struct Rec {  // a scheduled gate, in locations
+  Cls cls;
+  int tloc;
+  int cloc[2];
+  int nctl;
+  const double* m;
+};
+
+int choose_npos(const std::vector<int>& nonreg, int dtype, uint8_t* npos) {
+  // lanes (thread bits 0..4) should cover every residue class of the shared
+  // memory swizzle so a phase load is bank-conflict free
+  const int mod = (dtype == HS_C128) ? 3 : 4;
+  std::vector<int> order, rest;
+  std::vector<bool> used(nonreg.size(), false);
+  for (int c = 0; c < mod; ++c)
+    for (size_t i = 0; i < nonreg.size(); ++i)
+      if (!used[i] && nonreg[i] % mod == c) { order.push_back(nonreg[i]); used[i] = true; break; }
+  for (size_t i = 0; i < nonreg.size(); ++i)
+    if (!used[i]) rest.push_back(nonreg[i]);
+  // the lowest remaining bits fill the rest of the lanes, then the warp bits
+  std::vector<int> all = order;
+  all.insert(all.end(), rest.begin(), rest.end());
+  for (size_t i = 0; i < all.size(); ++i) npos[i] = (uint8_t)all[i];
+  return (int)all.size();
+}
+
+double paper_flops(const Rec& r) {
+  // dense 2x2 = 14 FLOPs per amplitude, diag with two
+  // non-unit entries 6, one non-unit 3, sign/permutation 0; controls scale by
+  // the fraction of amplitudes touched
+  double f = 0;
+  if (r.cls == C_DENSE) f = 14;
+  if (r.cls == C_DIAG) {
+    bool d0one = r.m[0] == 1.0 && r.m[1] == 0.0;
+    bool d1one = r.m[6] == 1.0 && r.m[7] == 0.0;
+    bool sign = d0one && r.m[6] == -1.0 && r.m[7] == 0.0;
+    f = sign ? 0 : (d0one || d1one) ? 3 : 6;
+  }
+  return f / double(1 << r.nctl);
+}
+
+}  // namespace
+
+int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w,
+              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err) {
+  if (n_local < 1 || n_local > 62) { err = "n_local outside [1, 62]"; return HS_ERR_INVALID; }
+  if (w < 0 || w > HS_MAX_STAGED) { err = "staged count outside [0, 24]"; return HS_ERR_INVALID; }
+  for (int j = 0; j < w; ++j) {
+    if (staged[j] < 0 || staged[j] >= n_local) {
+      err = "position " + std::to_string(staged[j]) + " outside 0.." + std::to_string(n_local - 1);
+      return HS_ERR_INVALID;
+    }
+    if (j && staged[j] <= staged[j - 1]) { err = "staged positions not strictly ascending"; return HS_ERR_INVALID; }
+  }
+  const int T = std::min(std::max(tile_max, w), n_local);
+  if (T > tile_max) {
+    err = "part stages " + std::to_string(w) + " qubits; the on-chip tile holds " +
+          std::to_string(tile_max);
+    return HS_ERR_TOO_WIDE;
+  }
+  if (T > MAX_TILE) { err = "tile wider than the kernels support"; return HS_ERR_TOO_WIDE; }
+  const int RB = std::min(MAX_RB, T);
+
+  // tile = staged positions + lowest free positions
+  std::vector<int> tile(staged, staged + w);
+  for (int p = 0; (int)tile.size() < T && p < n_local; ++p)
+    if (std::find(staged, staged + w, p) == staged + w) tile.push_back(p);
+  std::sort(tile.begin(), tile.end());
+  std::vector<int> tl(w);
+  for (int j = 0; j < w; ++j) tl[j] = int(std::find(tile.begin(), tile.end(), staged[j]) - tile.begin());
+
+  // classify gates
+  std::vector<Gate> gs(num_gates);
+  for (int g = 0; g < num_gates; ++g) {
+    const hs_gate& in = gates[g];
+    int ar = arity_of(in.kind);
+    if (ar < 0) { err = "unknown gate kind " + std::to_string(in.kind); return HS_ERR_UNSUPPORTED; }
+    if (in.num_slots != ar) { err = "gate " + std::to_string(g) + ": wrong operand count"; return HS_ERR_INVALID; }
+    int bits[3];
+    for (int a = 0; a < ar; ++a) {
+      int s = in.slots[a];
+      if (s < 0 || s >= w) { err = "gate " + std::to_string(g) + ": slot outside the part"; return HS_ERR_INVALID; }
+      bits[a] = tl[s];
+      for (int b = 0; b < a; ++b)
+        if (bits[b] == bits[a]) { err = "gate " + std::to_string(g) + ": repeated slot"; return HS_ERR_INVALID; }
+    }
+    Gate& G = gs[g];
+    G.nctl = 0;
+    if (in.kind == HS_SWAP) {
+      G.cls = C_SWAP; G.tgt = bits[0]; G.other = bits[1];
+      G.nd = (1u << bits[0]) | (1u << bits[1]); G.d = 0;
+      continue;
+    }
+    base_matrix(in.kind, in.params, G.m);
+    G.nctl = ar - 1;
+    for (int a = 0; a < G.nctl; ++a) G.ctl[a] = bits[a];
+    G.tgt = bits[ar - 1];
+    const double* m = G.m;
+    bool diag = m[2] == 0 && m[3] == 0 && m[4] == 0 && m[5] == 0;
+    bool perm = !diag && m[0] == 0 && m[1] == 0 && m[6] == 0 && m[7] == 0 && m[2] == 1 &&
+                m[3] == 0 && m[4] == 1 && m[5] == 0;
+    G.cls = diag ? C_DIAG : perm ? C_PERM : C_DENSE;
+    uint32_t cm = 0;
+    for (int a = 0; a < G.nctl; ++a) cm |= 1u << G.ctl[a];
+    if (G.cls == C_DIAG) { G.nd = 0; G.d = cm | (1u << G.tgt); }
+    else { G.nd = 1u << G.tgt; G.d = cm; }
+  }
+
+  // storage labelling: loc_of[tile bit] / bit_at[location]
+  std::vector<int> loc_of(T), bit_at(T);
+  for (int b = 0; b < T; ++b) loc_of[b] = bit_at[b] = b;
+
+  PartPlan& P = out;
+  P.prog.clear();
+  std::memset(&P.info, 0, sizeof(P.info));
+  std::vector<char> done(num_gates, 0);
+  int remaining = num_gates;
+  std::vector<int> R;
+  double flops = 0;
+  int phases = 0;
+  while (remaining > 0) {
+    R.clear();
+    std::vector<Rec> recs;
+    for (;;) {
+      bool progress = false;
+      uint32_t blk_nd = 0, blk_d = 0;
+      for (int g = 0; g < num_gates; ++g) {
+        if (done[g]) continue;
+        Gate& G = gs[g];
+        if ((G.nd & (blk_nd | blk_d)) || (G.d & blk_nd)) { blk_nd |= G.nd; blk_d |= G.d; continue; }
+        bool ok = false;
+        if (G.cls == C_DIAG || G.cls == C_SWAP) ok = true;
+        else {
+          int L = loc_of[G.tgt];
+          if (std::find(R.begin(), R.end(), L) != R.end()) ok = true;
+          else if ((int)R.size() < RB) { R.push_back(L); ok = true; }
+        }
+        if (!ok) { blk_nd |= G.nd; blk_d |= G.d; continue; }
+        if (G.cls == C_SWAP) {
+          int a = G.tgt, b = G.other;
+          std::swap(loc_of[a], loc_of[b]);
+          bit_at[loc_of[a]] = a;
+          bit_at[loc_of[b]] = b;
+          P.info.swaps_relabelled++;
+        } else {
+          Rec r{G.cls, loc_of[G.tgt], {0, 0}, G.nctl, G.m};
+          for (int a = 0; a < G.nctl; ++a) r.cloc[a] = loc_of[G.ctl[a]];
+          recs.push_back(r);
+        }
+        done[g] = 1;
+        --remaining;
+        progress = true;
+      }
+      if (!progress) break;
+    }
+    if (recs.empty()) continue;  // only relabels
+    for (int L = 0; (int)R.size() < RB; ++L)
+      if (std::find(R.begin(), R.end(), L) == R.end()) R.push_back(L);
+    Instr ph;
+    std::memset(&ph, 0, sizeof(ph));
+    ph.op = I_PHASE;
+    ph.k = K_NONE;
+    std::vector<int> nonreg;
+    for (int L = 0; L < T; ++L)
+      if (std::find(R.begin(), R.end(), L) == R.end()) nonreg.push_back(L);
+    for (int k = 0; k < RB; ++k) ph.rpos[k] = (uint8_t)R[k];
+    choose_npos(nonreg, dtype, ph.npos);
+    P.prog.push_back(ph);
+    ++phases;
+    auto reg_of = [&](int L) -> int {
+      for (int k = 0; k < RB; ++k) if (R[k] == L) return k;
+      return -1;
+    };
+    for (const Rec& r : recs) {
+      Instr in;
+      std::memset(&in, 0, sizeof(in));
+      in.k = K_NONE;
+      for (int a = 0; a < r.nctl; ++a) {
+        int k = reg_of(r.cloc[a]);
+        if (k >= 0) in.creg |= 1u << k; else in.ctid |= 1u << r.cloc[a];
+      }
+      int k = reg_of(r.tloc);
+      if (r.cls == C_DIAG) {
+        in.op = I_DIAG;
+        if (k >= 0) in.k = (uint8_t)k; else in.qtid = 1u << r.tloc;
+        in.m[0] = r.m[0]; in.m[1] = r.m[1]; in.m[2] = r.m[6]; in.m[3] = r.m[7];
+        bool d0one = r.m[0] == 1.0 && r.m[1] == 0.0;
+        bool d1one = r.m[6] == 1.0 && r.m[7] == 0.0;
+        if (d0one) in.flags |= F_D0_ONE;
+        if (d1one) in.flags |= F_D1_ONE;
+        if (d0one && r.m[6] == -1.0 && r.m[7] == 0.0) in.flags |= F_SIGN;
+        P.info.diag_gates++;
+      } else {
+        in.op = (r.cls == C_PERM) ? I_PERM : I_DENSE;
+        in.k = (uint8_t)k;  // target is a register bit by construction
+        std::memcpy(in.m, r.m, sizeof(in.m));
+        if (r.cls == C_PERM) P.info.perm_gates++; else P.info.dense_gates++;
+      }
+      flops += paper_flops(r);
+      P.prog.push_back(in);
+    }
+  }
+  if (phases == 0) {  // no arithmetic at all (empty part or SWAPs only)
+    Instr ph;
+    std::memset(&ph, 0, sizeof(ph));
+    ph.op = I_PHASE;
+    ph.k = K_NONE;
+    std::vector<int> nonreg;
+    for (int L = RB; L < T; ++L) nonreg.push_back(L);
+    for (int k = 0; k < RB; ++k) ph.rpos[k] = (uint8_t)k;
+    choose_npos(nonreg, dtype, ph.npos);
+    P.prog.push_back(ph);
+    phases = 1;
+  }
+  // final store: register k holds location R[k] of the last phase, which is
+  // tile bit bit_at[R[k]]; write it to that bit's natural position
+  const Instr* last = nullptr;
+  for (const Instr& in : P.prog) if (in.op == I_PHASE) last = &in;
+  PartLaunch& L = P.launch;
+  std::memset(&L, 0, sizeof(L));
+  L.nprog = (int32_t)P.prog.size();
+  L.T = T;
+  L.RB = RB;
+  for (int b = 0; b < T; ++b) L.tpos[b] = (uint8_t)tile[b];
+  bool ident = true;
+  for (int b = 0; b < T; ++b) ident &= (loc_of[b] == b);
+  L.fin_sync = ident ? 0 : 1;
+  for (int k = 0; k < RB; ++k) L.fin_rpos[k] = (uint8_t)bit_at[last->rpos[k]];
+  for (int m = 0; m < T - RB; ++m) L.fin_npos[m] = (uint8_t)bit_at[last->npos[m]];
+
+  hs_part_info& I = P.info;
+  I.tile_bits = T;
+  for (int b = 0; b < T; ++b) I.tile_pos[b] = tile[b];
+  I.reg_bits = RB;
+  I.phases = phases;
+  I.instructions = (int)P.prog.size();
+  I.tiles = int64_t(1) << (n_local - T);
+  I.fp_ops_per_amp = flops;
+  return HS_OK;
+}
+
+}  // namespace hs

@@ -1,0 +1,120 @@
+"""Numpy emulator of the part-kernel instruction stream (test helper).
+
+Decodes what ``hs_plan_part`` emits (PartLaunch header + Instr array, see
+paper_2205_06973_b200/csrc/hs_common.h) and executes it with the kernel's
+semantics, so the planner (gate scheduling into register phases, SWAP
+relabelling, control/diagonal resolution, final write map) can be checked
+against the oracle on a CPU-only machine. Shared-memory swizzling is a
+bijection on slots and is not modelled.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+I_PHASE, I_DENSE, I_PERM, I_DIAG = 1, 2, 3, 4
+F_D0_ONE, F_D1_ONE, F_SIGN = 1, 2, 4
+K_NONE = 0xFF
+
+LAUNCH = np.dtype([("prog_offset", "<i8"), ("nprog", "<i4"), ("T", "<i4"), ("RB", "<i4"), ("fin_sync", "<i4"),
+                   ("tpos", "u1", 16), ("fin_rpos", "u1", 4), ("fin_npos", "u1", 12)])
+INSTR = np.dtype([("op", "<u2"), ("k", "u1"), ("flags", "u1"), ("creg", "<u4"), ("ctid", "<u4"), ("qtid", "<u4"),
+                  ("rpos", "u1", 4), ("npos", "u1", 12), ("m", "<f8", 8)])
+assert LAUNCH.itemsize == 56 and INSTR.itemsize == 96
+
+
+def plan(native, n_local, dtype, tile_bits, staged, ops, op_slots):
+    """Call hs_plan_part; returns (launch record, instr array, info)."""
+    from paper_2205_06973_b200.hier import ExecutablePart, QubitSlotMap, _pack
+
+    exe = ExecutablePart(0, (), QubitSlotMap(tuple(staged)), tuple(ops), tuple(op_slots))
+    _, gates, total = _pack([exe])
+    lib = native.load()
+    st = (ctypes.c_int32 * max(1, len(staged)))(*staged)
+    size = ctypes.c_size_t()
+    info = native.HsPartInfo()
+    native.check(lib.hs_plan_part(n_local, dtype, tile_bits, st, len(staged), gates, total, None, 0,
+                                  ctypes.byref(size), ctypes.byref(info)))
+    buf = ctypes.create_string_buffer(size.value)
+    native.check(lib.hs_plan_part(n_local, dtype, tile_bits, st, len(staged), gates, total, buf, size.value,
+                                  ctypes.byref(size), ctypes.byref(info)))
+    raw = buf.raw
+    launch = np.frombuffer(raw[:LAUNCH.itemsize], dtype=LAUNCH)[0]
+    prog = np.frombuffer(raw[LAUNCH.itemsize:], dtype=INSTR)
+    return launch, prog, info
+
+
+def _deposit(x: np.ndarray, pos) -> np.ndarray:
+    out = np.zeros_like(x)
+    for m, p in enumerate(pos):
+        out |= ((x >> m) & 1) << int(p)
+    return out
+
+
+def emulate(psi: np.ndarray, n_local: int, launch, prog) -> None:
+    """Run one planned part in place on ``psi`` (rows x 2^n_local)."""
+    T, RB = int(launch["T"]), int(launch["RB"])
+    tpos = [int(x) for x in launch["tpos"][:T]]
+    flat = psi.reshape(-1)
+    rows = flat.size >> n_local
+    free = [q for q in range(n_local) if q not in tpos]
+    nt = 1 << (T - RB)
+    # gather tiles: tile index = (row, free fixing), slot s over tile bits
+    fix = np.arange(1 << len(free), dtype=np.int64)
+    base_f = _deposit(fix, free)
+    bases = (np.arange(rows, dtype=np.int64)[:, None] << n_local | base_f[None, :]).reshape(-1)
+    slots = np.arange(1 << T, dtype=np.int64)
+    ga = _deposit(slots, tpos)
+    smem = flat[bases[:, None] + ga[None, :]].copy()  # (tiles, 2^T)
+    tid = np.arange(nt, dtype=np.int64)
+    regs = None
+    cur = None
+
+    def slot_of(rpos, npos):
+        tdep = _deposit(tid, npos[: T - RB])
+        return tdep, [tdep | _deposit(np.array([i]), rpos[:RB])[0] for i in range(1 << RB)]
+
+    for ins in prog:
+        op = int(ins["op"])
+        if op == I_PHASE:
+            if regs is not None:
+                for i, s in enumerate(cur[1]):
+                    smem[:, s] = regs[i]
+            cur = slot_of([int(x) for x in ins["rpos"]], [int(x) for x in ins["npos"]])
+            regs = [smem[:, s].copy() for s in cur[1]]
+            continue
+        tdep = cur[0]
+        tok = (tdep & int(ins["ctid"])) == int(ins["ctid"])  # per thread
+        creg = int(ins["creg"])
+        m = ins["m"]
+        k = int(ins["k"])
+        if op in (I_DENSE, I_PERM):
+            u = [complex(m[0], m[1]), complex(m[2], m[3]), complex(m[4], m[5]), complex(m[6], m[7])]
+            for i in range(1 << RB):
+                if i & (1 << k) or (i & creg) != creg:
+                    continue
+                j = i | (1 << k)
+                a, b = regs[i], regs[j]
+                if op == I_PERM:
+                    na, nb = b, a
+                else:
+                    na, nb = u[0] * a + u[1] * b, u[2] * a + u[3] * b
+                regs[i] = np.where(tok[None, :], na, a)
+                regs[j] = np.where(tok[None, :], nb, b)
+        else:
+            d0, d1 = complex(m[0], m[1]), complex(m[2], m[3])
+            for i in range(1 << RB):
+                if (i & creg) != creg:
+                    continue
+                if k == K_NONE:
+                    one = (tdep & int(ins["qtid"])) != 0
+                else:
+                    one = np.full(nt, bool(i & (1 << k)))
+                f = np.where(one, d1, d0)
+                regs[i] = np.where(tok[None, :], regs[i] * f[None, :], regs[i])
+    fin = slot_of([int(x) for x in launch["fin_rpos"]], [int(x) for x in launch["fin_npos"]])
+    for i, s in enumerate(fin[1]):
+        smem[:, s] = regs[i]
+    flat[bases[:, None] + ga[None, :]] = smem

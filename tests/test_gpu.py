@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle
+and the reference's golden vectors. Tolerances are the north star's:
+max-abs 1e-10 for complex128, 1e-4 for complex64."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import parts_of, partition_of  # noqa: E402
+from oracle import c_oracle  # noqa: E402
+from oracle import hisim_oracle as orc  # noqa: E402
+from paper_2205_06973_b200 import (  # noqa: E402
+    _native,
+    build_dag,
+    configs,
+    execute_hierarchical,
+    execute_multilevel,
+    partition_dagp,
+    partition_dfs,
+    partition_multilevel,
+    partition_nat,
+    simulate_distributed,
+)
+from paper_2205_06973_b200.errors import PartTooWideForLayoutError  # noqa: E402
+from paper_2205_06973_b200.hier import HierarchicalRun, max_abs_diff, remap_part, run_part  # noqa: E402
+from paper_2205_06973_b200.qasm import GateKind, GateOp, parse_qasm  # noqa: E402
+from paper_2205_06973_b200.statevec import apply_gate, from_numpy, simulate_flat  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"complex128": 1e-10, "complex64": 1e-4}
+
+
+def _dev_err(state, ref):
+    return float(np.max(np.abs(state.to_numpy() - ref)))
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_corpus_every_partition_matches_reference(golden, dtype):
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    worst = 0.0
+    for i, doc in enumerate(docs):
+        c = parse_qasm(doc["qasm"])
+        for key, parts in doc["partitions"].items():
+            st = execute_hierarchical(c, partition_of(parts), dtype=dtype)
+            worst = max(worst, _dev_err(st, states[f"c{i}"]))
+    assert worst < TOL[dtype], worst
+
+
+def test_bundled_multilevel_and_traces(golden):
+    docs, states = golden.json("bundled"), golden.npz("bundled")
+    for name, doc in docs.items():
+        c = parse_qasm(doc["qasm"])
+        d = build_dag(c)
+        for strategy, parts in doc["partitions"].items():
+            st = execute_hierarchical(c, partition_of(parts))
+            assert _dev_err(st, states[name]) < 1e-10, (name, strategy)
+        _, tr = execute_hierarchical(c, partition_nat(d, doc["limit"]), with_trace=True)
+        assert tr.part_rows() == doc["nat_trace"]
+        if "multilevel" in doc:
+            ml = doc["multilevel"]
+            part = partition_multilevel(d, ml["limit1"], ml["limit2"])
+            st, tr = execute_multilevel(c, part, with_trace=True)
+            assert _dev_err(st, states[name]) < 1e-10
+            assert tr.part_rows() == ml["trace"]
+
+
+def test_flat_and_single_gates(golden):
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    for i, doc in enumerate(docs[:20]):
+        c = parse_qasm(doc["qasm"])
+        assert _dev_err(simulate_flat(c, max_qubits=c.num_qubits), states[f"c{i}"]) < 1e-10
+    # apply_gate on a random state, every gate kind, vs the oracle
+    rng = np.random.default_rng(3)
+    n = 7
+    raw = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    for kind in GateKind:
+        qubits = tuple(int(x) for x in rng.choice(n, kind.arity, replace=False))
+        op = GateOp(kind, qubits, tuple(float(x) for x in rng.uniform(-3, 3, kind.num_params)))
+        sv = from_numpy(raw)
+        apply_gate(sv, op)
+        want = raw.copy()
+        orc.apply_op(want, n, op)
+        assert _dev_err(sv, want) < 1e-12, kind
+
+
+def test_run_part_api_numpy_torch_and_batches():
+    c = configs.build("c2@12")
+    part = partition_dfs(build_dag(c), 9).parts[1]
+    exe = remap_part(c, part)
+    rng = np.random.default_rng(0)
+    data = rng.normal(size=(4, 1 << 12)) + 1j * rng.normal(size=(4, 1 << 12))
+    want = data.copy()
+    orc.run_part(want, exe.slot_map.qubits, exe.ops, exe.op_slots)
+    host = data.copy()
+    run_part(host, exe)  # numpy in, numpy out (copied through the device)
+    assert np.max(np.abs(host - want)) < 1e-12
+    dev = torch.from_numpy(data.copy()).cuda()
+    run_part(dev, exe)
+    assert np.max(np.abs(dev.cpu().numpy() - want)) < 1e-12
+    with pytest.raises(ValueError):
+        run_part(torch.zeros(3, dtype=torch.complex128, device="cuda"), exe)
+
+
+def _sample(golden, name, st):
+    arr = golden.npz("configs")
+    key = name.replace("@", "_")
+    idx, amp = arr[key + "_idx"], arr[key + "_amp"]
+    got = st.data[torch.as_tensor(idx, device=st.data.device)].cpu().numpy()
+    return float(np.max(np.abs(got - amp)))
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_config1_qft_full_state_closed_form(golden, dtype):
+    """c1 at full size: sampled reference amplitudes, and every one of the
+    2^20 amplitudes against the closed-form QFT of the prepared basis state."""
+    c = configs.build("c1")
+    for strategy in ("nat", "dfs", "dagp"):
+        part = {"nat": partition_nat, "dfs": partition_dfs, "dagp": partition_dagp}[strategy](build_dag(c), 10)
+        st = execute_hierarchical(c, part, dtype=dtype)
+        assert _sample(golden, "c1", st) < TOL[dtype]
+        x = configs.qft_prefix_index(20, 0)
+        ks = np.arange(1 << 20)
+        rev = np.zeros_like(ks)
+        for b in range(20):
+            rev |= ((ks >> b) & 1) << (19 - b)
+        rx = int(sum(((x >> b) & 1) << (19 - b) for b in range(20)))
+        closed = np.exp(2j * np.pi * ((rx * rev) % (1 << 20)) / (1 << 20)) / 1024.0
+        assert max_abs_diff(st, closed) < TOL[dtype]
+
+
+@pytest.mark.parametrize("name", ["c2@20", "c3@20", "c4@small18"])
+def test_scaled_configs_match_reference_samples(golden, name):
+    doc = golden.json("configs")[name + ":sample"]
+    c = configs.ising_config(18, 4) if name == "c4@small18" else configs.build(name)
+    st = execute_hierarchical(c, partition_of(doc["partition"]))
+    assert _sample(golden, name, st) < 1e-10
+    assert abs(st.norm() - doc["norm"]) < 1e-10
+
+
+@pytest.mark.parametrize("name,strategy", [("c2", "dfs"), ("c2", "dagp"), ("c3@26", "dfs")])
+def test_full_size_configs_match_c_oracle(golden, name, strategy):
+    """26-qubit runs against the multi-threaded C oracle (same partition)."""
+    c = configs.build(name)
+    d = build_dag(c)
+    part = (partition_dfs if strategy == "dfs" else partition_dagp)(d, 12)
+    st = execute_hierarchical(c, part)
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert max_abs_diff(st, ref) < 1e-10
+
+
+def test_distributed_emulated_ranks_match_reference(golden):
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    for i, doc in enumerate(docs):
+        c = parse_qasm(doc["qasm"])
+        for d in doc["dist"]:
+            run = simulate_distributed(c, partition_of(d["parts"]), d["p"])
+            assert _dev_err(run.state, states[f"c{i}"]) < 1e-10
+            assert [[list(l.local), list(l.process)] for l in run.layouts] == d["layouts"]
+            assert [s.bytes_remote for s in run.stats.switches] == [s["bytes_remote"] for s in d["switches"]]
+
+
+def test_distributed_c1_at_three_rank_bits(golden):
+    c = configs.build("c1")
+    part = partition_dagp(build_dag(c), 10)
+    run = simulate_distributed(c, part, 3)
+    assert _sample(golden, "c1", run.state) < 1e-10
+
+
+def test_program_reuse_graph_and_initial_state():
+    c = configs.build("c2@16")
+    part = partition_dfs(build_dag(c), 10)
+    run = HierarchicalRun(c, part)
+    rng = np.random.default_rng(9)
+    raw = rng.normal(size=1 << 16) + 1j * rng.normal(size=1 << 16)
+    raw /= np.linalg.norm(raw)
+    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts], initial=raw)
+    a = from_numpy(raw)
+    run.program.run(a.data)
+    b = from_numpy(raw)
+    run.program.run_graph(b.data)
+    run.program.run_graph(b.data)  # replay: applies the circuit twice
+    twice = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts], initial=want)
+    assert _dev_err(a, want) < 1e-10
+    assert _dev_err(b, twice) < 1e-10
+
+
+def test_layout_kernels_round_trip():
+    import ctypes
+
+    lib = _native.load()
+    n = 14
+    x = torch.randn(1 << n, dtype=torch.complex128, device="cuda")
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    perm = list(range(n))
+    np.random.default_rng(2).shuffle(perm)
+    inv = [perm.index(b) for b in range(n)]
+    s = torch.cuda.current_stream().cuda_stream
+    _native.check(lib.hs_bit_permute(x.data_ptr(), y.data_ptr(), n, 0, (ctypes.c_int32 * n)(*perm), s))
+    _native.check(lib.hs_bit_permute(y.data_ptr(), z.data_ptr(), n, 0, (ctypes.c_int32 * n)(*inv), s))
+    assert torch.equal(x, z)
+    idx = torch.arange(1 << n, device="cuda")
+    moved = torch.zeros(1 << n, dtype=torch.long, device="cuda")
+    dst = torch.zeros_like(idx)
+    for b in range(n):
+        dst |= ((idx >> b) & 1) << perm[b]
+    assert torch.equal(y[dst], x)
+    seg = (ctypes.c_int32 * 3)(2, 5, 11)
+    _native.check(lib.hs_pack_segments(x.data_ptr(), y.data_ptr(), n, 0, seg, 3, s))
+    _native.check(lib.hs_unpack_segments(y.data_ptr(), z.data_ptr(), n, 0, seg, 3, s))
+    assert torch.equal(x, z)
+    del moved
+
+
+def test_errors_surface_as_reference_exceptions():
+    from paper_2205_06973_b200.qasm import Circuit
+
+    c = Circuit(16, tuple(GateOp(GateKind.H, (q,)) for q in range(16)))
+    part = partition_of([(list(range(16)), list(range(16)))], limit=16)
+    with pytest.raises(PartTooWideForLayoutError):
+        execute_hierarchical(c, part)

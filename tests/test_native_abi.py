@@ -1,0 +1,109 @@
+"""The C ABI library without a GPU: it loads, exports every symbol the
+header declares, and its host-side planner produces device programs whose
+emulated execution matches the oracle."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import program_emulator as emu
+from conftest import parts_of
+from oracle import hisim_oracle as orc
+from paper_2205_06973_b200 import _native, build_dag, configs, partition_dfs
+from paper_2205_06973_b200.errors import PartTooWideForLayoutError
+from paper_2205_06973_b200.hier import remap_part
+from paper_2205_06973_b200.qasm import Circuit, GateKind, GateOp, parse_qasm
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "hisvsim.h"
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = _native.load()
+    declared = set(re.findall(r"\b(hs_[a-z_0-9]+)\s*\(", HEADER.read_text()))
+    assert declared == set(_native.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.hs_abi_version() == 1
+
+
+def _emulate_parts(circuit, parts, tile_bits, dtype=0, rows=1, initial=None):
+    n = circuit.num_qubits
+    if initial is None:
+        psi = np.zeros((rows, 1 << n), dtype=np.complex128)
+        psi[:, 0] = 1.0
+    else:
+        psi = initial.copy()
+    for gates, qubits in parts:
+        from paper_2205_06973_b200.partition import Part
+
+        exe = remap_part(circuit, Part(0, tuple(gates), tuple(qubits)))
+        launch, prog, _ = emu.plan(_native, n, dtype, tile_bits, exe.slot_map.qubits, exe.ops, exe.op_slots)
+        emu.emulate(psi, n, launch, prog)
+    return psi
+
+
+@pytest.mark.parametrize("tile_bits", [12, 13, 6])
+def test_planned_programs_match_oracle_on_corpus(golden, tile_bits):
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    for i, doc in enumerate(docs[:40]):
+        c = parse_qasm(doc["qasm"])
+        for key, parts in doc["partitions"].items():
+            if max(len(q) for _, q in parts) > tile_bits:
+                continue
+            got = _emulate_parts(c, parts_of(parts), tile_bits)[0]
+            assert np.max(np.abs(got - states[f"c{i}"])) < 1e-12, (i, key)
+
+
+def test_planned_programs_with_batch_rows_and_random_state():
+    c = configs.build("c2@11")
+    part = partition_dfs(build_dag(c), 7)
+    rng = np.random.default_rng(4)
+    psi = rng.normal(size=(4, 1 << 11)) + 1j * rng.normal(size=(4, 1 << 11))
+    got = _emulate_parts(c, [(p.gate_indices, p.qubits) for p in part.parts], 12, rows=4, initial=psi)
+    want = psi.copy()
+    for p in part.parts:
+        orc.run_part(want, *orc.part_slots(c, p.gate_indices, p.qubits))
+    assert np.max(np.abs(got - want)) < 1e-12
+
+
+def test_swaps_are_relabelled_not_moved():
+    c = configs.build("c1@8")
+    ops = tuple(range(c.num_ops))
+    from paper_2205_06973_b200.partition import Part
+
+    exe = remap_part(c, Part(0, ops, tuple(range(8))))
+    launch, prog, info = emu.plan(_native, 8, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots)
+    assert info.swaps_relabelled == 4
+    assert launch["fin_sync"] == 1
+    psi = np.zeros((1, 256), dtype=np.complex128)
+    psi[0, 0] = 1
+    emu.emulate(psi, 8, launch, prog)
+    assert np.max(np.abs(psi[0] - orc.simulate_flat(c))) < 1e-12
+
+
+def test_planner_rejects_bad_parts():
+    c = Circuit(14, tuple(GateOp(GateKind.H, (q,)) for q in range(14)))
+    from paper_2205_06973_b200.partition import Part
+
+    exe = remap_part(c, Part(0, tuple(range(14)), tuple(range(14))))
+    with pytest.raises(PartTooWideForLayoutError):
+        emu.plan(_native, 14, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots)
+    with pytest.raises(ValueError):
+        emu.plan(_native, 4, 0, 12, (5,), (GateOp(GateKind.H, (0,)),), ((0,),))
+    with pytest.raises(ValueError):
+        emu.plan(_native, 4, 0, 12, (2, 1), (GateOp(GateKind.H, (0,)),), ((0,),))
+
+
+def test_plan_summary_counts():
+    c = configs.build("c3@12")
+    part = partition_dfs(build_dag(c), 10).parts[1]
+    exe = remap_part(c, part)
+    _, prog, info = emu.plan(_native, 12, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots)
+    kinds = [op.kind for op in exe.ops]
+    assert info.dense_gates == sum(k in (GateKind.H, GateKind.RX) for k in kinds)
+    assert info.perm_gates == kinds.count(GateKind.CX)
+    assert info.diag_gates == kinds.count(GateKind.RZ)
+    assert info.phases == sum(int(i["op"]) == emu.I_PHASE for i in prog)
+    assert info.tile_bits == 12 and info.reg_bits == 4
