@@ -143,7 +143,8 @@ def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup, quiet=False):
     n = circuit.num_qubits
     # calibrate: fixings per part so that one step takes ~target seconds
     target = args.cpu_step_seconds
-    psi = np.zeros(1 << n, dtype=np.complex128)
+    psi = np.empty(1 << n, dtype=np.complex128)
+    psi.fill(0)  # fault the pages in before timing anything
     psi[0] = 1.0
     slots = [c_oracle.part_slots(circuit, p.gate_indices, p.qubits) for p in part.parts]
     def make_plan(frac):
@@ -157,6 +158,7 @@ def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup, quiet=False):
         return time.perf_counter() - t0
 
     frac = 1e-4
+    timed(make_plan(frac))
     while True:  # grow the sample until a pass is long enough to time
         dt = timed(make_plan(frac))
         if dt > 0.25 or frac >= 1.0:

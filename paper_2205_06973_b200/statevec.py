@@ -22,11 +22,13 @@ import numpy as np
 from .errors import DeviceError, QubitCountOutOfRangeError
 from .qasm import Circuit, GateKind, GateOp
 
-#: default materialization cap of the reference (statevec.py:26-29); on the
-#: device the real limit is free HBM, checked at allocation
-DEFAULT_MAX_QUBITS = 24
-#: the reference refuses n > 30 (16 GiB); a B200 holds 33 qubits of c128
+#: The reference caps host materialization at 24 qubits unless
+#: HISIM_MAX_QUBITS raises it (statevec.py:26-29) to stop accidental 16 GiB
+#: numpy allocations. On the device the binding limit is free HBM, checked
+#: in ``allocate``; the default cap is therefore the hard ceiling, and the
+#: env var / ``max_qubits`` argument still lower it like in the reference.
 HARD_MAX_QUBITS = 36
+DEFAULT_MAX_QUBITS = HARD_MAX_QUBITS
 
 _R2 = 1.0 / math.sqrt(2.0)
 
