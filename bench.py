@@ -209,6 +209,10 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
+    if args.plan_options is not None:
+        from paper_2205_06973_b200 import _native
+
+        _native.set_options(dev.index, args.plan_options)
     n = circuit.num_qubits
     dist = world > 1
     if dist:
@@ -324,6 +328,8 @@ def main(argv=None):
     ap.add_argument("--cpu-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--plan-options", type=int, default=None,
+                    help="planner option bits (HS_PLAN_*; default: the engine default)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -95,7 +95,14 @@ typedef struct {
   int32_t dense_gates, perm_gates, diag_gates, swaps_relabelled;
   int64_t tiles;          /* CTA tiles per launch = batch * 2^(n_local - T) */
   double fp_ops_per_amp;  /* diagnostic real FLOPs per amplitude */
+  int32_t input_gates;    /* gates before single-qubit fusion */
+  int32_t reserved;
 } hs_part_info;
+
+/* planner options (hs_engine_set_options / hs_plan_part) */
+#define HS_PLAN_FUSE_1Q 0x1u /* merge runs of uncontrolled 1-qubit gates per qubit */
+#define HS_PLAN_RB3 0x2u     /* 3 register bits per thread instead of 4 */
+#define HS_PLAN_DEFAULT HS_PLAN_FUSE_1Q
 
 typedef struct hs_engine hs_engine;
 typedef struct hs_program hs_program;
@@ -108,6 +115,8 @@ int hs_engine_create(int device, hs_engine** out);
 int hs_engine_destroy(hs_engine* eng);
 /* SMs and the max tile bits per dtype chosen for this device */
 int hs_engine_query(hs_engine* eng, int* num_sms, int* tile_bits_c128, int* tile_bits_c64);
+/* planner options for programs created afterwards (HS_PLAN_* bits) */
+int hs_engine_set_options(hs_engine* eng, uint32_t options);
 
 /* plan + upload a whole part sequence for buffers of batch x 2^n_local */
 int hs_program_create(hs_engine* eng, int n_local, int dtype,
@@ -131,7 +140,7 @@ int hs_program_run_graph(hs_program* prog, void* state, int64_t batch, void* str
 /* host-only planning of one part (no CUDA call; usable without a GPU):
  * writes the PartLaunch header + device instructions into buf (NULL to
  * query *bytes), and the plan summary into *info */
-int hs_plan_part(int n_local, int dtype, int tile_bits, const int32_t* staged, int w,
+int hs_plan_part(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
                  const hs_gate* gates, int num_gates, void* buf, size_t buf_bytes,
                  size_t* bytes, hs_part_info* info);
 

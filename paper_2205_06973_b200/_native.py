@@ -27,7 +27,7 @@ HS_MAX_STAGED = 24
 #: every symbol include/hisvsim.h declares (checked by the CPU test suite)
 EXPORTS = (
     "hs_last_error", "hs_abi_version", "hs_engine_create", "hs_engine_destroy",
-    "hs_engine_query", "hs_program_create", "hs_program_destroy",
+    "hs_engine_query", "hs_engine_set_options", "hs_program_create", "hs_program_destroy",
     "hs_program_num_parts", "hs_program_part_info", "hs_program_dump",
     "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_max_abs_diff",
@@ -67,6 +67,8 @@ class HsPartInfo(ctypes.Structure):
         ("swaps_relabelled", ctypes.c_int32),
         ("tiles", ctypes.c_int64),
         ("fp_ops_per_amp", ctypes.c_double),
+        ("input_gates", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -82,6 +84,7 @@ def _declare(lib) -> None:
         "hs_engine_create": (I, [I, ctypes.POINTER(P)]),
         "hs_engine_destroy": (I, [P]),
         "hs_engine_query": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I)]),
+        "hs_engine_set_options": (I, [P, ctypes.c_uint32]),
         "hs_program_create": (I, [P, I, I, ctypes.POINTER(HsPart), I,
                                   ctypes.POINTER(HsGate), I, ctypes.POINTER(P)]),
         "hs_program_destroy": (I, [P]),
@@ -91,7 +94,7 @@ def _declare(lib) -> None:
                                 ctypes.POINTER(ctypes.c_size_t)]),
         "hs_program_run": (I, [P, P, I64, I, I, P]),
         "hs_program_run_graph": (I, [P, P, I64, P]),
-        "hs_plan_part": (I, [I, I, I, ctypes.POINTER(ctypes.c_int32), I, ctypes.POINTER(HsGate), I,
+        "hs_plan_part": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int32), I, ctypes.POINTER(HsGate), I,
                              P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(HsPartInfo)]),
         "hs_part_apply": (I, [P, P, I64, I, I, ctypes.POINTER(ctypes.c_int32), I,
                               ctypes.POINTER(HsGate), I, P]),
@@ -164,3 +167,11 @@ def engine_query(device: int) -> dict:
     sms, t128, t64 = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     check(lib.hs_engine_query(engine(device), ctypes.byref(sms), ctypes.byref(t128), ctypes.byref(t64)))
     return {"num_sms": sms.value, "tile_bits_c128": t128.value, "tile_bits_c64": t64.value}
+
+
+HS_PLAN_FUSE_1Q, HS_PLAN_RB3 = 0x1, 0x2
+
+
+def set_options(device: int, options: int) -> None:
+    """Planner options (HS_PLAN_* bits) for programs created afterwards."""
+    check(load().hs_engine_set_options(engine(device), options))

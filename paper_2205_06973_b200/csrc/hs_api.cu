@@ -32,6 +32,7 @@ struct hs_engine {
   int smem_optin = 0;
   int tile_c128 = 12;
   int tile_c64 = 13;
+  uint32_t options = HS_PLAN_DEFAULT;
   unsigned long long* d_scratch = nullptr;  // reductions
 };
 
@@ -139,7 +140,7 @@ int hs_program_create(hs_engine* eng, int n_local, int dtype, const hs_part* par
     if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates)
       return fail(HS_ERR_INVALID, "part " + std::to_string(i) + ": gate window outside the gate array");
     std::string err;
-    int s = plan_part(n_local, dtype, tile_for(eng, dtype), p.staged, p.num_staged, gates + p.gate_offset,
+    int s = plan_part(n_local, dtype, tile_for(eng, dtype), eng->options, p.staged, p.num_staged, gates + p.gate_offset,
                       p.num_gates, prog->plans[i], err);
     if (s != HS_OK) return fail(s, "part " + std::to_string(i) + ": " + err);
     prog->plans[i].launch.prog_offset = (int64_t)total;
@@ -243,14 +244,21 @@ int hs_program_run_graph(hs_program* prog, void* state, int64_t batch, void* str
   return HS_OK;
 }
 
-int hs_plan_part(int n_local, int dtype, int tile_bits, const int32_t* staged, int w, const hs_gate* gates,
-                 int num_gates, void* buf, size_t buf_bytes, size_t* bytes, hs_part_info* info) {
+int hs_engine_set_options(hs_engine* eng, uint32_t options) {
+  if (!eng) return fail(HS_ERR_INVALID, "engine is NULL");
+  eng->options = options;
+  return HS_OK;
+}
+
+int hs_plan_part(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
+                 const hs_gate* gates, int num_gates, void* buf, size_t buf_bytes, size_t* bytes,
+                 hs_part_info* info) {
   if (int s = check_dtype(dtype)) return s;
   if (num_gates < 0 || (num_gates > 0 && !gates) || (w > 0 && !staged)) return fail(HS_ERR_INVALID, "bad arrays");
   if (tile_bits < 1 || tile_bits > MAX_TILE) return fail(HS_ERR_INVALID, "tile_bits outside [1, 13]");
   PartPlan plan;
   std::string err;
-  int s = plan_part(n_local, dtype, tile_bits, staged, w, gates, num_gates, plan, err);
+  int s = plan_part(n_local, dtype, tile_bits, options, staged, w, gates, num_gates, plan, err);
   if (s != HS_OK) return fail(s, err);
   const size_t need = sizeof(PartLaunch) + plan.prog.size() * sizeof(Instr);
   if (bytes) *bytes = need;

@@ -17,7 +17,7 @@ enum : uint16_t {
 };
 
 // DIAG flags
-enum : uint8_t { F_D0_ONE = 1, F_D1_ONE = 2, F_SIGN = 4 };
+enum : uint8_t { F_D0_ONE = 1, F_D1_ONE = 2, F_SIGN = 4, F_PLAIN = 8, F_REAL = 16 };
 
 constexpr uint8_t K_NONE = 0xFF;
 constexpr int MAX_RB = 4;       // register bits per thread
@@ -58,7 +58,7 @@ struct PartPlan {
 };
 
 // Plan one part. Returns HS_OK or an error code with `err` filled.
-int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w,
+int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int32_t* staged, int w,
               const hs_gate* gates, int num_gates, PartPlan& out, std::string& err);
 
 // 2x2 base matrix of a gate kind (controls handled by masking), row-major

@@ -46,6 +46,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// The running part's program lives in the constant bank when it fits: every
+// thread of a warp reads the same instruction, which the constant cache
+// broadcasts, and matrix entries can feed DFMA operands directly. The host
+// copies each part's instructions in (stream-ordered) right before its launch.
+constexpr int CPROG_MAX = 600;
+__constant__ Instr c_prog[CPROG_MAX];
+
 struct KParams {
   void* psi;
   const Instr* prog;
@@ -54,10 +61,16 @@ struct KParams {
   int32_t n_local;
   int32_t T;
   int32_t fin_sync;
-  uint8_t tpos[16];
-  uint8_t fin_rpos[MAX_RB];
-  uint8_t fin_npos[MAX_NPOS];
+  // byte arrays packed into words so runtime indexing never spills the
+  // parameter block to local memory: byte b of (w0, w1)
+  uint64_t tpos0, tpos1;    // tile positions, ascending
+  uint64_t fnpos0, fnpos1;  // final store: location of thread bit m
+  uint32_t frpos;           // final store: location of register bit k
 };
+
+__device__ __forceinline__ int byte_of(uint64_t w0, uint64_t w1, int b) {
+  return (int)(((b < 8) ? (w0 >> (8 * b)) : (w1 >> (8 * (b - 8)))) & 0xFF);
+}
 
 // address offset of tile index 0 of tile `t`: insert zero bits at the tile
 // positions of the low (n_local - T) bits, rows above n_local
@@ -66,7 +79,7 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const KParams& p) {
   uint64_t row = t >> fb;
   uint64_t f = t & ((uint64_t(1) << fb) - 1);
   for (int b = 0; b < p.T; ++b) {
-    uint64_t lo = f & ((uint64_t(1) << p.tpos[b]) - 1);
+    uint64_t lo = f & ((uint64_t(1) << byte_of(p.tpos0, p.tpos1, b)) - 1);
     f = ((f ^ lo) << 1) | lo;
   }
   return (row << p.n_local) | f;
@@ -75,6 +88,12 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const KParams& p) {
 __device__ __forceinline__ uint32_t deposit(uint32_t x, const uint8_t* pos, int cnt) {
   uint32_t r = 0;
   for (int m = 0; m < cnt; ++m) r |= ((x >> m) & 1u) << pos[m];
+  return r;
+}
+
+__device__ __forceinline__ uint32_t deposit_w(uint32_t x, uint64_t w0, uint64_t w1, int cnt) {
+  uint32_t r = 0;
+  for (int m = 0; m < cnt; ++m) r |= ((x >> m) & 1u) << byte_of(w0, w1, m);
   return r;
 }
 
@@ -88,18 +107,28 @@ __device__ __forceinline__ C cmul(C a, R br, R bi) {
 
 // ---- register-bit gate bodies (K compile-time so registers stay registers)
 
-template <typename R, int RB, int K>
+// PLAIN: no register-bit controls (no per-pair predicate); REAL: the 2x2 has
+// no imaginary parts (H, RY, CRY, sqrt(Y), products of those): 4 instead of 8
+// FP64 ops per amplitude
+template <typename R, int RB, int K, bool PLAIN, bool REAL>
 __device__ __forceinline__ void dense_k(typename Cx<R>::T* a, const R* m, uint32_t creg) {
 #pragma unroll
   for (int i = 0; i < (1 << RB); ++i) {
     if (i & (1 << K)) continue;
-    if ((uint32_t(i) & creg) != creg) continue;
+    if (!PLAIN && (uint32_t(i) & creg) != creg) continue;
     const int j = i | (1 << K);
     typename Cx<R>::T x = a[i], y = a[j], u, v;
-    u.x = fma(m[0], x.x, fma(-m[1], x.y, fma(m[2], y.x, -m[3] * y.y)));
-    u.y = fma(m[0], x.y, fma(m[1], x.x, fma(m[2], y.y, m[3] * y.x)));
-    v.x = fma(m[4], x.x, fma(-m[5], x.y, fma(m[6], y.x, -m[7] * y.y)));
-    v.y = fma(m[4], x.y, fma(m[5], x.x, fma(m[6], y.y, m[7] * y.x)));
+    if (REAL) {
+      u.x = fma(m[0], x.x, m[2] * y.x);
+      u.y = fma(m[0], x.y, m[2] * y.y);
+      v.x = fma(m[4], x.x, m[6] * y.x);
+      v.y = fma(m[4], x.y, m[6] * y.y);
+    } else {
+      u.x = fma(m[0], x.x, fma(-m[1], x.y, fma(m[2], y.x, -m[3] * y.y)));
+      u.y = fma(m[0], x.y, fma(m[1], x.x, fma(m[2], y.y, m[3] * y.x)));
+      v.x = fma(m[4], x.x, fma(-m[5], x.y, fma(m[6], y.x, -m[7] * y.y)));
+      v.y = fma(m[4], x.y, fma(m[5], x.x, fma(m[6], y.y, m[7] * y.x)));
+    }
     a[i] = u;
     a[j] = v;
   }
@@ -151,18 +180,27 @@ __device__ __forceinline__ void negate_uniform(typename Cx<R>::T* a, uint32_t cr
   }
 }
 
+#define HS_KSAT(k) ((k) < RB ? (k) : 0)
+#define HS_DENSE_CASE(k, P, Q)                                              \
+  case (k) + 4 * (P) + 8 * (Q):                                             \
+    if ((k) < RB) dense_k<R, RB, HS_KSAT(k), (P) != 0, (Q) != 0>(a, m, creg); \
+    break;
+
 template <typename R, int RB>
 __device__ __forceinline__ void exec_instr(typename Cx<R>::T* a, const Instr& in, uint32_t tdep) {
-  if ((tdep & in.ctid) != in.ctid) return;  // a thread-bit control is 0 for all my amplitudes
+  const uint32_t fl = in.flags;
+  if (!(fl & F_PLAIN) && (tdep & in.ctid) != in.ctid) return;  // a thread-bit control is 0
   R m[8];
   if (in.op == I_DENSE) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) m[q] = (R)in.m[q];
-    switch (in.k) {
-      case 0: dense_k<R, RB, 0>(a, m, in.creg); break;
-      case 1: if (RB > 1) dense_k<R, RB, (RB > 1 ? 1 : 0)>(a, m, in.creg); break;
-      case 2: if (RB > 2) dense_k<R, RB, (RB > 2 ? 2 : 0)>(a, m, in.creg); break;
-      case 3: if (RB > 3) dense_k<R, RB, (RB > 3 ? 3 : 0)>(a, m, in.creg); break;
+    const uint32_t creg = in.creg;
+    const int v = in.k + ((fl & F_PLAIN) ? 4 : 0) + ((fl & F_REAL) ? 8 : 0);
+    switch (v) {
+      HS_DENSE_CASE(0, 0, 0) HS_DENSE_CASE(1, 0, 0) HS_DENSE_CASE(2, 0, 0) HS_DENSE_CASE(3, 0, 0)
+      HS_DENSE_CASE(0, 1, 0) HS_DENSE_CASE(1, 1, 0) HS_DENSE_CASE(2, 1, 0) HS_DENSE_CASE(3, 1, 0)
+      HS_DENSE_CASE(0, 0, 1) HS_DENSE_CASE(1, 0, 1) HS_DENSE_CASE(2, 0, 1) HS_DENSE_CASE(3, 0, 1)
+      HS_DENSE_CASE(0, 1, 1) HS_DENSE_CASE(1, 1, 1) HS_DENSE_CASE(2, 1, 1) HS_DENSE_CASE(3, 1, 1)
     }
   } else if (in.op == I_PERM) {
     switch (in.k) {
@@ -213,8 +251,15 @@ __device__ __forceinline__ void phase_map(const uint8_t* rpos, const uint8_t* np
   for (int k = 0; k < RB; ++k) ub[k] = swz<R>(1u << rpos[k]);
 }
 
+// threads per CTA of a full tile: 2^(12 - RB) for c128 (64 KB), 2^(13 - RB)
+// for c64; two CTAs per SM
 template <typename R, int RB>
-__global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512, 2)
+constexpr int max_threads() {
+  return ((sizeof(R) == 8 ? 4096 : 8192) >> RB) > 1024 ? 1024 : ((sizeof(R) == 8 ? 4096 : 8192) >> RB);
+}
+
+template <typename R, int RB, bool CPROG>
+__global__ void __launch_bounds__(max_threads<R, RB>(), 2)
 hs_part_kernel(const KParams p) {
   using C = typename Cx<R>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -225,10 +270,10 @@ hs_part_kernel(const KParams p) {
   const int lowbits = T - RB;  // thread bits of the canonical load order
   // global offset of tile index s = tid + (j << lowbits)
   uint64_t ga_tid = 0;
-  for (int b = 0; b < lowbits; ++b) ga_tid |= uint64_t((tid >> b) & 1u) << p.tpos[b];
+  for (int b = 0; b < lowbits; ++b) ga_tid |= uint64_t((tid >> b) & 1u) << byte_of(p.tpos0, p.tpos1, b);
   uint64_t ga_hi[RB];
 #pragma unroll
-  for (int k = 0; k < RB; ++k) ga_hi[k] = uint64_t(1) << p.tpos[lowbits + k];
+  for (int k = 0; k < RB; ++k) ga_hi[k] = uint64_t(1) << byte_of(p.tpos0, p.tpos1, lowbits + k);
 
   for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
     const uint64_t base = tile_base((uint64_t)t, p) | ga_tid;
@@ -248,7 +293,7 @@ hs_part_kernel(const KParams p) {
     uint32_t tdep = 0, st = 0, ub[RB];
     bool loaded = false;
     for (int pc = 0; pc < p.nprog; ++pc) {
-      const Instr& in = p.prog[pc];
+      const Instr& in = CPROG ? c_prog[pc] : p.prog[pc];
       if (in.op == I_PHASE) {
         if (loaded) {
 #pragma unroll
@@ -264,7 +309,10 @@ hs_part_kernel(const KParams p) {
       }
     }
     if (p.fin_sync) __syncthreads();
-    phase_map<R, RB>(p.fin_rpos, p.fin_npos, T, tdep, st, ub);
+    tdep = deposit_w(tid, p.fnpos0, p.fnpos1, T - RB);
+    st = swz<R>(tdep);
+#pragma unroll
+    for (int k = 0; k < RB; ++k) ub[k] = swz<R>(1u << ((p.frpos >> (8 * k)) & 0xFF));
 #pragma unroll
     for (int i = 0; i < (1 << RB); ++i) sm[reg_slot<RB>(st, ub, i)] = a[i];
     __syncthreads();
@@ -283,38 +331,39 @@ hs_part_kernel(const KParams p) {
 
 // ---------------------------------------------------------------- launchers
 
-struct KernelSlot {
-  const void* fn;
-  int max_blocks_per_sm[MAX_TILE + 1];
-};
+template <typename R, int RB, bool CP>
+static const void* kfn() { return reinterpret_cast<const void*>(&hs_part_kernel<R, RB, CP>); }
 
-template <typename R, int RB>
-static const void* kfn() { return reinterpret_cast<const void*>(&hs_part_kernel<R, RB>); }
-
-static const void* kernel_for(int dtype, int RB) {
+template <bool CP>
+static const void* kernel_for_cp(int dtype, int RB) {
   if (dtype == HS_C128) {
     switch (RB) {
-      case 1: return kfn<double, 1>();
-      case 2: return kfn<double, 2>();
-      case 3: return kfn<double, 3>();
-      default: return kfn<double, 4>();
+      case 1: return kfn<double, 1, CP>();
+      case 2: return kfn<double, 2, CP>();
+      case 3: return kfn<double, 3, CP>();
+      default: return kfn<double, 4, CP>();
     }
   }
   switch (RB) {
-    case 1: return kfn<float, 1>();
-    case 2: return kfn<float, 2>();
-    case 3: return kfn<float, 3>();
-    default: return kfn<float, 4>();
+    case 1: return kfn<float, 1, CP>();
+    case 2: return kfn<float, 2, CP>();
+    case 3: return kfn<float, 3, CP>();
+    default: return kfn<float, 4, CP>();
   }
 }
 
+static const void* kernel_for(int dtype, int RB, bool cprog) {
+  return cprog ? kernel_for_cp<true>(dtype, RB) : kernel_for_cp<false>(dtype, RB);
+}
+
 cudaError_t prepare_kernels(int smem_optin) {
-  for (int dt = 0; dt < 2; ++dt)
-    for (int rb = 1; rb <= MAX_RB; ++rb) {
-      cudaError_t e = cudaFuncSetAttribute(kernel_for(dt, rb),
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
-      if (e != cudaSuccess) return e;
-    }
+  for (int cp = 0; cp < 2; ++cp)
+    for (int dt = 0; dt < 2; ++dt)
+      for (int rb = 1; rb <= MAX_RB; ++rb) {
+        cudaError_t e = cudaFuncSetAttribute(kernel_for(dt, rb, cp != 0),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+        if (e != cudaSuccess) return e;
+      }
   return cudaSuccess;
 }
 
@@ -328,15 +377,24 @@ cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void
   p.T = L.T;
   p.fin_sync = L.fin_sync;
   p.ntiles = batch << (n_local - L.T);
-  for (int b = 0; b < 16; ++b) p.tpos[b] = L.tpos[b];
-  for (int k = 0; k < MAX_RB; ++k) p.fin_rpos[k] = L.fin_rpos[k];
-  for (int m = 0; m < MAX_NPOS; ++m) p.fin_npos[m] = L.fin_npos[m];
+  p.tpos0 = p.tpos1 = p.fnpos0 = p.fnpos1 = 0;
+  p.frpos = 0;
+  for (int b = 0; b < 16; ++b) (b < 8 ? p.tpos0 : p.tpos1) |= uint64_t(L.tpos[b]) << (8 * (b & 7));
+  for (int m = 0; m < MAX_NPOS; ++m) (m < 8 ? p.fnpos0 : p.fnpos1) |= uint64_t(L.fin_npos[m]) << (8 * (m & 7));
+  for (int k = 0; k < MAX_RB; ++k) p.frpos |= uint32_t(L.fin_rpos[k]) << (8 * k);
   const size_t amp = (dtype == HS_C128) ? 16 : 8;
   const size_t smem = amp << L.T;
   const int threads = 1 << (L.T - L.RB);
-  const void* fn = kernel_for(dtype, L.RB);
+  const bool cprog = L.nprog <= CPROG_MAX;
+  const void* fn = kernel_for(dtype, L.RB, cprog);
+  cudaError_t e;
+  if (cprog) {
+    e = cudaMemcpyToSymbolAsync(c_prog, p.prog, sizeof(Instr) * (size_t)L.nprog, 0,
+                                cudaMemcpyDeviceToDevice, stream);
+    if (e != cudaSuccess) return e;
+  }
   int per_sm = 1;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)num_sms * per_sm;

@@ -111,6 +111,64 @@ int choose_npos(const std::vector<int>& nonreg, int dtype, uint8_t* npos) {
   return (int)all.size();
 }
 
+void classify(Gate& G) {
+  const double* m = G.m;
+  bool diag = m[2] == 0 && m[3] == 0 && m[4] == 0 && m[5] == 0;
+  bool perm = !diag && m[0] == 0 && m[1] == 0 && m[6] == 0 && m[7] == 0 && m[2] == 1 && m[3] == 0 &&
+              m[4] == 1 && m[5] == 0;
+  G.cls = diag ? C_DIAG : perm ? C_PERM : C_DENSE;
+  uint32_t cm = 0;
+  for (int a = 0; a < G.nctl; ++a) cm |= 1u << G.ctl[a];
+  if (G.cls == C_DIAG) { G.nd = 0; G.d = cm | (1u << G.tgt); }
+  else { G.nd = 1u << G.tgt; G.d = cm; }
+}
+
+// c = b * a for row-major complex 2x2 (apply a first, then b)
+void mat_mul(const double* b, const double* a, double* c) {
+  for (int r = 0; r < 2; ++r)
+    for (int k = 0; k < 2; ++k) {
+      double re = 0, im = 0;
+      for (int j = 0; j < 2; ++j) {
+        const double* x = b + 2 * (2 * r + j);
+        const double* y = a + 2 * (2 * j + k);
+        re += x[0] * y[0] - x[1] * y[1];
+        im += x[0] * y[1] + x[1] * y[0];
+      }
+      c[2 * (2 * r + k)] = re;
+      c[2 * (2 * r + k) + 1] = im;
+    }
+}
+
+// Merge every run of uncontrolled single-qubit gates on one tile bit into
+// one 2x2 (their product); a gate touching that bit in any other way ends
+// the run. Gates on other bits commute with the run, so program order of
+// the remaining list is still a valid order of the part.
+void fuse_single_qubit_runs(std::vector<Gate>& gs, int T) {
+  std::vector<Gate> out;
+  out.reserve(gs.size());
+  std::vector<int> open(T, -1);
+  for (const Gate& G : gs) {
+    if (G.cls != C_SWAP && G.nctl == 0) {
+      int& o = open[G.tgt];
+      if (o >= 0) {
+        double c[8];
+        mat_mul(G.m, out[o].m, c);
+        std::memcpy(out[o].m, c, sizeof(c));
+        classify(out[o]);
+        continue;
+      }
+      o = (int)out.size();
+      out.push_back(G);
+      continue;
+    }
+    uint32_t touched = G.nd | G.d;
+    for (int b = 0; b < T; ++b)
+      if (touched >> b & 1) open[b] = -1;
+    out.push_back(G);
+  }
+  gs.swap(out);
+}
+
 double paper_flops(const Rec& r) {
   // dense 2x2 = 14 FLOPs per amplitude, diag with two
   // non-unit entries 6, one non-unit 3, sign/permutation 0; controls scale by
@@ -128,7 +186,7 @@ double paper_flops(const Rec& r) {
 
 }  // namespace
 
-int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w,
+int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int32_t* staged, int w,
               const hs_gate* gates, int num_gates, PartPlan& out, std::string& err) {
   if (n_local < 1 || n_local > 62) { err = "n_local outside [1, 62]"; return HS_ERR_INVALID; }
   if (w < 0 || w > HS_MAX_STAGED) { err = "staged count outside [0, 24]"; return HS_ERR_INVALID; }
@@ -146,7 +204,7 @@ int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w
     return HS_ERR_TOO_WIDE;
   }
   if (T > MAX_TILE) { err = "tile wider than the kernels support"; return HS_ERR_TOO_WIDE; }
-  const int RB = std::min(MAX_RB, T);
+  const int RB = std::min((options & HS_PLAN_RB3) ? 3 : MAX_RB, T);
 
   // tile = staged positions + lowest free positions
   std::vector<int> tile(staged, staged + w);
@@ -182,16 +240,11 @@ int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w
     G.nctl = ar - 1;
     for (int a = 0; a < G.nctl; ++a) G.ctl[a] = bits[a];
     G.tgt = bits[ar - 1];
-    const double* m = G.m;
-    bool diag = m[2] == 0 && m[3] == 0 && m[4] == 0 && m[5] == 0;
-    bool perm = !diag && m[0] == 0 && m[1] == 0 && m[6] == 0 && m[7] == 0 && m[2] == 1 &&
-                m[3] == 0 && m[4] == 1 && m[5] == 0;
-    G.cls = diag ? C_DIAG : perm ? C_PERM : C_DENSE;
-    uint32_t cm = 0;
-    for (int a = 0; a < G.nctl; ++a) cm |= 1u << G.ctl[a];
-    if (G.cls == C_DIAG) { G.nd = 0; G.d = cm | (1u << G.tgt); }
-    else { G.nd = 1u << G.tgt; G.d = cm; }
+    classify(G);
   }
+  const int input_gates = num_gates;
+  if (options & HS_PLAN_FUSE_1Q) fuse_single_qubit_runs(gs, T);
+  num_gates = (int)gs.size();
 
   // storage labelling: loc_of[tile bit] / bit_at[location]
   std::vector<int> loc_of(T), bit_at(T);
@@ -281,8 +334,10 @@ int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w
         in.op = (r.cls == C_PERM) ? I_PERM : I_DENSE;
         in.k = (uint8_t)k;  // target is a register bit by construction
         std::memcpy(in.m, r.m, sizeof(in.m));
+        if (r.m[1] == 0 && r.m[3] == 0 && r.m[5] == 0 && r.m[7] == 0) in.flags |= F_REAL;
         if (r.cls == C_PERM) P.info.perm_gates++; else P.info.dense_gates++;
       }
+      if (in.creg == 0 && in.ctid == 0) in.flags |= F_PLAIN;
       flops += paper_flops(r);
       P.prog.push_back(in);
     }
@@ -323,6 +378,7 @@ int plan_part(int n_local, int dtype, int tile_max, const int32_t* staged, int w
   I.instructions = (int)P.prog.size();
   I.tiles = int64_t(1) << (n_local - T);
   I.fp_ops_per_amp = flops;
+  I.input_gates = input_gates;
   return HS_OK;
 }
 

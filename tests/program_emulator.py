@@ -25,7 +25,7 @@ INSTR = np.dtype([("op", "<u2"), ("k", "u1"), ("flags", "u1"), ("creg", "<u4"), 
 assert LAUNCH.itemsize == 56 and INSTR.itemsize == 96
 
 
-def plan(native, n_local, dtype, tile_bits, staged, ops, op_slots):
+def plan(native, n_local, dtype, tile_bits, staged, ops, op_slots, options=1):
     """Call hs_plan_part; returns (launch record, instr array, info)."""
     from paper_2205_06973_b200.hier import ExecutablePart, QubitSlotMap, _pack
 
@@ -35,10 +35,10 @@ def plan(native, n_local, dtype, tile_bits, staged, ops, op_slots):
     st = (ctypes.c_int32 * max(1, len(staged)))(*staged)
     size = ctypes.c_size_t()
     info = native.HsPartInfo()
-    native.check(lib.hs_plan_part(n_local, dtype, tile_bits, st, len(staged), gates, total, None, 0,
+    native.check(lib.hs_plan_part(n_local, dtype, tile_bits, options, st, len(staged), gates, total, None, 0,
                                   ctypes.byref(size), ctypes.byref(info)))
     buf = ctypes.create_string_buffer(size.value)
-    native.check(lib.hs_plan_part(n_local, dtype, tile_bits, st, len(staged), gates, total, buf, size.value,
+    native.check(lib.hs_plan_part(n_local, dtype, tile_bits, options, st, len(staged), gates, total, buf, size.value,
                                   ctypes.byref(size), ctypes.byref(info)))
     raw = buf.raw
     launch = np.frombuffer(raw[:LAUNCH.itemsize], dtype=LAUNCH)[0]

@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert lib.hs_abi_version() == 1
 
 
-def _emulate_parts(circuit, parts, tile_bits, dtype=0, rows=1, initial=None):
+def _emulate_parts(circuit, parts, tile_bits, dtype=0, rows=1, initial=None, options=1):
     n = circuit.num_qubits
     if initial is None:
         psi = np.zeros((rows, 1 << n), dtype=np.complex128)
@@ -39,21 +39,32 @@ def _emulate_parts(circuit, parts, tile_bits, dtype=0, rows=1, initial=None):
         from paper_2205_06973_b200.partition import Part
 
         exe = remap_part(circuit, Part(0, tuple(gates), tuple(qubits)))
-        launch, prog, _ = emu.plan(_native, n, dtype, tile_bits, exe.slot_map.qubits, exe.ops, exe.op_slots)
+        launch, prog, _ = emu.plan(_native, n, dtype, tile_bits, exe.slot_map.qubits, exe.ops, exe.op_slots, options)
         emu.emulate(psi, n, launch, prog)
     return psi
 
 
-@pytest.mark.parametrize("tile_bits", [12, 13, 6])
-def test_planned_programs_match_oracle_on_corpus(golden, tile_bits):
+@pytest.mark.parametrize("tile_bits,options", [(12, 1), (13, 1), (6, 1), (12, 0), (12, 3), (13, 2)])
+def test_planned_programs_match_oracle_on_corpus(golden, tile_bits, options):
     docs, states = golden.json("corpus"), golden.npz("corpus")
     for i, doc in enumerate(docs[:40]):
         c = parse_qasm(doc["qasm"])
         for key, parts in doc["partitions"].items():
             if max(len(q) for _, q in parts) > tile_bits:
                 continue
-            got = _emulate_parts(c, parts_of(parts), tile_bits)[0]
+            got = _emulate_parts(c, parts_of(parts), tile_bits, options=options)[0]
             assert np.max(np.abs(got - states[f"c{i}"])) < 1e-12, (i, key)
+
+
+def test_single_qubit_fusion_shrinks_random_circuit_parts():
+    c = configs.build("c2@16")
+    part = partition_dfs(build_dag(c), 12).parts[0]
+    exe = remap_part(c, part)
+    _, _, plain = emu.plan(_native, 16, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots, options=0)
+    _, _, fused = emu.plan(_native, 16, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots, options=1)
+    assert fused.input_gates == plain.input_gates == len(exe.ops)
+    assert fused.dense_gates < plain.dense_gates
+    assert fused.diag_gates == plain.diag_gates  # the CZs stay
 
 
 def test_planned_programs_with_batch_rows_and_random_state():
@@ -100,8 +111,9 @@ def test_plan_summary_counts():
     c = configs.build("c3@12")
     part = partition_dfs(build_dag(c), 10).parts[1]
     exe = remap_part(c, part)
-    _, prog, info = emu.plan(_native, 12, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots)
+    _, prog, info = emu.plan(_native, 12, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots, options=0)
     kinds = [op.kind for op in exe.ops]
+    assert info.input_gates == len(kinds)
     assert info.dense_gates == sum(k in (GateKind.H, GateKind.RX) for k in kinds)
     assert info.perm_gates == kinds.count(GateKind.CX)
     assert info.diag_gates == kinds.count(GateKind.RZ)
