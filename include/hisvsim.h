@@ -102,7 +102,8 @@ typedef struct {
 /* planner options (hs_engine_set_options / hs_plan_part) */
 #define HS_PLAN_FUSE_1Q 0x1u /* merge runs of uncontrolled 1-qubit gates per qubit */
 #define HS_PLAN_RB3 0x2u     /* 3 register bits per thread instead of 4 */
-#define HS_PLAN_DEFAULT HS_PLAN_FUSE_1Q
+#define HS_PLAN_PARITY 0x4u  /* CX(a,b) D(b) CX(a,b) -> one diagonal on a xor b */
+#define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
 
 typedef struct hs_engine hs_engine;
 typedef struct hs_program hs_program;

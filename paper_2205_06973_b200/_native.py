@@ -169,7 +169,8 @@ def engine_query(device: int) -> dict:
     return {"num_sms": sms.value, "tile_bits_c128": t128.value, "tile_bits_c64": t64.value}
 
 
-HS_PLAN_FUSE_1Q, HS_PLAN_RB3 = 0x1, 0x2
+HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY = 0x1, 0x2, 0x4
+HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY
 
 
 def set_options(device: int, options: int) -> None:

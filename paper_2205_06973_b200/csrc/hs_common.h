@@ -17,7 +17,9 @@ enum : uint16_t {
 };
 
 // DIAG flags
-enum : uint8_t { F_D0_ONE = 1, F_D1_ONE = 2, F_SIGN = 4, F_PLAIN = 8, F_REAL = 16 };
+// F_PARITY (DIAG): the entry index is the parity of the register bits in
+// rpos[0] (mask over the register index) and the thread bits in qtid
+enum : uint8_t { F_D0_ONE = 1, F_D1_ONE = 2, F_SIGN = 4, F_PLAIN = 8, F_REAL = 16, F_PARITY = 32 };
 
 constexpr uint8_t K_NONE = 0xFF;
 constexpr int MAX_RB = 4;       // register bits per thread

@@ -80,6 +80,7 @@ struct Gate {
   int other;    // SWAP: second operand
   int ctl[2];
   int nctl;
+  int par = -1; // DIAG on the parity tgt ^ par (from CX . D . CX), else -1
   double m[8];
   uint32_t nd;  // tile-logical bits touched non-diagonally
   uint32_t d;   // tile-logical bits touched diagonally (controls, diag targets)
@@ -90,6 +91,7 @@ struct Rec {  // a scheduled gate, in locations
   int tloc;
   int cloc[2];
   int nctl;
+  int ploc;     // parity partner location or -1
   const double* m;
 };
 
@@ -119,8 +121,43 @@ void classify(Gate& G) {
   G.cls = diag ? C_DIAG : perm ? C_PERM : C_DENSE;
   uint32_t cm = 0;
   for (int a = 0; a < G.nctl; ++a) cm |= 1u << G.ctl[a];
+  if (G.par >= 0) cm |= 1u << G.par;
   if (G.cls == C_DIAG) { G.nd = 0; G.d = cm | (1u << G.tgt); }
   else { G.nd = 1u << G.tgt; G.d = cm; }
+}
+
+bool is_cx(const Gate& G) { return G.cls == C_PERM && G.nctl == 1 && G.par < 0; }
+
+// CX(a,b) . D(b) . CX(a,b) with D = diag(d0, d1) equals the diagonal
+// d_{a xor b}: rewrite it as one parity-diagonal (ZZ interaction of QAOA /
+// Ising Trotter steps). Ops between the three that touch neither a nor b
+// commute with them and stay where they are.
+void fuse_parity_diagonals(std::vector<Gate>& gs) {
+  const int n = (int)gs.size();
+  std::vector<char> dead(n, 0);
+  for (int i = 0; i < n; ++i) {
+    if (dead[i] || !is_cx(gs[i])) continue;
+    const int a = gs[i].ctl[0], b = gs[i].tgt;
+    const uint32_t ab = (1u << a) | (1u << b);
+    auto next_on = [&](int from) {
+      for (int j = from; j < n; ++j)
+        if (!dead[j] && ((gs[j].nd | gs[j].d) & ab)) return j;
+      return -1;
+    };
+    const int jd = next_on(i + 1);
+    if (jd < 0) continue;
+    const Gate& D = gs[jd];
+    if (!(D.cls == C_DIAG && D.nctl == 0 && D.par < 0 && D.tgt == b)) continue;
+    const int jc = next_on(jd + 1);
+    if (jc < 0 || !is_cx(gs[jc]) || gs[jc].ctl[0] != a || gs[jc].tgt != b) continue;
+    gs[jd].par = a;
+    classify(gs[jd]);
+    dead[i] = dead[jc] = 1;
+  }
+  std::vector<Gate> out;
+  for (int i = 0; i < n; ++i)
+    if (!dead[i]) out.push_back(gs[i]);
+  gs.swap(out);
 }
 
 // c = b * a for row-major complex 2x2 (apply a first, then b)
@@ -148,7 +185,7 @@ void fuse_single_qubit_runs(std::vector<Gate>& gs, int T) {
   out.reserve(gs.size());
   std::vector<int> open(T, -1);
   for (const Gate& G : gs) {
-    if (G.cls != C_SWAP && G.nctl == 0) {
+    if (G.cls != C_SWAP && G.nctl == 0 && G.par < 0) {
       int& o = open[G.tgt];
       if (o >= 0) {
         double c[8];
@@ -244,6 +281,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   }
   const int input_gates = num_gates;
   if (options & HS_PLAN_FUSE_1Q) fuse_single_qubit_runs(gs, T);
+  if (options & HS_PLAN_PARITY) fuse_parity_diagonals(gs);
   num_gates = (int)gs.size();
 
   // storage labelling: loc_of[tile bit] / bit_at[location]
@@ -283,7 +321,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
           bit_at[loc_of[b]] = b;
           P.info.swaps_relabelled++;
         } else {
-          Rec r{G.cls, loc_of[G.tgt], {0, 0}, G.nctl, G.m};
+          Rec r{G.cls, loc_of[G.tgt], {0, 0}, G.nctl, G.par >= 0 ? loc_of[G.par] : -1, G.m};
           for (int a = 0; a < G.nctl; ++a) r.cloc[a] = loc_of[G.ctl[a]];
           recs.push_back(r);
         }
@@ -322,7 +360,21 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       int k = reg_of(r.tloc);
       if (r.cls == C_DIAG) {
         in.op = I_DIAG;
-        if (k >= 0) in.k = (uint8_t)k; else in.qtid = 1u << r.tloc;
+        uint32_t kreg = 0, qt = 0;
+        for (int loc : {r.tloc, r.ploc}) {
+          if (loc < 0) continue;
+          int kk = reg_of(loc);
+          if (kk >= 0) kreg |= 1u << kk; else qt |= 1u << loc;
+        }
+        if (r.ploc < 0 && k >= 0) {
+          in.k = (uint8_t)k;  // one register bit
+        } else if (kreg == 0) {
+          in.qtid = qt;       // parity of thread bits: uniform per thread
+        } else {
+          in.flags |= F_PARITY;
+          in.rpos[0] = (uint8_t)kreg;
+          in.qtid = qt;
+        }
         in.m[0] = r.m[0]; in.m[1] = r.m[1]; in.m[2] = r.m[6]; in.m[3] = r.m[7];
         bool d0one = r.m[0] == 1.0 && r.m[1] == 0.0;
         bool d1one = r.m[6] == 1.0 && r.m[7] == 0.0;

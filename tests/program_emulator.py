@@ -15,7 +15,7 @@ import ctypes
 import numpy as np
 
 I_PHASE, I_DENSE, I_PERM, I_DIAG = 1, 2, 3, 4
-F_D0_ONE, F_D1_ONE, F_SIGN = 1, 2, 4
+F_D0_ONE, F_D1_ONE, F_SIGN, F_PARITY = 1, 2, 4, 32
 K_NONE = 0xFF
 
 LAUNCH = np.dtype([("prog_offset", "<i8"), ("nprog", "<i4"), ("T", "<i4"), ("RB", "<i4"), ("fin_sync", "<i4"),
@@ -105,11 +105,14 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog) -> None:
                 regs[j] = np.where(tok[None, :], nb, b)
         else:
             d0, d1 = complex(m[0], m[1]), complex(m[2], m[3])
+            tpar = np.array([bin(int(t) & int(ins["qtid"])).count("1") & 1 for t in tdep], dtype=bool)
             for i in range(1 << RB):
                 if (i & creg) != creg:
                     continue
-                if k == K_NONE:
-                    one = (tdep & int(ins["qtid"])) != 0
+                if int(ins["flags"]) & F_PARITY:
+                    one = tpar ^ bool(bin(i & int(ins["rpos"][0])).count("1") & 1)
+                elif k == K_NONE:
+                    one = tpar
                 else:
                     one = np.full(nt, bool(i & (1 << k)))
                 f = np.where(one, d1, d0)

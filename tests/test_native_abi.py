@@ -44,7 +44,7 @@ def _emulate_parts(circuit, parts, tile_bits, dtype=0, rows=1, initial=None, opt
     return psi
 
 
-@pytest.mark.parametrize("tile_bits,options", [(12, 1), (13, 1), (6, 1), (12, 0), (12, 3), (13, 2)])
+@pytest.mark.parametrize("tile_bits,options", [(12, 5), (13, 5), (6, 5), (12, 0), (12, 7), (13, 2), (12, 4)])
 def test_planned_programs_match_oracle_on_corpus(golden, tile_bits, options):
     docs, states = golden.json("corpus"), golden.npz("corpus")
     for i, doc in enumerate(docs[:40]):
@@ -65,6 +65,27 @@ def test_single_qubit_fusion_shrinks_random_circuit_parts():
     assert fused.input_gates == plain.input_gates == len(exe.ops)
     assert fused.dense_gates < plain.dense_gates
     assert fused.diag_gates == plain.diag_gates  # the CZs stay
+
+
+@pytest.mark.parametrize("name", ["c3@12", "c4@12"])
+def test_parity_diagonals_replace_cx_rz_cx(name):
+    """QAOA / Ising bonds (CX . RZ . CX) become one parity diagonal each;
+    the emulated program still matches the oracle."""
+    c = configs.ising_config(12, 3) if name == "c4@12" else configs.build(name)
+    part = partition_dfs(build_dag(c), 10)
+    for p in part.parts:
+        exe = remap_part(c, p)
+        _, _, off = emu.plan(_native, 12, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots, options=1)
+        _, _, on = emu.plan(_native, 12, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots, options=5)
+        assert on.perm_gates <= off.perm_gates
+    cx = sum(op.kind is GateKind.CX for op in c.ops)
+    total_on = 0
+    for p in part.parts:
+        exe = remap_part(c, p)
+        total_on += emu.plan(_native, 12, 0, 12, exe.slot_map.qubits, exe.ops, exe.op_slots, options=5)[2].perm_gates
+    assert total_on < cx / 4
+    got = _emulate_parts(c, [(p.gate_indices, p.qubits) for p in part.parts], 12, options=5)[0]
+    assert np.max(np.abs(got - orc.simulate_flat(c))) < 1e-12
 
 
 def test_planned_programs_with_batch_rows_and_random_state():
