@@ -212,7 +212,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     if args.plan_options is not None:
         from paper_2205_06973_b200 import _native
 
-        _native.set_options(dev.index, args.plan_options)
+        _native.set_default_options(args.plan_options)
     n = circuit.num_qubits
     dist = world > 1
     if dist:
@@ -224,6 +224,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         run = HierarchicalRun(circuit, part, device=dev)
         n_local = n
     num_parts = part.num_parts
+    num_launches = run.program.num_launches if not dist else len(run.exes)
     bytes_per_pass = 2 * (1 << n_local) * 16
     state = allocate(n_local, "complex128", dev)
     stream = torch.cuda.current_stream(dev)
@@ -241,7 +242,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         elif timed_events is None:
             run.program.run(state)
         else:
-            for i in range(num_parts):
+            for i in range(num_launches):
                 run.program.run(state, i, 1)
                 timed_events.append(torch.cuda.Event(enable_timing=True))
                 timed_events[-1].record(stream)
@@ -267,9 +268,11 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     total_ms = start.elapsed_time(stop)
     clk = clocks.stop()
     # per-launch durations of the part kernel (events between launches)
-    durs = []
+    durs, restore_ms = [], 0.0
     for ev in marks:
-        durs += [ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)]
+        d = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)]
+        durs += d[:num_parts]
+        restore_ms += sum(d[num_parts:])
     # only the part kernels sit between the events when not distributed
     if dist:
         t = torch.tensor([total_ms], device=dev)
@@ -313,6 +316,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     return {
         "ms_step": ms_step, "value": value, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
         "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
+        "num_launches": num_launches, "restore_ms_per_step": restore_ms / args.steps,
         "comm": run.comm_summary() if dist else None,
     }
 
@@ -388,7 +392,8 @@ def main(argv=None):
             "warmup": args.warmup, "ms_per_step": g["ms_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
             "config": config, "roofline": roofline, "clocks": g["clocks"],
-            "gpu_launches": args.steps * g["num_parts"] + (args.steps * g["num_parts"] if g["e2e"] else 0),
+            "gpu_launches": args.steps * g["num_launches"] + (args.steps * g["num_launches"] if g["e2e"] else 0),
+            "layout_restore_ms_per_step": g["restore_ms_per_step"],
             "e2e": g["e2e"],
             "time_to_solution_ms": g["ms_step"],
             "fp64_flops_per_step_paper_count": flops,

@@ -96,13 +96,19 @@ typedef struct {
   int64_t tiles;          /* CTA tiles per launch = batch * 2^(n_local - T) */
   double fp_ops_per_amp;  /* diagnostic real FLOPs per amplitude */
   int32_t input_gates;    /* gates before single-qubit fusion */
-  int32_t reserved;
+  int32_t restore;        /* 1: a layout-restore launch (no gates) */
 } hs_part_info;
 
 /* planner options (hs_engine_set_options / hs_plan_part) */
 #define HS_PLAN_FUSE_1Q 0x1u /* merge runs of uncontrolled 1-qubit gates per qubit */
 #define HS_PLAN_RB3 0x2u     /* 3 register bits per thread instead of 4 */
 #define HS_PLAN_PARITY 0x4u  /* CX(a,b) D(b) CX(a,b) -> one diagonal on a xor b */
+/* program-internal qubit layout: each part's write-back permutes the qubits
+ * of its tile so the next parts' qubits sit in the lowest physical bits
+ * (long contiguous runs); restore launches appended after the last part
+ * bring the buffer back to natural order. Programs must then be run over
+ * all their launches, in order. */
+#define HS_PLAN_LAYOUT 0x8u
 #define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
 
 typedef struct hs_engine hs_engine;
@@ -125,13 +131,16 @@ int hs_program_create(hs_engine* eng, int n_local, int dtype,
                       const hs_gate* gates, int num_gates, hs_program** out);
 int hs_program_destroy(hs_program* prog);
 int hs_program_num_parts(hs_program* prog);
+/* launches = parts + layout-restore launches (HS_PLAN_LAYOUT) */
+int hs_program_num_launches(hs_program* prog);
+/* per launch (index < num_launches) */
 int hs_program_part_info(hs_program* prog, int part, hs_part_info* out);
-/* device instructions of one part, copied to host (test/debug); returns the
+/* device instructions of one launch, copied to host (test/debug); returns the
  * count via *count; buf may be NULL to query the size in bytes */
 int hs_program_dump(hs_program* prog, int part, void* buf, size_t buf_bytes,
                     int* count, size_t* instr_bytes);
-/* launch parts [first, first+count) in order on `stream` over `batch`
- * contiguous rows of 2^n_local amplitudes each */
+/* launch [first, first+count) of the program's launches in order on
+ * `stream` over `batch` contiguous rows of 2^n_local amplitudes each */
 int hs_program_run(hs_program* prog, void* state, int64_t batch,
                    int first, int count, void* stream);
 /* same, but records the launches into a CUDA graph on first use and
@@ -144,6 +153,13 @@ int hs_program_run_graph(hs_program* prog, void* state, int64_t batch, void* str
 int hs_plan_part(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
                  const hs_gate* gates, int num_gates, void* buf, size_t buf_bytes,
                  size_t* bytes, hs_part_info* info);
+
+/* host-only planning of a whole program (layout + restore launches
+ * included): buf receives, per launch, a PartLaunch header followed by its
+ * instructions (NULL to query *bytes); *num_launches is set */
+int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options,
+                    const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
+                    void* buf, size_t buf_bytes, size_t* bytes, int* num_launches);
 
 /* one-shot run_part: plan, upload, launch, free (synchronizes the stream) */
 int hs_part_apply(hs_engine* eng, void* state, int64_t batch, int n_local, int dtype,

@@ -18,7 +18,7 @@ from .errors import (
     QubitCountOutOfRangeError,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhisvsim.so"
+LIB_PATH = Path(os.environ.get("HISVSIM_LIB") or Path(__file__).resolve().parent / "_lib" / "libhisvsim.so")
 
 HS_OK, HS_ERR_INVALID, HS_ERR_CAPACITY, HS_ERR_CUDA, HS_ERR_TOO_WIDE, HS_ERR_UNSUPPORTED = range(6)
 HS_C128, HS_C64 = 0, 1
@@ -28,8 +28,8 @@ HS_MAX_STAGED = 24
 EXPORTS = (
     "hs_last_error", "hs_abi_version", "hs_engine_create", "hs_engine_destroy",
     "hs_engine_query", "hs_engine_set_options", "hs_program_create", "hs_program_destroy",
-    "hs_program_num_parts", "hs_program_part_info", "hs_program_dump",
-    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_part_apply",
+    "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_dump",
+    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_max_abs_diff",
     "hs_pack_segments", "hs_unpack_segments",
 )
@@ -68,7 +68,7 @@ class HsPartInfo(ctypes.Structure):
         ("tiles", ctypes.c_int64),
         ("fp_ops_per_amp", ctypes.c_double),
         ("input_gates", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("restore", ctypes.c_int32),
     ]
 
 
@@ -89,6 +89,7 @@ def _declare(lib) -> None:
                                   ctypes.POINTER(HsGate), I, ctypes.POINTER(P)]),
         "hs_program_destroy": (I, [P]),
         "hs_program_num_parts": (I, [P]),
+        "hs_program_num_launches": (I, [P]),
         "hs_program_part_info": (I, [P, I, ctypes.POINTER(HsPartInfo)]),
         "hs_program_dump": (I, [P, I, P, ctypes.c_size_t, ctypes.POINTER(I),
                                 ctypes.POINTER(ctypes.c_size_t)]),
@@ -96,6 +97,8 @@ def _declare(lib) -> None:
         "hs_program_run_graph": (I, [P, P, I64, P]),
         "hs_plan_part": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int32), I, ctypes.POINTER(HsGate), I,
                              P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(HsPartInfo)]),
+        "hs_plan_program": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(HsPart), I, ctypes.POINTER(HsGate), I,
+                                P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I)]),
         "hs_part_apply": (I, [P, P, I64, I, I, ctypes.POINTER(ctypes.c_int32), I,
                               ctypes.POINTER(HsGate), I, P]),
         "hs_state_init_basis": (I, [P, I64, I, I64, P]),
@@ -169,10 +172,25 @@ def engine_query(device: int) -> dict:
     return {"num_sms": sms.value, "tile_bits_c128": t128.value, "tile_bits_c64": t64.value}
 
 
-HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY = 0x1, 0x2, 0x4
+HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY, HS_PLAN_LAYOUT = 0x1, 0x2, 0x4, 0x8
 HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY
 
 
 def set_options(device: int, options: int) -> None:
     """Planner options (HS_PLAN_* bits) for programs created afterwards."""
     check(load().hs_engine_set_options(engine(device), options))
+
+
+_default_options = HS_PLAN_DEFAULT | HS_PLAN_LAYOUT
+
+
+def default_options() -> int:
+    """Planner bits new programs use unless they pass their own (programs
+    run in part ranges, e.g. between distributed layout switches, drop
+    HS_PLAN_LAYOUT)."""
+    return _default_options
+
+
+def set_default_options(options: int) -> None:
+    global _default_options
+    _default_options = int(options)

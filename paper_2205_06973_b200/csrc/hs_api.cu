@@ -40,6 +40,7 @@ struct hs_program {
   hs_engine* eng = nullptr;
   int n_local = 0;
   int dtype = 0;
+  int user_parts = 0;            // plans beyond this are layout-restore launches
   std::vector<PartPlan> plans;
   Instr* d_prog = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -133,18 +134,17 @@ int hs_program_create(hs_engine* eng, int n_local, int dtype, const hs_part* par
   prog->eng = eng;
   prog->n_local = n_local;
   prog->dtype = dtype;
-  prog->plans.resize(num_parts);
-  size_t total = 0;
-  for (int i = 0; i < num_parts; ++i) {
-    const hs_part& p = parts[i];
-    if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates)
-      return fail(HS_ERR_INVALID, "part " + std::to_string(i) + ": gate window outside the gate array");
+  {
     std::string err;
-    int s = plan_part(n_local, dtype, tile_for(eng, dtype), eng->options, p.staged, p.num_staged, gates + p.gate_offset,
-                      p.num_gates, prog->plans[i], err);
-    if (s != HS_OK) return fail(s, "part " + std::to_string(i) + ": " + err);
-    prog->plans[i].launch.prog_offset = (int64_t)total;
-    total += prog->plans[i].prog.size();
+    int s = plan_program(n_local, dtype, tile_for(eng, dtype), eng->options, parts, num_parts, gates, num_gates,
+                         prog->plans, err);
+    if (s != HS_OK) return fail(s, err);
+  }
+  prog->user_parts = num_parts;
+  size_t total = 0;
+  for (auto& pl : prog->plans) {
+    pl.launch.prog_offset = (int64_t)total;
+    total += pl.prog.size();
   }
   if (total) {
     HS_CUDA(cudaSetDevice(eng->device), "cudaSetDevice");
@@ -168,7 +168,9 @@ int hs_program_destroy(hs_program* prog) {
   return HS_OK;
 }
 
-int hs_program_num_parts(hs_program* prog) { return prog ? (int)prog->plans.size() : -1; }
+int hs_program_num_parts(hs_program* prog) { return prog ? prog->user_parts : -1; }
+
+int hs_program_num_launches(hs_program* prog) { return prog ? (int)prog->plans.size() : -1; }
 
 int hs_program_part_info(hs_program* prog, int part, hs_part_info* out) {
   if (!prog || !out) return fail(HS_ERR_INVALID, "program/out is NULL");
@@ -268,6 +270,33 @@ int hs_plan_part(int n_local, int dtype, int tile_bits, uint32_t options, const 
   plan.launch.prog_offset = 0;
   std::memcpy(buf, &plan.launch, sizeof(PartLaunch));
   std::memcpy((char*)buf + sizeof(PartLaunch), plan.prog.data(), plan.prog.size() * sizeof(Instr));
+  return HS_OK;
+}
+
+int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options, const hs_part* parts, int num_parts,
+                    const hs_gate* gates, int num_gates, void* buf, size_t buf_bytes, size_t* bytes,
+                    int* num_launches) {
+  if (int s = check_dtype(dtype)) return s;
+  if (num_parts < 0 || (num_parts > 0 && !parts)) return fail(HS_ERR_INVALID, "bad part array");
+  if (tile_bits < 1 || tile_bits > MAX_TILE) return fail(HS_ERR_INVALID, "tile_bits outside [1, 13]");
+  std::vector<PartPlan> plans;
+  std::string err;
+  int s = plan_program(n_local, dtype, tile_bits, options, parts, num_parts, gates, num_gates, plans, err);
+  if (s != HS_OK) return fail(s, err);
+  size_t need = 0;
+  for (auto& pl : plans) need += sizeof(PartLaunch) + pl.prog.size() * sizeof(Instr);
+  if (bytes) *bytes = need;
+  if (num_launches) *num_launches = (int)plans.size();
+  if (!buf) return HS_OK;
+  if (buf_bytes < need) return fail(HS_ERR_INVALID, "plan buffer too small");
+  char* o = (char*)buf;
+  for (auto& pl : plans) {
+    pl.launch.prog_offset = 0;
+    std::memcpy(o, &pl.launch, sizeof(PartLaunch));
+    o += sizeof(PartLaunch);
+    std::memcpy(o, pl.prog.data(), pl.prog.size() * sizeof(Instr));
+    o += pl.prog.size() * sizeof(Instr);
+  }
   return HS_OK;
 }
 

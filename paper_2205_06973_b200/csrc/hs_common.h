@@ -59,9 +59,28 @@ struct PartPlan {
   hs_part_info info;
 };
 
+// Program-level qubit layout: logical position q (what parts stage) lives at
+// physical bit phys[q] of the buffer. A part's write-back may permute the
+// positions inside its tile (see hs_planner.cpp); inv is phys^-1.
+enum { LAYOUT_KEEP = 0, LAYOUT_PRIORITY = 1, LAYOUT_TARGET = 2 };
+struct LayoutIO {
+  const int32_t* phys_in = nullptr;   // null = identity
+  const int32_t* inv_in = nullptr;
+  int32_t* phys_out = nullptr;        // updated for the tile's qubits
+  const int32_t* next_use = nullptr;  // PRIORITY: parts until q is staged again
+  const int32_t* target = nullptr;    // TARGET: wanted physical position of q
+  int mode = LAYOUT_KEEP;
+};
+
 // Plan one part. Returns HS_OK or an error code with `err` filled.
 int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int32_t* staged, int w,
-              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err);
+              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err,
+              const LayoutIO* lay = nullptr);
+
+// Plan a whole part sequence (with HS_PLAN_LAYOUT: evolving layout plus the
+// restore launches that bring every qubit home at the end).
+int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
+                 const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err);
 
 // 2x2 base matrix of a gate kind (controls handled by masking), row-major
 // complex: m[0..7] = m00 re/im, m01, m10, m11. Mirrors statevec.py:33-98.

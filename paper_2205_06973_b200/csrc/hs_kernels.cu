@@ -134,16 +134,12 @@ __device__ __forceinline__ void dense_k(typename Cx<R>::T* a, const R* m, uint32
   }
 }
 
-// X-type exchange on register bit K. C = 0..3: one control on register bit
-// C (a static register renaming); C = 4: no register control; C = 5:
-// several register controls, tested at run time.
-template <typename R, int RB, int K, int C>
+template <typename R, int RB, int K>
 __device__ __forceinline__ void perm_k(typename Cx<R>::T* a, uint32_t creg) {
 #pragma unroll
   for (int i = 0; i < (1 << RB); ++i) {
     if (i & (1 << K)) continue;
-    if (C < 4 && !(i & (1 << C))) continue;
-    if (C == 5 && (uint32_t(i) & creg) != creg) continue;
+    if ((uint32_t(i) & creg) != creg) continue;
     const int j = i | (1 << K);
     typename Cx<R>::T t = a[i];
     a[i] = a[j];
@@ -151,18 +147,16 @@ __device__ __forceinline__ void perm_k(typename Cx<R>::T* a, uint32_t creg) {
   }
 }
 
-// diag(d0, d1) on register bit K; MODE 0: both entries, 1: d0 == 1,
-// 2: sign flip (d0 == 1, d1 == -1); PLAIN: no register controls
-template <typename R, int RB, int K, int MODE, bool PLAIN>
-__device__ __forceinline__ void diag_k(typename Cx<R>::T* a, const R* d, uint32_t creg) {
+template <typename R, int RB, int K>
+__device__ __forceinline__ void diag_k(typename Cx<R>::T* a, const R* d, uint32_t creg, int flags) {
 #pragma unroll
   for (int i = 0; i < (1 << RB); ++i) {
-    if (!PLAIN && (uint32_t(i) & creg) != creg) continue;
+    if ((uint32_t(i) & creg) != creg) continue;
     if (i & (1 << K)) {
-      if (MODE == 2) { a[i].x = -a[i].x; a[i].y = -a[i].y; }
-      else a[i] = cmul(a[i], d[2], d[3]);
-    } else if (MODE == 0) {
-      a[i] = cmul(a[i], d[0], d[1]);
+      if (flags & F_SIGN) { a[i].x = -a[i].x; a[i].y = -a[i].y; }
+      else if (!(flags & F_D1_ONE)) a[i] = cmul(a[i], d[2], d[3]);
+    } else {
+      if (!(flags & F_D0_ONE)) a[i] = cmul(a[i], d[0], d[1]);
     }
   }
 }
@@ -227,16 +221,11 @@ __device__ __forceinline__ void exec_instr(typename Cx<R>::T* a, const Instr& in
       HS_DENSE_CASE(0, 1, 1) HS_DENSE_CASE(1, 1, 1) HS_DENSE_CASE(2, 1, 1) HS_DENSE_CASE(3, 1, 1)
     }
   } else if (in.op == I_PERM) {
-    const uint32_t creg = in.creg;
-    const int c = creg == 0 ? 4 : (creg & (creg - 1)) == 0 ? __ffs(creg) - 1 : 5;
-    switch (in.k * 8 + c) {
-#define HS_PERM_CASE(k, c) \
-  case (k) * 8 + (c):      \
-    if ((k) < RB && ((c) >= 4 || (c) < RB)) perm_k<R, RB, HS_KSAT(k), ((c) >= 4 || (c) < RB) ? (c) : 4>(a, creg); \
-    break;
-#define HS_PERM_ROW(k) HS_PERM_CASE(k, 0) HS_PERM_CASE(k, 1) HS_PERM_CASE(k, 2) HS_PERM_CASE(k, 3) \
-                       HS_PERM_CASE(k, 4) HS_PERM_CASE(k, 5)
-      HS_PERM_ROW(0) HS_PERM_ROW(1) HS_PERM_ROW(2) HS_PERM_ROW(3)
+    switch (in.k) {
+      case 0: perm_k<R, RB, 0>(a, in.creg); break;
+      case 1: if (RB > 1) perm_k<R, RB, (RB > 1 ? 1 : 0)>(a, in.creg); break;
+      case 2: if (RB > 2) perm_k<R, RB, (RB > 2 ? 2 : 0)>(a, in.creg); break;
+      case 3: if (RB > 3) perm_k<R, RB, (RB > 3 ? 3 : 0)>(a, in.creg); break;
     }
   } else {  // I_DIAG
 #pragma unroll
@@ -255,16 +244,11 @@ __device__ __forceinline__ void exec_instr(typename Cx<R>::T* a, const Instr& in
       }
       return;
     }
-    const int mode = (fl & F_SIGN) ? 2 : (fl & F_D0_ONE) ? 1 : 0;
-    const uint32_t creg = in.creg;
-    switch (in.k * 8 + mode * 2 + (creg == 0 ? 1 : 0)) {
-#define HS_DIAG_CASE(k, md, pl) \
-  case (k) * 8 + (md) * 2 + (pl): \
-    if ((k) < RB) diag_k<R, RB, HS_KSAT(k), (md), (pl) != 0>(a, m, creg); \
-    break;
-#define HS_DIAG_ROW(k) HS_DIAG_CASE(k, 0, 0) HS_DIAG_CASE(k, 0, 1) HS_DIAG_CASE(k, 1, 0) HS_DIAG_CASE(k, 1, 1) \
-                       HS_DIAG_CASE(k, 2, 0) HS_DIAG_CASE(k, 2, 1)
-      HS_DIAG_ROW(0) HS_DIAG_ROW(1) HS_DIAG_ROW(2) HS_DIAG_ROW(3)
+    switch (in.k) {
+      case 0: diag_k<R, RB, 0>(a, m, in.creg, in.flags); break;
+      case 1: if (RB > 1) diag_k<R, RB, (RB > 1 ? 1 : 0)>(a, m, in.creg, in.flags); break;
+      case 2: if (RB > 2) diag_k<R, RB, (RB > 2 ? 2 : 0)>(a, m, in.creg, in.flags); break;
+      case 3: if (RB > 3) diag_k<R, RB, (RB > 3 ? 3 : 0)>(a, m, in.creg, in.flags); break;
     }
   }
 }
@@ -296,36 +280,6 @@ constexpr int max_threads() {
   return ((sizeof(R) == 8 ? 4096 : 8192) >> RB) > 1024 ? 1024 : ((sizeof(R) == 8 ? 4096 : 8192) >> RB);
 }
 
-// Global <-> shared copy of tile t in canonical order (slot s = tid + j <<
-// (T - RB): consecutive threads take consecutive tile indices, so the low
-// tile bits give contiguous runs). The addressing is recomputed from the
-// kernel parameters on every call (the opaque move keeps the compiler from
-// holding it in registers across the gate program).
-template <typename R, int RB, bool LOAD>
-__device__ __forceinline__ void tile_io(typename Cx<R>::T* sm, typename Cx<R>::T* psi, int64_t t, const KParams& p) {
-  using C = typename Cx<R>::T;
-  uint64_t w0, w1;
-  asm volatile("mov.b64 %0, %1;" : "=l"(w0) : "l"(p.tpos0));
-  asm volatile("mov.b64 %0, %1;" : "=l"(w1) : "l"(p.tpos1));
-  const uint32_t tid = threadIdx.x;
-  const int lowbits = p.T - RB;
-  uint64_t base = tile_base((uint64_t)t, p);
-  for (int b = 0; b < lowbits; ++b) base |= uint64_t((tid >> b) & 1u) << byte_of(w0, w1, b);
-  uint64_t hi[RB];
-#pragma unroll
-  for (int k = 0; k < RB; ++k) hi[k] = uint64_t(1) << byte_of(w0, w1, lowbits + k);
-#pragma unroll
-  for (int j = 0; j < (1 << RB); ++j) {
-    uint64_t off = base;
-#pragma unroll
-    for (int k = 0; k < RB; ++k)
-      if (j & (1 << k)) off |= hi[k];
-    const uint32_t s = tid + (uint32_t(j) << lowbits);
-    if (LOAD) cp_async(&sm[swz<R>(s)], &psi[off], sizeof(C));
-    else psi[off] = sm[swz<R>(s)];
-  }
-}
-
 template <typename R, int RB, bool CPROG>
 __global__ void __launch_bounds__(max_threads<R, RB>(), 2)
 hs_part_kernel(const KParams p) {
@@ -335,9 +289,25 @@ hs_part_kernel(const KParams p) {
   C* psi = reinterpret_cast<C*>(p.psi);
   const uint32_t tid = threadIdx.x;
   const int T = p.T;
+  const int lowbits = T - RB;  // thread bits of the canonical load order
+  // global offset of tile index s = tid + (j << lowbits)
+  uint64_t ga_tid = 0;
+  for (int b = 0; b < lowbits; ++b) ga_tid |= uint64_t((tid >> b) & 1u) << byte_of(p.tpos0, p.tpos1, b);
+  uint64_t ga_hi[RB];
+#pragma unroll
+  for (int k = 0; k < RB; ++k) ga_hi[k] = uint64_t(1) << byte_of(p.tpos0, p.tpos1, lowbits + k);
 
   for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-    tile_io<R, RB, true>(sm, psi, t, p);
+    const uint64_t base = tile_base((uint64_t)t, p) | ga_tid;
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+      uint64_t off = base;
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (j & (1 << k)) off |= ga_hi[k];
+      const uint32_t s = tid + (uint32_t(j) << lowbits);
+      cp_async(&sm[swz<R>(s)], &psi[off], sizeof(C));
+    }
     cp_async_wait_all();
     __syncthreads();
 
@@ -368,7 +338,15 @@ hs_part_kernel(const KParams p) {
 #pragma unroll
     for (int i = 0; i < (1 << RB); ++i) sm[reg_slot<RB>(st, ub, i)] = a[i];
     __syncthreads();
-    tile_io<R, RB, false>(sm, psi, t, p);
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) {
+      uint64_t off = base;
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (j & (1 << k)) off |= ga_hi[k];
+      const uint32_t s = tid + (uint32_t(j) << lowbits);
+      psi[off] = sm[swz<R>(s)];
+    }
     __syncthreads();
   }
 }

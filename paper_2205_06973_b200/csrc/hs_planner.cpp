@@ -224,7 +224,7 @@ double paper_flops(const Rec& r) {
 }  // namespace
 
 int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int32_t* staged, int w,
-              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err) {
+              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err, const LayoutIO* lay) {
   if (n_local < 1 || n_local > 62) { err = "n_local outside [1, 62]"; return HS_ERR_INVALID; }
   if (w < 0 || w > HS_MAX_STAGED) { err = "staged count outside [0, 24]"; return HS_ERR_INVALID; }
   for (int j = 0; j < w; ++j) {
@@ -243,13 +243,16 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   if (T > MAX_TILE) { err = "tile wider than the kernels support"; return HS_ERR_TOO_WIDE; }
   const int RB = std::min((options & HS_PLAN_RB3) ? 3 : MAX_RB, T);
 
-  // tile = staged positions + lowest free positions
-  std::vector<int> tile(staged, staged + w);
+  // physical positions of the staged qubits under the program's layout
+  std::vector<int> phy(w);
+  for (int j = 0; j < w; ++j) phy[j] = lay && lay->phys_in ? lay->phys_in[staged[j]] : staged[j];
+  // tile = staged physical positions + lowest free physical positions
+  std::vector<int> tile(phy);
   for (int p = 0; (int)tile.size() < T && p < n_local; ++p)
-    if (std::find(staged, staged + w, p) == staged + w) tile.push_back(p);
+    if (std::find(phy.begin(), phy.end(), p) == phy.end()) tile.push_back(p);
   std::sort(tile.begin(), tile.end());
   std::vector<int> tl(w);
-  for (int j = 0; j < w; ++j) tl[j] = int(std::find(tile.begin(), tile.end(), staged[j]) - tile.begin());
+  for (int j = 0; j < w; ++j) tl[j] = int(std::find(tile.begin(), tile.end(), phy[j]) - tile.begin());
 
   // classify gates
   std::vector<Gate> gs(num_gates);
@@ -406,8 +409,45 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     P.prog.push_back(ph);
     phases = 1;
   }
+  // write-back relabel rho: the qubit in tile bit b is stored at tile
+  // position rho[b] (a permutation of the tile's own positions, so the store
+  // stays in place). It is how the program's layout evolves: qubits staged
+  // soonest move to the lowest physical positions so later tiles read long
+  // contiguous runs, and the final launches steer every qubit home.
+  std::vector<int> rho(T);
+  for (int b = 0; b < T; ++b) rho[b] = b;
+  if (lay && lay->mode != LAYOUT_KEEP) {
+    std::vector<int> occ(T);  // logical position living at tile[b]
+    for (int b = 0; b < T; ++b) occ[b] = lay->inv_in ? lay->inv_in[tile[b]] : tile[b];
+    auto index_in_tile = [&](int p) {
+      auto it = std::find(tile.begin(), tile.end(), p);
+      return it == tile.end() ? -1 : int(it - tile.begin());
+    };
+    if (lay->mode == LAYOUT_PRIORITY) {
+      std::vector<int> order(T);
+      for (int b = 0; b < T; ++b) order[b] = b;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int x, int y) { return lay->next_use[occ[x]] < lay->next_use[occ[y]]; });
+      for (int r = 0; r < T; ++r) rho[order[r]] = r;
+    } else {  // LAYOUT_TARGET: each occupant to target[occ] when that lies in the tile
+      std::vector<char> taken(T, 0), placed(T, 0);
+      for (int b = 0; b < T; ++b) {
+        int t = index_in_tile(lay->target[occ[b]]);
+        if (t >= 0 && !taken[t]) { rho[b] = t; taken[t] = 1; placed[b] = 1; }
+      }
+      int next = 0;
+      for (int b = 0; b < T; ++b) {
+        if (placed[b]) continue;
+        while (taken[next]) ++next;
+        rho[b] = next;
+        taken[next] = 1;
+      }
+    }
+    if (lay->phys_out)
+      for (int b = 0; b < T; ++b) lay->phys_out[occ[b]] = tile[rho[b]];
+  }
   // final store: register k holds location R[k] of the last phase, which is
-  // tile bit bit_at[R[k]]; write it to that bit's natural position
+  // tile bit bit_at[R[k]]; it is written to tile position rho[bit_at[R[k]]]
   const Instr* last = nullptr;
   for (const Instr& in : P.prog) if (in.op == I_PHASE) last = &in;
   PartLaunch& L = P.launch;
@@ -417,10 +457,10 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   L.RB = RB;
   for (int b = 0; b < T; ++b) L.tpos[b] = (uint8_t)tile[b];
   bool ident = true;
-  for (int b = 0; b < T; ++b) ident &= (loc_of[b] == b);
+  for (int loc = 0; loc < T; ++loc) ident &= (rho[bit_at[loc]] == loc);
   L.fin_sync = ident ? 0 : 1;
-  for (int k = 0; k < RB; ++k) L.fin_rpos[k] = (uint8_t)bit_at[last->rpos[k]];
-  for (int m = 0; m < T - RB; ++m) L.fin_npos[m] = (uint8_t)bit_at[last->npos[m]];
+  for (int k = 0; k < RB; ++k) L.fin_rpos[k] = (uint8_t)rho[bit_at[last->rpos[k]]];
+  for (int m = 0; m < T - RB; ++m) L.fin_npos[m] = (uint8_t)rho[bit_at[last->npos[m]]];
 
   hs_part_info& I = P.info;
   I.tile_bits = T;
@@ -431,6 +471,116 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   I.tiles = int64_t(1) << (n_local - T);
   I.fp_ops_per_amp = flops;
   I.input_gates = input_gates;
+  return HS_OK;
+}
+
+namespace {
+
+// Launches that permute the buffer back to the natural layout: every cycle of
+// the displacement (data at p belongs at inv[p]) is closed inside one tile;
+// cycles longer than a tile are shortened by T - 1 per launch.
+int plan_restore(int n_local, int dtype, int tile_max, uint32_t options, std::vector<int32_t>& phys,
+                 std::vector<PartPlan>& plans, std::string& err) {
+  const int T = std::min(tile_max, n_local);
+  for (int guard = 0; guard < 4 * n_local + 4; ++guard) {
+    std::vector<int32_t> inv(n_local);
+    for (int q = 0; q < n_local; ++q) inv[phys[q]] = q;
+    std::vector<std::vector<int>> cycles;
+    std::vector<char> seen(n_local, 0);
+    for (int p = 0; p < n_local; ++p) {
+      if (seen[p] || inv[p] == p) continue;
+      std::vector<int> c;
+      for (int x = p; !seen[x]; x = inv[x]) { seen[x] = 1; c.push_back(x); }
+      cycles.push_back(c);
+    }
+    if (cycles.empty()) return HS_OK;
+    // one launch: whole cycles first-fit, or a T-long chunk of a long cycle
+    std::vector<int> set, dest;
+    for (auto& c : cycles) {
+      if ((int)c.size() <= T - (int)set.size()) {
+        for (size_t k = 0; k < c.size(); ++k) { set.push_back(c[k]); dest.push_back(c[(k + 1) % c.size()]); }
+      } else if (set.empty()) {
+        for (int k = 0; k < T; ++k) { set.push_back(c[k]); dest.push_back(k + 1 < T ? c[k + 1] : c[0]); }
+        break;
+      }
+    }
+    std::vector<int32_t> staged, target(phys), next(phys);
+    for (size_t k = 0; k < set.size(); ++k) {
+      staged.push_back(inv[set[k]]);
+      target[inv[set[k]]] = dest[k];
+    }
+    std::sort(staged.begin(), staged.end());
+    LayoutIO lay;
+    lay.phys_in = phys.data();
+    lay.inv_in = inv.data();
+    lay.phys_out = next.data();
+    lay.target = target.data();
+    lay.mode = LAYOUT_TARGET;
+    PartPlan pl;
+    int s = plan_part(n_local, dtype, tile_max, options, staged.data(), (int)staged.size(), nullptr, 0, pl, err, &lay);
+    if (s != HS_OK) return s;
+    pl.info.restore = 1;
+    plans.push_back(pl);
+    phys = next;
+  }
+  err = "internal: layout restore did not converge";
+  return HS_ERR_INVALID;
+}
+
+}  // namespace
+
+int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
+                 const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err) {
+  plans.assign(num_parts, PartPlan());
+  const bool layout = (options & HS_PLAN_LAYOUT) && num_parts > 0 && n_local > 0;
+  std::vector<int32_t> phys(std::max(n_local, 1)), inv(std::max(n_local, 1));
+  for (int q = 0; q < n_local; ++q) phys[q] = inv[q] = q;
+  // next_use[i][q]: parts after i until q is staged again (large = never)
+  std::vector<std::vector<int32_t>> next_use;
+  if (layout) {
+    const int32_t never = 1 << 29;
+    next_use.assign(num_parts, std::vector<int32_t>(n_local, never));
+    std::vector<int32_t> upcoming(n_local, -1);
+    for (int i = num_parts - 1; i >= 0; --i) {
+      for (int q = 0; q < n_local; ++q)
+        if (upcoming[q] >= 0) next_use[i][q] = upcoming[q] - i;
+      for (int j = 0; j < parts[i].num_staged; ++j) {
+        int q = parts[i].staged[j];
+        if (q >= 0 && q < n_local) upcoming[q] = i;
+      }
+    }
+  }
+  std::vector<int32_t> home(std::max(n_local, 1));
+  for (int q = 0; q < n_local; ++q) home[q] = q;
+  for (int i = 0; i < num_parts; ++i) {
+    const hs_part& p = parts[i];
+    if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates) {
+      err = "part " + std::to_string(i) + ": gate window outside the gate array";
+      return HS_ERR_INVALID;
+    }
+    LayoutIO lay;
+    std::vector<int32_t> next(phys);
+    if (layout) {
+      lay.phys_in = phys.data();
+      lay.inv_in = inv.data();
+      lay.phys_out = next.data();
+      lay.next_use = next_use[i].data();
+      lay.target = home.data();
+      lay.mode = (i + 1 == num_parts) ? LAYOUT_TARGET : LAYOUT_PRIORITY;
+    }
+    std::string e;
+    int s = plan_part(n_local, dtype, tile_max, options, p.staged, p.num_staged, gates + p.gate_offset, p.num_gates,
+                      plans[i], e, layout ? &lay : nullptr);
+    if (s != HS_OK) {
+      err = "part " + std::to_string(i) + ": " + e;
+      return s;
+    }
+    if (layout) {
+      phys = next;
+      for (int q = 0; q < n_local; ++q) inv[phys[q]] = q;
+    }
+  }
+  if (layout) return plan_restore(n_local, dtype, tile_max, options, phys, plans, err);
   return HS_OK;
 }
 

@@ -207,7 +207,10 @@ class PartProgram:
     ``rows x 2^n_local`` amplitudes (hs_program_create). Planning happens
     once; ``run`` only launches."""
 
-    def __init__(self, n_local: int, exes: Sequence[ExecutablePart], dtype="complex128", device=None):
+    def __init__(self, n_local: int, exes: Sequence[ExecutablePart], dtype="complex128", device=None,
+                 options: int | None = None):
+        """``options``: planner bits (``_native.HS_PLAN_*``); default: the
+        engine default plus ``HS_PLAN_LAYOUT`` (whole-program runs)."""
         import torch
 
         self.n_local = n_local
@@ -215,14 +218,24 @@ class PartProgram:
         self.device = torch.device(device) if device is not None else default_device()
         self.num_parts = len(exes)
         lib = _native.load()
-        eng = _native.engine(self.device.index if self.device.index is not None else 0)
+        dev = self.device.index if self.device.index is not None else 0
+        eng = _native.engine(dev)
+        if options is None:
+            options = _native.default_options()
+        self.options = options
         parts, gates, total = _pack(exes)
         out = ctypes.c_void_p()
         code = 0 if self.dtype == torch.complex128 else 1
         with torch.cuda.device(self.device):
-            _native.check(lib.hs_program_create(eng, n_local, code, parts, len(exes), gates, total, ctypes.byref(out)))
+            _native.check(lib.hs_engine_set_options(eng, options))
+            try:
+                _native.check(lib.hs_program_create(eng, n_local, code, parts, len(exes), gates, total,
+                                                    ctypes.byref(out)))
+            finally:
+                lib.hs_engine_set_options(eng, _native.default_options())
         self._h = out.value
         self._lib = lib
+        self.num_launches = lib.hs_program_num_launches(self._h)
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
@@ -247,6 +260,8 @@ class PartProgram:
             "swaps_relabelled": inf.swaps_relabelled,
             "tiles": inf.tiles,
             "fp_ops_per_amp": inf.fp_ops_per_amp,
+            "input_gates": inf.input_gates,
+            "restore": bool(inf.restore),
         }
 
     def dump(self, i: int) -> bytes:
@@ -270,11 +285,12 @@ class PartProgram:
         return rows
 
     def run(self, data, first: int = 0, count: int | None = None, stream=None) -> None:
-        """Launch parts [first, first+count) on ``data`` (stream-ordered)."""
+        """Launch launches [first, first+count) on ``data`` (stream-ordered;
+        default: all of them, i.e. every part plus any layout restore)."""
         import torch
 
         rows = self._check(data)
-        count = self.num_parts - first if count is None else count
+        count = self.num_launches - first if count is None else count
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
         _native.check(self._lib.hs_program_run(self._h, data.data_ptr(), rows, first, count, s))
 

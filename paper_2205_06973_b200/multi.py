@@ -29,6 +29,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+from . import _native
 from .dist import CommStats, DistributedRun, RankLayout, _part_exes, plan_layouts, storage_order
 from .hier import PartProgram
 
@@ -122,7 +123,8 @@ class ShardedRun:
             e = _part_exes(circuit, partition, i, lay)
             self.bounds.append((len(self.exes), len(e)))
             self.exes += e
-        self.program = (PartProgram(self.n_local, self.exes, dtype=dtype, device=device)
+        self.program = (PartProgram(self.n_local, self.exes, dtype=dtype, device=device,
+                                    options=_native.default_options() & ~_native.HS_PLAN_LAYOUT)
                         if program and self.exes else None)
         self.ops = ops or DeviceOps()
         self.stats = CommStats(self.n, num_rank_bits, len(self.layouts),

@@ -121,3 +121,27 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog) -> None:
     for i, s in enumerate(fin[1]):
         smem[:, s] = regs[i]
     flat[bases[:, None] + ga[None, :]] = smem
+
+
+def plan_program(native, n_local, dtype, tile_bits, exes, options):
+    """Call hs_plan_program; returns [(launch record, instr array)] per launch."""
+    from paper_2205_06973_b200.hier import _pack
+
+    parts, gates, total = _pack(exes)
+    lib = native.load()
+    size = ctypes.c_size_t()
+    nl = ctypes.c_int()
+    native.check(lib.hs_plan_program(n_local, dtype, tile_bits, options, parts, len(exes), gates, total, None, 0,
+                                     ctypes.byref(size), ctypes.byref(nl)))
+    buf = ctypes.create_string_buffer(max(1, size.value))
+    native.check(lib.hs_plan_program(n_local, dtype, tile_bits, options, parts, len(exes), gates, total, buf,
+                                     size.value, ctypes.byref(size), ctypes.byref(nl)))
+    raw, out, off = buf.raw, [], 0
+    for _ in range(nl.value):
+        launch = np.frombuffer(raw[off:off + LAUNCH.itemsize], dtype=LAUNCH)[0]
+        off += LAUNCH.itemsize
+        n = int(launch["nprog"])
+        prog = np.frombuffer(raw[off:off + n * INSTR.itemsize], dtype=INSTR)
+        off += n * INSTR.itemsize
+        out.append((launch, prog))
+    return out

@@ -140,3 +140,26 @@ def test_plan_summary_counts():
     assert info.diag_gates == kinds.count(GateKind.RZ)
     assert info.phases == sum(int(i["op"]) == emu.I_PHASE for i in prog)
     assert info.tile_bits == 12 and info.reg_bits == 4
+
+
+@pytest.mark.parametrize("name,limit", [("c2@13", 8), ("c3@14", 9), ("c1@12", 6)])
+def test_program_layout_and_restore_match_oracle(name, limit):
+    """HS_PLAN_LAYOUT: parts permute qubits inside their tiles toward the low
+    physical bits, restore launches bring the buffer home; the emulated
+    launch sequence must equal the oracle and end in natural order."""
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), limit)
+    exes = [remap_part(c, p) for p in part.parts]
+    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    for tile_bits in (limit, 12):
+        launches = emu.plan_program(_native, c.num_qubits, 0, tile_bits, exes, options=5 | 8)
+        assert len(launches) >= len(exes)
+        psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
+        psi[0, 0] = 1
+        for launch, prog in launches:
+            emu.emulate(psi, c.num_qubits, launch, prog)
+        assert np.max(np.abs(psi[0] - want)) < 1e-12
+    # the layout moves at least some later tiles onto the low physical bits
+    low = [int(l["tpos"][0]) for l, _ in emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=5 | 8)]
+    plain = [int(l["tpos"][0]) for l, _ in emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=5)]
+    assert sum(x == 0 for x in low) >= sum(x == 0 for x in plain)
