@@ -97,6 +97,8 @@ typedef struct {
   double fp_ops_per_amp;  /* diagnostic real FLOPs per amplitude */
   int32_t input_gates;    /* gates before single-qubit fusion */
   int32_t restore;        /* 1: a layout-restore launch (no gates) */
+  int32_t compiled;       /* 1: runs as an NVRTC-compiled kernel (HS_PLAN_JIT) */
+  int32_t reserved;
 } hs_part_info;
 
 /* planner options (hs_engine_set_options / hs_plan_part) */
@@ -109,6 +111,10 @@ typedef struct {
  * bring the buffer back to natural order. Programs must then be run over
  * all their launches, in order. */
 #define HS_PLAN_LAYOUT 0x8u
+/* compile each part's program to a straight-line kernel with NVRTC (parts
+ * are compiled in parallel and cached per process); if NVRTC fails the
+ * interpreter kernel runs the same program */
+#define HS_PLAN_JIT 0x10u
 #define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
 
 typedef struct hs_engine hs_engine;
@@ -135,6 +141,8 @@ int hs_program_num_parts(hs_program* prog);
 int hs_program_num_launches(hs_program* prog);
 /* per launch (index < num_launches) */
 int hs_program_part_info(hs_program* prog, int part, hs_part_info* out);
+/* empty unless HS_PLAN_JIT compilation failed (the interpreter then runs) */
+const char* hs_program_jit_error(hs_program* prog);
 /* device instructions of one launch, copied to host (test/debug); returns the
  * count via *count; buf may be NULL to query the size in bytes */
 int hs_program_dump(hs_program* prog, int part, void* buf, size_t buf_bytes,
@@ -160,6 +168,11 @@ int hs_plan_part(int n_local, int dtype, int tile_bits, uint32_t options, const 
 int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options,
                     const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
                     void* buf, size_t buf_bytes, size_t* bytes, int* num_launches);
+
+/* CUDA C++ source of the compiled (HS_PLAN_JIT) kernel of one part, as
+ * generated from its plan (host-only; tests compile it with nvcc) */
+int hs_jit_source(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
+                  const hs_gate* gates, int num_gates, char* buf, size_t buf_bytes, size_t* bytes);
 
 /* one-shot run_part: plan, upload, launch, free (synchronizes the stream) */
 int hs_part_apply(hs_engine* eng, void* state, int64_t batch, int n_local, int dtype,

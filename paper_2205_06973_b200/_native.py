@@ -28,8 +28,9 @@ HS_MAX_STAGED = 24
 EXPORTS = (
     "hs_last_error", "hs_abi_version", "hs_engine_create", "hs_engine_destroy",
     "hs_engine_query", "hs_engine_set_options", "hs_program_create", "hs_program_destroy",
-    "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_dump",
-    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_part_apply",
+    "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_jit_error",
+    "hs_program_dump",
+    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_jit_source", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_max_abs_diff",
     "hs_pack_segments", "hs_unpack_segments",
 )
@@ -69,6 +70,8 @@ class HsPartInfo(ctypes.Structure):
         ("fp_ops_per_amp", ctypes.c_double),
         ("input_gates", ctypes.c_int32),
         ("restore", ctypes.c_int32),
+        ("compiled", ctypes.c_int32),
+        ("reserved2", ctypes.c_int32),
     ]
 
 
@@ -90,6 +93,7 @@ def _declare(lib) -> None:
         "hs_program_destroy": (I, [P]),
         "hs_program_num_parts": (I, [P]),
         "hs_program_num_launches": (I, [P]),
+        "hs_program_jit_error": (ctypes.c_char_p, [P]),
         "hs_program_part_info": (I, [P, I, ctypes.POINTER(HsPartInfo)]),
         "hs_program_dump": (I, [P, I, P, ctypes.c_size_t, ctypes.POINTER(I),
                                 ctypes.POINTER(ctypes.c_size_t)]),
@@ -99,6 +103,8 @@ def _declare(lib) -> None:
                              P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(HsPartInfo)]),
         "hs_plan_program": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(HsPart), I, ctypes.POINTER(HsGate), I,
                                 P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I)]),
+        "hs_jit_source": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int32), I, ctypes.POINTER(HsGate), I,
+                              ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
         "hs_part_apply": (I, [P, P, I64, I, I, ctypes.POINTER(ctypes.c_int32), I,
                               ctypes.POINTER(HsGate), I, P]),
         "hs_state_init_basis": (I, [P, I64, I, I64, P]),
@@ -172,7 +178,7 @@ def engine_query(device: int) -> dict:
     return {"num_sms": sms.value, "tile_bits_c128": t128.value, "tile_bits_c64": t64.value}
 
 
-HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY, HS_PLAN_LAYOUT = 0x1, 0x2, 0x4, 0x8
+HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY, HS_PLAN_LAYOUT, HS_PLAN_JIT = 0x1, 0x2, 0x4, 0x8, 0x10
 HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY
 
 
@@ -181,7 +187,7 @@ def set_options(device: int, options: int) -> None:
     check(load().hs_engine_set_options(engine(device), options))
 
 
-_default_options = HS_PLAN_DEFAULT | HS_PLAN_LAYOUT
+_default_options = HS_PLAN_DEFAULT
 
 
 def default_options() -> int:

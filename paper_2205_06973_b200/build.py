@@ -10,12 +10,13 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 SRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libhisvsim.so"
-SOURCES = ("hs_api.cu", "hs_kernels.cu", "hs_planner.cpp")
+SOURCES = ("hs_api.cu", "hs_kernels.cu", "hs_planner.cpp", "hs_jit.cpp")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC,-O3",
     "-Xptxas", "-v",
+    "-lnvrtc", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
 ]
 
 

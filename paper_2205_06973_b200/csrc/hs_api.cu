@@ -41,6 +41,7 @@ struct hs_program {
   int n_local = 0;
   int dtype = 0;
   int user_parts = 0;            // plans beyond this are layout-restore launches
+  std::string jit_error;         // why HS_PLAN_JIT fell back to the interpreter
   std::vector<PartPlan> plans;
   Instr* d_prog = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -141,6 +142,12 @@ int hs_program_create(hs_engine* eng, int n_local, int dtype, const hs_part* par
     if (s != HS_OK) return fail(s, err);
   }
   prog->user_parts = num_parts;
+  if (eng->options & HS_PLAN_JIT) {
+    std::string err;
+    HS_CUDA(cudaSetDevice(eng->device), "cudaSetDevice");
+    int s = jit_compile_program(prog->plans, dtype, n_local, eng->device, eng->smem_optin, err);
+    if (s != HS_OK) prog->jit_error = err;  // interpreter fallback on the GPU, reported
+  }
   size_t total = 0;
   for (auto& pl : prog->plans) {
     pl.launch.prog_offset = (int64_t)total;
@@ -176,6 +183,7 @@ int hs_program_part_info(hs_program* prog, int part, hs_part_info* out) {
   if (!prog || !out) return fail(HS_ERR_INVALID, "program/out is NULL");
   if (part < 0 || part >= (int)prog->plans.size()) return fail(HS_ERR_INVALID, "part index out of range");
   *out = prog->plans[part].info;
+  out->compiled = prog->plans[part].jit != nullptr;
   return HS_OK;
 }
 
@@ -199,11 +207,25 @@ static int run_range(hs_program* prog, void* state, int64_t batch, int first, in
   hs_engine* eng = prog->eng;
   for (int i = first; i < first + count; ++i) {
     const PartPlan& pl = prog->plans[i];
+    if (pl.jit) {
+      long long ntiles = (long long)(batch << (prog->n_local - pl.launch.T));
+      void* psi = state;
+      void* args[] = {&psi, &ntiles};
+      const size_t smem = size_t(prog->dtype == HS_C128 ? 16 : 8) << pl.launch.T;
+      long long grid = (long long)eng->num_sms * 2;
+      if (grid > ntiles) grid = ntiles;
+      HS_CUDA(cudaLaunchKernel((const void*)pl.jit, dim3((unsigned)grid), dim3(1u << (pl.launch.T - pl.launch.RB)),
+                               args, smem, s),
+              "compiled part kernel launch");
+      continue;
+    }
     HS_CUDA(launch_part(prog->dtype, pl.launch, prog->d_prog, state, prog->n_local, batch, eng->num_sms, s),
             "part kernel launch");
   }
   return HS_OK;
 }
+
+const char* hs_program_jit_error(hs_program* prog) { return prog ? prog->jit_error.c_str() : ""; }
 
 int hs_program_run(hs_program* prog, void* state, int64_t batch, int first, int count, void* stream) {
   if (!prog || !state) return fail(HS_ERR_INVALID, "program/state is NULL");
@@ -297,6 +319,22 @@ int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options, con
     std::memcpy(o, pl.prog.data(), pl.prog.size() * sizeof(Instr));
     o += pl.prog.size() * sizeof(Instr);
   }
+  return HS_OK;
+}
+
+int hs_jit_source(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
+                  const hs_gate* gates, int num_gates, char* buf, size_t buf_bytes, size_t* bytes) {
+  if (int s = check_dtype(dtype)) return s;
+  if (tile_bits < 1 || tile_bits > MAX_TILE) return fail(HS_ERR_INVALID, "tile_bits outside [1, 13]");
+  PartPlan plan;
+  std::string err;
+  int s = plan_part(n_local, dtype, tile_bits, options, staged, w, gates, num_gates, plan, err);
+  if (s != HS_OK) return fail(s, err);
+  std::string src = jit_source_for(plan, dtype, n_local);
+  if (bytes) *bytes = src.size() + 1;
+  if (!buf) return HS_OK;
+  if (buf_bytes < src.size() + 1) return fail(HS_ERR_INVALID, "source buffer too small");
+  std::memcpy(buf, src.c_str(), src.size() + 1);
   return HS_OK;
 }
 

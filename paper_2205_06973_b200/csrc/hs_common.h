@@ -57,7 +57,14 @@ struct PartPlan {
   PartLaunch launch;
   std::vector<Instr> prog;
   hs_part_info info;
+  void* jit = nullptr;  // cudaKernel_t of the compiled part (HS_PLAN_JIT), else null
 };
+
+// Compile every plan to a straight-line kernel (hs_jit.cpp); on failure all
+// plans keep jit == nullptr and the interpreter kernel runs them.
+int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, int device, int smem_optin,
+                        std::string& err);
+std::string jit_source_for(const PartPlan& pl, int dtype, int n_local);
 
 // Program-level qubit layout: logical position q (what parts stage) lives at
 // physical bit phys[q] of the buffer. A part's write-back may permute the

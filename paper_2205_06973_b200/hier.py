@@ -39,6 +39,10 @@ __all__ = [
 
 _KIND_CODE = {k: i for i, k in enumerate(GateKind)}
 
+#: programs over states of at least this many local qubits compile their
+#: parts to straight-line kernels (HS_PLAN_JIT) unless options say otherwise
+JIT_MIN_QUBITS = 20
+
 
 # --- addressing (host) --------------------------------------------------------
 
@@ -222,6 +226,10 @@ class PartProgram:
         eng = _native.engine(dev)
         if options is None:
             options = _native.default_options()
+            if n_local >= JIT_MIN_QUBITS:
+                # compiling a part costs ~0.5-1 s of host time (parallel over
+                # parts, cached); worth it once a pass moves >= 32 MiB
+                options |= _native.HS_PLAN_JIT
         self.options = options
         parts, gates, total = _pack(exes)
         out = ctypes.c_void_p()
@@ -236,6 +244,7 @@ class PartProgram:
         self._h = out.value
         self._lib = lib
         self.num_launches = lib.hs_program_num_launches(self._h)
+        self.jit_error = lib.hs_program_jit_error(self._h).decode(errors="replace")
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
@@ -262,6 +271,7 @@ class PartProgram:
             "fp_ops_per_amp": inf.fp_ops_per_amp,
             "input_gates": inf.input_gates,
             "restore": bool(inf.restore),
+            "compiled": bool(inf.compiled),
         }
 
     def dump(self, i: int) -> bytes:

@@ -221,3 +221,41 @@ def test_errors_surface_as_reference_exceptions():
     part = partition_of([(list(range(16)), list(range(16)))], limit=16)
     with pytest.raises(PartTooWideForLayoutError):
         execute_hierarchical(c, part)
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_compiled_parts_match_reference(golden, dtype):
+    """HS_PLAN_JIT (NVRTC straight-line kernels) on corpus circuits, the full
+    c1 QFT and scaled c2/c3 against the reference's results."""
+    from paper_2205_06973_b200.hier import PartProgram
+
+    opts = _native.default_options() | _native.HS_PLAN_JIT
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    for i, doc in enumerate(docs[:12]):
+        c = parse_qasm(doc["qasm"])
+        key = sorted(doc["partitions"])[0]
+        part = partition_of(doc["partitions"][key])
+        exes = [remap_part(c, p) for p in part.parts]
+        prog = PartProgram(c.num_qubits, exes, dtype=dtype, options=opts)
+        assert prog.jit_error == "" and all(prog.info(j)["compiled"] for j in range(prog.num_parts))
+        st = from_numpy(np.eye(1, 1 << c.num_qubits, 0).ravel().astype(np.complex128), dtype=dtype)
+        prog.run(st.data)
+        assert _dev_err(st, states[f"c{i}"]) < TOL[dtype]
+    for name in ("c2@20", "c3@20"):
+        doc = golden.json("configs")[name + ":sample"]
+        c = configs.build(name)
+        st = execute_hierarchical(c, partition_of(doc["partition"]), dtype=dtype)  # n >= 20: compiled
+        assert _sample(golden, name, st) < TOL[dtype]
+
+
+def test_compiled_full_size_c2_matches_c_oracle():
+    c = configs.build("c2")
+    part = partition_dfs(build_dag(c), 12)
+    run = HierarchicalRun(c, part)
+    assert all(run.program.info(j)["compiled"] for j in range(run.program.num_parts))
+    from paper_2205_06973_b200.statevec import zero_state
+
+    st = zero_state(26)
+    run.program.run(st.data)
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert max_abs_diff(st, ref) < 1e-10

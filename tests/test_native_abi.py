@@ -163,3 +163,40 @@ def test_program_layout_and_restore_match_oracle(name, limit):
     low = [int(l["tpos"][0]) for l, _ in emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=5 | 8)]
     plain = [int(l["tpos"][0]) for l, _ in emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=5)]
     assert sum(x == 0 for x in low) >= sum(x == 0 for x in plain)
+
+
+def _jit_source(c, p, dtype=0, options=5, tile_bits=12):
+    import ctypes
+
+    from paper_2205_06973_b200.hier import _pack
+
+    exe = remap_part(c, p)
+    _, gates, total = _pack([exe])
+    st = (ctypes.c_int32 * max(1, exe.num_slots))(*exe.slot_map.qubits)
+    lib = _native.load()
+    n = ctypes.c_size_t()
+    _native.check(lib.hs_jit_source(c.num_qubits, dtype, tile_bits, options, st, exe.num_slots, gates, total, None, 0,
+                                     ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value)
+    _native.check(lib.hs_jit_source(c.num_qubits, dtype, tile_bits, options, st, exe.num_slots, gates, total, buf,
+                                    n.value, ctypes.byref(n)))
+    return buf.value.decode()
+
+
+@pytest.mark.parametrize("name,dtype", [("c2@16", 0), ("c3@16", 0), ("c1@14", 0), ("c2@16", 1)])
+def test_compiled_part_sources_build_for_sm100a(tmp_path, name, dtype):
+    """The HS_PLAN_JIT code generator emits CUDA that nvcc compiles for
+    sm_100a without local-memory spills (NVRTC does the same at run time)."""
+    import shutil
+    import subprocess
+
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), 10)
+    for i, p in enumerate(part.parts[:2]):
+        src = tmp_path / f"p{i}.cu"
+        src.write_text(_jit_source(c, p, dtype))
+        res = subprocess.run([nvcc, "-arch=sm_100a", "-cubin", "-o", str(tmp_path / f"p{i}.cubin"), str(src),
+                              "-Xptxas", "-v"], capture_output=True, text=True)
+        assert res.returncode == 0, res.stderr[-2000:]
+        assert "hs_jit_part" in res.stderr
