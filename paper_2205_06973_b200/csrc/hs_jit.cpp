@@ -127,6 +127,84 @@ struct Gen {
     }
   }
 
+  // ---- folding of diagonal runs. Diagonal gates commute with each other, so
+  // a run of them (up to the next non-diagonal instruction or phase change)
+  // is applied as ONE complex factor per amplitude: gates that depend only
+  // on register bits fold into a compile-time constant per register, gates
+  // that depend only on thread bits fold into one runtime scalar per thread.
+  // Gates mixing both are emitted as they come.
+  std::vector<double> cre, cim;  // pending constant factor per register
+  bool have_const = false, have_u = false;
+  int u_id = 0;
+
+  void reset_pending() {
+    cre.assign(nreg, 1.0);
+    cim.assign(nreg, 0.0);
+    have_const = have_u = false;
+  }
+  void flush() {
+    if (!have_const && !have_u) return;
+    o << "    {\n";
+    for (int i = 0; i < nreg; ++i) {
+      const bool unit = cre[i] == 1.0 && cim[i] == 0.0;
+      if (!have_u) {
+        if (unit) continue;
+        if (cre[i] == -1.0 && cim[i] == 0.0) {
+          o << "      " << re(i) << " = -" << re(i) << "; " << im(i) << " = -" << im(i) << ";\n";
+          continue;
+        }
+        cmul_into(i, lit(cre[i], c128), lit(cim[i], c128));
+        continue;
+      }
+      const std::string ur = "ur" + std::to_string(u_id), ui = "ui" + std::to_string(u_id);
+      if (unit) {
+        cmul_into(i, ur, ui);
+      } else {
+        o << "      { const " << R() << " fr = fma(" << lit(cre[i], c128) << ", " << ur << ", -" << lit(cim[i], c128)
+          << " * " << ui << "), fi = fma(" << lit(cre[i], c128) << ", " << ui << ", " << lit(cim[i], c128) << " * "
+          << ur << ");\n  ";
+        cmul_into(i, "fr", "fi");
+        o << "      }\n";
+      }
+    }
+    o << "    }\n";
+    reset_pending();
+  }
+  // returns true if the instruction was folded into the pending run
+  bool fold_diag(const Instr& in) {
+    const bool parity = in.flags & F_PARITY;
+    const uint32_t kreg = parity ? in.rpos[0] : (in.k == K_NONE ? 0u : (1u << in.k));
+    const bool tdep = in.qtid != 0 || in.ctid != 0;
+    const bool rdep = kreg != 0 || in.creg != 0;
+    const double d0r = in.m[0], d0i = in.m[1], d1r = in.m[2], d1i = in.m[3];
+    if (!tdep) {
+      for (int i = 0; i < nreg; ++i) {
+        if ((uint32_t(i) & in.creg) != in.creg) continue;
+        const bool one = __builtin_popcount(uint32_t(i) & kreg) & 1;
+        const double fr = one ? d1r : d0r, fi = one ? d1i : d0i;
+        const double nr = cre[i] * fr - cim[i] * fi, ni = cre[i] * fi + cim[i] * fr;
+        cre[i] = nr;
+        cim[i] = ni;
+      }
+      have_const = true;
+      return true;
+    }
+    if (rdep) return false;
+    // uniform per thread: one scalar factor, selected by this thread's bits
+    if (!have_u) {
+      ++u_id;
+      o << "    " << R() << " ur" << u_id << " = 1, ui" << u_id << " = 0;\n";
+      have_u = true;
+    }
+    const std::string ur = "ur" + std::to_string(u_id), ui = "ui" + std::to_string(u_id);
+    o << "    { const bool tp = (__popc(t & " << in.qtid << "u) & 1) != 0;\n";
+    std::string cond = in.ctid ? "((t & " + std::to_string(in.ctid) + "u) == " + std::to_string(in.ctid) + "u)" : "true";
+    o << "      if (" << cond << ") { const " << R() << " fr = tp ? " << lit(d1r, c128) << " : " << lit(d0r, c128)
+      << ", fi = tp ? " << lit(d1i, c128) << " : " << lit(d0i, c128) << "; const " << R() << " a = " << ur << ", b = "
+      << ui << "; " << ur << " = a * fr - b * fi; " << ui << " = a * fi + b * fr; } }\n";
+    return true;
+  }
+
   void diag(const Instr& in) {
     const std::string d0r = lit(in.m[0], c128), d0i = lit(in.m[1], c128);
     const std::string d1r = lit(in.m[2], c128), d1i = lit(in.m[3], c128);
@@ -216,7 +294,10 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local) {
   for (int i = 0; i < g.nreg; ++i) o << (i ? ", " : "") << "r" << i << ", q" << i;
   o << ";\n    unsigned t, st;\n";
   const Instr* cur = nullptr;
+  g.reset_pending();
   for (const Instr& in : pl.prog) {
+    if (in.op == I_DIAG && g.fold_diag(in)) continue;
+    if (in.op != I_DIAG) g.flush();  // a non-diagonal step: apply the pending run first
     if (in.op == I_PHASE) {
       if (cur) {
         g.store_regs(cur->rpos);
@@ -236,6 +317,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local) {
     else g.diag(in);
     o << "    }\n";
   }
+  g.flush();
   if (pl.launch.fin_sync) o << "    __syncthreads();\n";
   g.emit_tdep("t", pl.launch.fin_npos);
   o << "    st = swz(t);\n";
