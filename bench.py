@@ -313,10 +313,24 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
                        "-> final state to pinned host"}
 
     info = [run.program.info(i) for i in range(num_parts)] if not dist else run.part_infos()
+    # FP64 roofline: issued FP64 pipe work of the part kernels vs a measured DFMA peak
+    import ctypes
+
+    from paper_2205_06973_b200 import _native
+
+    peak = ctypes.c_double()
+    _native.check(_native.load().hs_fp64_peak(ctypes.byref(peak), stream.cuda_stream))
+    fp64_instr = sum(i["fp64_instr_per_amp"] for i in info) * (1 << n_local)
+    part_ms = sum(durs) / args.steps if durs else ms_step
+    fp64 = {"bound_note": "random-circuit parts are FP64-bound, not HBM-bound (SURVEY.md 7.3)",
+            "instr_per_step": fp64_instr, "achieved_tflops": 2 * fp64_instr / (part_ms / 1e3) / 1e12,
+            "peak_tflops_measured": peak.value,
+            "frac": (2 * fp64_instr / (part_ms / 1e3) / 1e12) / peak.value if peak.value else None,
+            "part_kernel_ms_per_step": part_ms}
     return {
         "ms_step": ms_step, "value": value, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
         "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
-        "num_launches": num_launches, "restore_ms_per_step": restore_ms / args.steps,
+        "num_launches": num_launches, "restore_ms_per_step": restore_ms / args.steps, "fp64": fp64,
         "comm": run.comm_summary() if dist else None,
     }
 
@@ -397,6 +411,7 @@ def main(argv=None):
             "e2e": g["e2e"],
             "time_to_solution_ms": g["ms_step"],
             "fp64_flops_per_step_paper_count": flops,
+            "fp64": g["fp64"],
             "phases_per_part": [i["phases"] for i in infos],
             "comm": g["comm"]}
     if not args.no_cpu_baseline and world == 1:

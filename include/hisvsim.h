@@ -98,7 +98,7 @@ typedef struct {
   int32_t input_gates;    /* gates before single-qubit fusion */
   int32_t restore;        /* 1: a layout-restore launch (no gates) */
   int32_t compiled;       /* 1: runs as an NVRTC-compiled kernel (HS_PLAN_JIT) */
-  int32_t reserved;
+  float fp64_instr_per_amp; /* FP64 pipe instructions per amplitude (FMA = 1) */
 } hs_part_info;
 
 /* planner options (hs_engine_set_options / hs_plan_part) */
@@ -187,6 +187,10 @@ int hs_state_init_basis(void* state, int64_t num_amps, int dtype, int64_t index,
  * out-of-place, num_bits <= 40 */
 int hs_bit_permute(const void* in, void* out, int num_bits, int dtype,
                    const int32_t* dst_of, void* stream);
+
+/* measured FP64 FMA throughput of the current device (a DFMA-chain
+ * microbenchmark, ~20 ms): the denominator of the FP64 roofline */
+int hs_fp64_peak(double* tflops, void* stream);
 
 /* max |a - b| over n amplitudes of `dtype`, b given as complex128 (the
  * oracle's type); result written to *host_result after a stream sync */

@@ -31,7 +31,7 @@ EXPORTS = (
     "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_jit_error",
     "hs_program_dump",
     "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_jit_source", "hs_part_apply",
-    "hs_state_init_basis", "hs_bit_permute", "hs_max_abs_diff",
+    "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
     "hs_pack_segments", "hs_unpack_segments",
 )
 
@@ -71,7 +71,7 @@ class HsPartInfo(ctypes.Structure):
         ("input_gates", ctypes.c_int32),
         ("restore", ctypes.c_int32),
         ("compiled", ctypes.c_int32),
-        ("reserved2", ctypes.c_int32),
+        ("fp64_instr_per_amp", ctypes.c_float),
     ]
 
 
@@ -109,6 +109,7 @@ def _declare(lib) -> None:
                               ctypes.POINTER(HsGate), I, P]),
         "hs_state_init_basis": (I, [P, I64, I, I64, P]),
         "hs_bit_permute": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), P]),
+        "hs_fp64_peak": (I, [ctypes.POINTER(D), P]),
         "hs_max_abs_diff": (I, [P, I, P, I64, ctypes.POINTER(D), P]),
         "hs_pack_segments": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, P]),
         "hs_unpack_segments": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, P]),

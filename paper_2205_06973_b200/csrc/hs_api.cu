@@ -22,6 +22,7 @@ cudaError_t launch_segments(bool pack, const void* in, void* out, int nbits, int
                             const int32_t* seg_pos, int nseg, int num_sms, cudaStream_t s);
 cudaError_t launch_maxdiff(const void* a, int dtype, const void* b, int64_t n, unsigned long long* dres,
                            int num_sms, cudaStream_t s);
+cudaError_t measure_fp64_peak(double* tflops, int num_sms, cudaStream_t s);
 }  // namespace hs
 
 using namespace hs;
@@ -417,6 +418,12 @@ int hs_pack_segments(const void* src, void* dst, int num_bits, int dtype, const 
 int hs_unpack_segments(const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos, int nseg,
                        void* stream) {
   return segments(false, src, dst, num_bits, dtype, seg_pos, nseg, stream);
+}
+
+int hs_fp64_peak(double* tflops, void* stream) {
+  if (!tflops) return fail(HS_ERR_INVALID, "NULL argument");
+  HS_CUDA(measure_fp64_peak(tflops, sms_of_current(), (cudaStream_t)stream), "fp64 probe");
+  return HS_OK;
 }
 
 int hs_max_abs_diff(const void* a, int dtype, const void* b_c128, int64_t n, double* host_result, void* stream) {

@@ -555,3 +555,47 @@ cudaError_t launch_maxdiff(const void* a, int dtype, const void* b, int64_t n,
 }
 
 }  // namespace hs
+
+namespace hs {
+
+// FP64 FMA throughput probe: 8 independent DFMA chains per thread, enough
+// warps per SM to cover the pipe latency; the result keeps the chains live.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+         x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.6789) out[0] = s;  // practically never taken; defeats dead-code elimination
+}
+
+cudaError_t measure_fp64_peak(double* tflops, int num_sms, cudaStream_t s) {
+  const int iters = 2048, threads = 256, blocks = num_sms * 8;
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double));
+  if (e != cudaSuccess) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp64_probe_kernel<<<blocks, threads, 0, s>>>(d, 64, 0.999999, 1e-7);  // warm-up
+  cudaEventRecord(e0, s);
+  fp64_probe_kernel<<<blocks, threads, 0, s>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1, s);
+  e = cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return e;
+  const double fmas = double(blocks) * threads * iters * 16 * 8;
+  *tflops = 2.0 * fmas / (ms * 1e-3) / 1e12;
+  return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -297,7 +297,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   std::vector<char> done(num_gates, 0);
   int remaining = num_gates;
   std::vector<int> R;
-  double flops = 0;
+  double flops = 0, fp64 = 0;
   int phases = 0;
   while (remaining > 0) {
     R.clear();
@@ -394,6 +394,12 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       }
       if (in.creg == 0 && in.ctid == 0) in.flags |= F_PLAIN;
       flops += paper_flops(r);
+      {  // FP64 pipe instructions per amplitude, FMA = 1 (what the kernels issue)
+        double share = 1.0 / double(1 << r.nctl);
+        if (in.op == I_DENSE) fp64 += share * ((in.flags & F_REAL) ? 4.0 : 8.0);
+        if (in.op == I_DIAG && !(in.flags & F_SIGN))
+          fp64 += share * (((in.flags & (F_D0_ONE | F_D1_ONE)) && !(in.flags & F_PARITY)) ? 2.0 : 4.0);
+      }
       P.prog.push_back(in);
     }
   }
@@ -424,11 +430,35 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       return it == tile.end() ? -1 : int(it - tile.begin());
     };
     if (lay->mode == LAYOUT_PRIORITY) {
+      // the lowest 3 tile positions (the coalescing bits when they are the
+      // physical bits 0..2) go to the qubits staged soonest; qubits never
+      // staged again go home when home is in the tile (less to restore at
+      // the end); the rest fill the remaining positions by next use
       std::vector<int> order(T);
       for (int b = 0; b < T; ++b) order[b] = b;
       std::stable_sort(order.begin(), order.end(),
                        [&](int x, int y) { return lay->next_use[occ[x]] < lay->next_use[occ[y]]; });
-      for (int r = 0; r < T; ++r) rho[order[r]] = r;
+      const int32_t never = 1 << 29;
+      std::vector<char> taken(T, 0), placed(T, 0);
+      const int hot = std::min(3, T);
+      for (int r = 0; r < hot; ++r) {
+        rho[order[r]] = r;
+        taken[r] = placed[order[r]] = 1;
+      }
+      for (int r = hot; r < T; ++r) {
+        const int b = order[r];
+        if (lay->next_use[occ[b]] < never) continue;
+        int h = index_in_tile(occ[b]);
+        if (h >= hot && !taken[h]) { rho[b] = h; taken[h] = placed[b] = 1; }
+      }
+      int next = 0;
+      for (int r = 0; r < T; ++r) {
+        const int b = order[r];
+        if (placed[b]) continue;
+        while (taken[next]) ++next;
+        rho[b] = next;
+        taken[next] = 1;
+      }
     } else {  // LAYOUT_TARGET: each occupant to target[occ] when that lies in the tile
       std::vector<char> taken(T, 0), placed(T, 0);
       for (int b = 0; b < T; ++b) {
@@ -470,6 +500,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   I.instructions = (int)P.prog.size();
   I.tiles = int64_t(1) << (n_local - T);
   I.fp_ops_per_amp = flops;
+  I.fp64_instr_per_amp = (float)fp64;
   I.input_gates = input_gates;
   return HS_OK;
 }

@@ -42,6 +42,8 @@ _KIND_CODE = {k: i for i, k in enumerate(GateKind)}
 #: programs over states of at least this many local qubits compile their
 #: parts to straight-line kernels (HS_PLAN_JIT) unless options say otherwise
 JIT_MIN_QUBITS = 20
+#: ... and plan the coalescing layout (HS_PLAN_LAYOUT) from this size on
+LAYOUT_MIN_QUBITS = 23
 
 
 # --- addressing (host) --------------------------------------------------------
@@ -230,6 +232,10 @@ class PartProgram:
                 # compiling a part costs ~0.5-1 s of host time (parallel over
                 # parts, cached); worth it once a pass moves >= 32 MiB
                 options |= _native.HS_PLAN_JIT
+            if n_local >= LAYOUT_MIN_QUBITS:
+                # coalescing layout + restore launches pay off once the state
+                # streams from HBM (measured: c2/c3 win, the L2-resident c1 loses)
+                options |= _native.HS_PLAN_LAYOUT
         self.options = options
         parts, gates, total = _pack(exes)
         out = ctypes.c_void_p()
@@ -272,6 +278,7 @@ class PartProgram:
             "input_gates": inf.input_gates,
             "restore": bool(inf.restore),
             "compiled": bool(inf.compiled),
+            "fp64_instr_per_amp": float(inf.fp64_instr_per_amp),
         }
 
     def dump(self, i: int) -> bytes:

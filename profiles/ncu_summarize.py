@@ -79,3 +79,21 @@ def mix(rep):
 if __name__ == "__main__":
     rep = sys.argv[1]
     print(json.dumps({"launches": raw(rep), "first_launch_sass_mix": mix(rep)}, indent=1))
+
+
+def write_summary(rep: str, workload: str, out: str, note: str = "") -> dict:
+    """Condensed, committed form of one capture (read by bench.py for
+    roofline.traffic): per-launch metrics + instruction mix."""
+    launches = raw(rep)
+    per = [1e9 * (l.get("dram_read_GB", 0) + l.get("dram_write_GB", 0)) for l in launches]
+    doc = {
+        "workload": workload,
+        "source_report": rep,
+        "note": note,
+        "dram_bytes_per_launch": sum(per) / len(per) if per else None,
+        "launches": launches,
+        "first_launch_sass_mix": mix(rep),
+    }
+    with open(out, "w") as f:
+        json.dump(doc, f, indent=1)
+    return doc
