@@ -174,6 +174,12 @@ int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options,
 int hs_jit_source(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
                   const hs_gate* gates, int num_gates, char* buf, size_t buf_bytes, size_t* bytes);
 
+/* the structured form compiled kernels use for a 2x2 gate matrix m
+ * (row-major complex, 8 doubles): m = s * m_out with m_out's entries
+ * snapped to 0 / +-1 within a few ulps; returns the FP64 instructions per
+ * amplitude pair (allow_scale = 0: s = 1). Host-only. */
+int hs_structure_2x2(const double* m, int allow_scale, double* s_out, double* m_out);
+
 /* one-shot run_part: plan, upload, launch, free (synchronizes the stream) */
 int hs_part_apply(hs_engine* eng, void* state, int64_t batch, int n_local, int dtype,
                   const int32_t* staged, int w, const hs_gate* gates, int num_gates,

@@ -339,6 +339,14 @@ int hs_jit_source(int n_local, int dtype, int tile_bits, uint32_t options, const
   return HS_OK;
 }
 
+int hs_structure_2x2(const double* m, int allow_scale, double* s_out, double* m_out) {
+  if (!m) return -1;
+  Mat2 r = structure_2x2(m, allow_scale != 0);
+  if (s_out) { s_out[0] = r.s[0]; s_out[1] = r.s[1]; }
+  if (m_out) std::memcpy(m_out, r.m, sizeof(r.m));
+  return r.cost;
+}
+
 int hs_part_apply(hs_engine* eng, void* state, int64_t batch, int n_local, int dtype, const int32_t* staged,
                   int w, const hs_gate* gates, int num_gates, void* stream) {
   if (!eng || !state) return fail(HS_ERR_INVALID, "engine/state is NULL");

@@ -93,4 +93,24 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
 // complex: m[0..7] = m00 re/im, m01, m10, m11. Mirrors statevec.py:33-98.
 bool base_matrix(int kind, const double* params, double m[8]);
 
+// Structured 2x2: M = s * M' where M' has its entries snapped to 0 / +-1
+// when they are within a few ulps of them. A compiled kernel evaluates each
+// of the four real output components (u.re, u.im, v.re, v.im of the pair)
+// as a linear combination of the inputs (x.re, x.im, y.re, y.im): a zero
+// coefficient costs nothing, a +-1 coefficient turns an FMA into an add, so
+// sqrt(X), sqrt(Y), H (scaled) cost 1 FP64 op per output instead of 4.
+// `cost` = FP64 instructions per amplitude pair. With allow_scale, s may be
+// any entry of M (the caller then owes the scalar s to every amplitude);
+// without, s = 1.
+struct Mat2 {
+  double s[2];
+  double m[8];
+  int cost;
+};
+Mat2 structure_2x2(const double* m, bool allow_scale);
+// real coefficients of output component c (0: u.re, 1: u.im, 2: v.re, 3: v.im)
+// on the inputs (x.re, x.im, y.re, y.im)
+void component_coefs(const double* m, int c, double coef[4]);
+int component_cost(const double coef[4]);
+
 }  // namespace hs

@@ -15,6 +15,7 @@
 #include <nvrtc.h>
 
 #include <cinttypes>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -80,36 +81,91 @@ struct Gen {
   void cmul_into(int i, const std::string& dr, const std::string& di) {
     o << "      { const " << R() << " x = " << re(i) << ", y = " << im(i) << "; " << re(i) << " = fma(x, " << dr
       << ", -y * " << di << "); " << im(i) << " = fma(x, " << di << ", y * " << dr << "); }\n";
+    ops += 4 * wgt;
+  }
+  // multiply register i by a compile-time constant, exploiting 0 / +-1 parts
+  void cmul_const(int i, double fr, double fi) {
+    if (fr == 1.0 && fi == 0.0) return;
+    if (fi == 0.0) {
+      if (fr == -1.0) {
+        o << "      " << re(i) << " = -" << re(i) << "; " << im(i) << " = -" << im(i) << ";\n";
+        return;
+      }
+      o << "      " << re(i) << " *= " << lit(fr, c128) << "; " << im(i) << " *= " << lit(fr, c128) << ";\n";
+      ops += 2 * wgt;
+      return;
+    }
+    if (fr == 0.0) {  // (x + iy) * (i b) = -b y + i b x
+      const std::string b = lit(fi, c128);
+      o << "      { const " << R() << " x = " << re(i) << ", y = " << im(i) << "; ";
+      if (fi == 1.0) o << re(i) << " = -y; " << im(i) << " = x; }\n";
+      else if (fi == -1.0) o << re(i) << " = y; " << im(i) << " = -x; }\n";
+      else {
+        o << re(i) << " = -" << b << " * y; " << im(i) << " = " << b << " * x; }\n";
+        ops += 2 * wgt;
+      }
+      return;
+    }
+    cmul_into(i, lit(fr, c128), lit(fi, c128));
+  }
+
+  // ---- the part's scalar. structure_2x2 and the diagonal-run folding
+  // factor a constant s out of uncontrolled gates; every amplitude of the
+  // state owes the product S of those constants, applied once before the
+  // final store (folded into the last diagonal run when there is one).
+  double Sr = 1.0, Si = 0.0;
+  double ops = 0;   // FP64 instructions per thread per tile (control-weighted)
+  double wgt = 1;   // fraction of threads executing the current block
+  bool scale_ok(double sr, double si) const {
+    const double nr = Sr * sr - Si * si, ni = Sr * si + Si * sr;
+    const double mag = std::hypot(nr, ni);
+    return mag > 0 && std::fabs(std::log2(mag)) < 300;  // amplitudes stay far from overflow
+  }
+  void push_scale(double sr, double si) {
+    const double nr = Sr * sr - Si * si, ni = Sr * si + Si * sr;
+    Sr = nr;
+    Si = ni;
+  }
+
+  // one real output: sum_t coef[t] * src[t]; +-1 coefficients become adds
+  std::string comb(const double coef[4], const std::string* src) {
+    int start = -1;
+    for (int t = 0; t < 4 && start < 0; ++t)
+      if (coef[t] == 1.0) start = t;
+    for (int t = 0; t < 4 && start < 0; ++t)
+      if (coef[t] == -1.0) start = t;
+    std::string e;
+    if (start >= 0) e = (coef[start] == 1.0 ? "" : "-") + src[start];
+    for (int t = 0; t < 4; ++t) {
+      if (t == start || coef[t] == 0.0) continue;
+      if (e.empty()) e = lit(coef[t], c128) + " * " + src[t];
+      else if (coef[t] == 1.0) e = "(" + e + " + " + src[t] + ")";
+      else if (coef[t] == -1.0) e = "(" + e + " - " + src[t] + ")";
+      else e = "fma(" + lit(coef[t], c128) + ", " + src[t] + ", " + e + ")";
+      ops += wgt;
+    }
+    return e.empty() ? std::string(c128 ? "0.0" : "0.0f") : e;
   }
 
   void dense(const Instr& in) {
-    const double* m = in.m;
-    const bool real = in.flags & F_REAL;
-    std::string M[8];
-    for (int q = 0; q < 8; ++q) M[q] = lit(m[q], c128);
+    const bool plain = in.creg == 0 && in.ctid == 0;
+    Mat2 M = structure_2x2(in.m, plain);
+    if ((M.s[0] != 1.0 || M.s[1] != 0.0) && !scale_ok(M.s[0], M.s[1])) M = structure_2x2(in.m, false);
+    push_scale(M.s[0], M.s[1]);
+    const std::string src[4] = {"xr", "xi", "yr", "yi"};
     for (int i = 0; i < nreg; ++i) {
       if (i >> in.k & 1) continue;
       if ((uint32_t(i) & in.creg) != in.creg) continue;
       const int j = i | (1 << in.k);
       o << "      { const " << R() << " xr = " << re(i) << ", xi = " << im(i) << ", yr = " << re(j) << ", yi = "
         << im(j) << ";\n";
-      if (real) {
-        o << "        " << re(i) << " = fma(" << M[0] << ", xr, " << M[2] << " * yr); " << im(i) << " = fma(" << M[0]
-          << ", xi, " << M[2] << " * yi);\n";
-        o << "        " << re(j) << " = fma(" << M[4] << ", xr, " << M[6] << " * yr); " << im(j) << " = fma(" << M[4]
-          << ", xi, " << M[6] << " * yi); }\n";
-      } else {
-        auto out = [&](const std::string& dst_r, const std::string& dst_i, int a, int b) {
-          // (ma + i mb) * x + (mc + i md) * y with (a, b) = entries of x, y
-          o << "        " << dst_r << " = fma(" << M[a] << ", xr, fma(-" << M[a + 1] << ", xi, fma(" << M[b]
-            << ", yr, -" << M[b + 1] << " * yi)));\n";
-          o << "        " << dst_i << " = fma(" << M[a] << ", xi, fma(" << M[a + 1] << ", xr, fma(" << M[b]
-            << ", yi, " << M[b + 1] << " * yr)));\n";
-        };
-        out(re(i), im(i), 0, 2);
-        out(re(j), im(j), 4, 6);
-        o << "      }\n";
+      const std::string dst[4] = {re(i), im(i), re(j), im(j)};
+      for (int c = 0; c < 4; ++c) {
+        double coef[4];
+        component_coefs(M.m, c, coef);
+        o << "        " << dst[c] << " = " << comb(coef, src) << ";\n";
       }
+      o << "      }\n";
     }
   }
 
@@ -142,18 +198,51 @@ struct Gen {
     cim.assign(nreg, 0.0);
     have_const = have_u = false;
   }
-  void flush() {
+  // final: fold the part's scalar S into the run and apply it (no
+  // normalisation); otherwise the most common factor of the run is pulled
+  // out into S so the registers carrying it cost nothing
+  void flush(bool final = false) {
+    if (final && (Sr != 1.0 || Si != 0.0)) {
+      for (int i = 0; i < nreg; ++i) {
+        const double nr = cre[i] * Sr - cim[i] * Si, ni = cre[i] * Si + cim[i] * Sr;
+        cre[i] = nr;
+        cim[i] = ni;
+      }
+      have_const = true;
+      Sr = 1.0;
+      Si = 0.0;
+    }
     if (!have_const && !have_u) return;
+    if (have_const && !final) {
+      int best = -1, best_n = 0;
+      for (int i = 0; i < nreg; ++i) {
+        int n = 0;
+        for (int j = 0; j < nreg; ++j) n += cre[j] == cre[i] && cim[j] == cim[i];
+        if (n > best_n) { best_n = n; best = i; }
+      }
+      const double fr = cre[best], fi = cim[best];
+      const double n2 = fr * fr + fi * fi;
+      if (!(fr == 1.0 && fi == 0.0) && n2 > 0 && scale_ok(fr, fi)) {
+        for (int i = 0; i < nreg; ++i) {
+          if (cre[i] == fr && cim[i] == fi) { cre[i] = 1.0; cim[i] = 0.0; continue; }
+          double nr = (cre[i] * fr + cim[i] * fi) / n2, ni = (cim[i] * fr - cre[i] * fi) / n2;
+          if (std::fabs(ni) < 2e-15) ni = 0;
+          if (std::fabs(nr) < 2e-15) nr = 0;
+          if (ni == 0 && std::fabs(nr - 1) < 2e-15) nr = 1;
+          if (ni == 0 && std::fabs(nr + 1) < 2e-15) nr = -1;
+          if (nr == 0 && std::fabs(ni - 1) < 2e-15) ni = 1;
+          if (nr == 0 && std::fabs(ni + 1) < 2e-15) ni = -1;
+          cre[i] = nr;
+          cim[i] = ni;
+        }
+        push_scale(fr, fi);
+      }
+    }
     o << "    {\n";
     for (int i = 0; i < nreg; ++i) {
       const bool unit = cre[i] == 1.0 && cim[i] == 0.0;
       if (!have_u) {
-        if (unit) continue;
-        if (cre[i] == -1.0 && cim[i] == 0.0) {
-          o << "      " << re(i) << " = -" << re(i) << "; " << im(i) << " = -" << im(i) << ";\n";
-          continue;
-        }
-        cmul_into(i, lit(cre[i], c128), lit(cim[i], c128));
+        cmul_const(i, cre[i], cim[i]);
         continue;
       }
       const std::string ur = "ur" + std::to_string(u_id), ui = "ui" + std::to_string(u_id);
@@ -163,6 +252,7 @@ struct Gen {
         o << "      { const " << R() << " fr = fma(" << lit(cre[i], c128) << ", " << ur << ", -" << lit(cim[i], c128)
           << " * " << ui << "), fi = fma(" << lit(cre[i], c128) << ", " << ui << ", " << lit(cim[i], c128) << " * "
           << ur << ");\n  ";
+        ops += 4 * wgt;
         cmul_into(i, "fr", "fi");
         o << "      }\n";
       }
@@ -202,6 +292,7 @@ struct Gen {
     o << "      if (" << cond << ") { const " << R() << " fr = tp ? " << lit(d1r, c128) << " : " << lit(d0r, c128)
       << ", fi = tp ? " << lit(d1i, c128) << " : " << lit(d0i, c128) << "; const " << R() << " a = " << ur << ", b = "
       << ui << "; " << ur << " = a * fr - b * fi; " << ui << " = a * fi + b * fr; } }\n";
+    ops += 4;
     return true;
   }
 
@@ -221,9 +312,9 @@ struct Gen {
         const bool one = rp;
         if (one) {
           if (sign) o << "      " << re(i) << " = -" << re(i) << "; " << im(i) << " = -" << im(i) << ";\n";
-          else if (!d1one) cmul_into(i, d1r, d1i);
+          else if (!d1one) cmul_const(i, in.m[2], in.m[3]);
         } else if (!d0one) {
-          cmul_into(i, d0r, d0i);
+          cmul_const(i, in.m[0], in.m[1]);
         }
         continue;
       }
@@ -240,7 +331,7 @@ struct Gen {
   }
 };
 
-std::string jit_source(const PartPlan& pl, int dtype, int n_local) {
+std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_per_amp = nullptr) {
   Gen g;
   g.c128 = dtype == HS_C128;
   g.RB = pl.launch.RB;
@@ -312,12 +403,15 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local) {
     const bool ctl_t = in.ctid != 0;
     if (ctl_t) o << "    if ((t & " << in.ctid << "u) == " << in.ctid << "u) {\n";
     else o << "    {\n";
+    g.wgt = 1.0 / double(1u << __builtin_popcount(in.ctid));
     if (in.op == I_DENSE) g.dense(in);
     else if (in.op == I_PERM) g.perm(in, !ctl_t);
     else g.diag(in);
+    g.wgt = 1.0;
     o << "    }\n";
   }
-  g.flush();
+  g.flush(true);  // pending diagonal run + the part's scalar
+  if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
   if (pl.launch.fin_sync) o << "    __syncthreads();\n";
   g.emit_tdep("t", pl.launch.fin_npos);
   o << "    st = swz(t);\n";
@@ -376,7 +470,8 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
                         std::string& err) {
   const size_t n = plans.size();
   std::vector<std::string> srcs(n);
-  for (size_t i = 0; i < n; ++i) srcs[i] = jit_source(plans[i], dtype, n_local);
+  std::vector<double> fp64(n, 0.0);
+  for (size_t i = 0; i < n; ++i) srcs[i] = jit_source(plans[i], dtype, n_local, &fp64[i]);
   std::vector<int> status(n, HS_OK);
   std::vector<std::string> errs(n);
   unsigned hw = std::thread::hardware_concurrency();
@@ -395,6 +490,7 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
       return status[i];
     }
     cudaFuncSetAttribute((const void*)plans[i].jit, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+    plans[i].info.fp64_instr_per_amp = (float)fp64[i];
   }
   return HS_OK;
 }

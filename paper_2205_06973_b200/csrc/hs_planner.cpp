@@ -62,6 +62,84 @@ bool base_matrix(int kind, const double* p, double m[8]) {
   }
 }
 
+void component_coefs(const double* m, int c, double coef[4]) {
+  const double* a = m + (c < 2 ? 0 : 4);  // m00 or m10 (multiplies x)
+  const double* b = a + 2;                // m01 or m11 (multiplies y)
+  if ((c & 1) == 0) {  // real part: a.re x.re - a.im x.im + b.re y.re - b.im y.im
+    coef[0] = a[0]; coef[1] = -a[1]; coef[2] = b[0]; coef[3] = -b[1];
+  } else {             // imaginary part: a.im x.re + a.re x.im + b.im y.re + b.re y.im
+    coef[0] = a[1]; coef[1] = a[0]; coef[2] = b[1]; coef[3] = b[0];
+  }
+}
+
+int component_cost(const double coef[4]) {
+  int nz = 0;
+  bool unit = false;
+  for (int t = 0; t < 4; ++t) {
+    if (coef[t] == 0.0) continue;
+    ++nz;
+    unit |= coef[t] == 1.0 || coef[t] == -1.0;
+  }
+  return nz == 0 ? 0 : nz - (unit ? 1 : 0);
+}
+
+namespace {
+
+// snap entries within a few ulps of 0 / +-1 (relative to the largest entry)
+void snap8(double* m) {
+  double mx = 0;
+  for (int q = 0; q < 8; ++q) mx = std::max(mx, std::fabs(m[q]));
+  const double eps = 2e-15 * std::max(mx, 1.0);
+  for (int q = 0; q < 8; ++q) {
+    if (std::fabs(m[q]) < eps) m[q] = 0.0;
+    else if (std::fabs(m[q] - 1.0) < eps) m[q] = 1.0;
+    else if (std::fabs(m[q] + 1.0) < eps) m[q] = -1.0;
+  }
+}
+
+int cost8(const double* m) {
+  int c = 0;
+  for (int k = 0; k < 4; ++k) {
+    double coef[4];
+    component_coefs(m, k, coef);
+    c += component_cost(coef);
+  }
+  return c;
+}
+
+}  // namespace
+
+Mat2 structure_2x2(const double* m, bool allow_scale) {
+  Mat2 best;
+  best.s[0] = 1.0;
+  best.s[1] = 0.0;
+  std::memcpy(best.m, m, sizeof(best.m));
+  snap8(best.m);
+  best.cost = cost8(best.m);
+  if (!allow_scale) return best;
+  double mx = 0;
+  for (int e = 0; e < 4; ++e) mx = std::max(mx, std::hypot(m[2 * e], m[2 * e + 1]));
+  for (int e = 0; e < 4; ++e) {
+    const double sr = m[2 * e], si = m[2 * e + 1];
+    const double n2 = sr * sr + si * si;
+    if (!(n2 > 0) || std::sqrt(n2) < 1e-3 * mx) continue;  // keep M' entries O(1)
+    Mat2 c;
+    c.s[0] = sr;
+    c.s[1] = si;
+    for (int q = 0; q < 4; ++q) {  // m / s = m * conj(s) / |s|^2
+      const double xr = m[2 * q], xi = m[2 * q + 1];
+      c.m[2 * q] = (xr * sr + xi * si) / n2;
+      c.m[2 * q + 1] = (xi * sr - xr * si) / n2;
+    }
+    c.m[2 * e] = 1.0;  // exact by construction
+    c.m[2 * e + 1] = 0.0;
+    snap8(c.m);
+    c.cost = cost8(c.m);
+    if (c.cost < best.cost) best = c;
+  }
+  return best;
+}
+
 namespace {
 
 enum Cls { C_DENSE, C_PERM, C_DIAG, C_SWAP };
@@ -176,11 +254,32 @@ void mat_mul(const double* b, const double* a, double* c) {
     }
 }
 
-// Merge every run of uncontrolled single-qubit gates on one tile bit into
-// one 2x2 (their product); a gate touching that bit in any other way ends
-// the run. Gates on other bits commute with the run, so program order of
-// the remaining list is still a valid order of the part.
-void fuse_single_qubit_runs(std::vector<Gate>& gs, int T) {
+// FP64 instructions per amplitude pair a compiled kernel spends on an
+// uncontrolled gate (structure_2x2 for dense; a diagonal is normalised to
+// diag(1, d1/d0) with d0 pushed into the part's scalar)
+int compiled_cost(const Gate& G) {
+  if (G.cls == C_PERM || G.cls == C_SWAP) return 0;
+  if (G.cls == C_DIAG) {
+    const double ar = G.m[0], ai = G.m[1], br = G.m[6], bi = G.m[7];
+    const double n2 = ar * ar + ai * ai;
+    if (!(n2 > 0)) return 4;
+    double qr = (br * ar + bi * ai) / n2, qi = (bi * ar - br * ai) / n2;
+    if (std::fabs(qi) < 2e-15) qi = 0;
+    if (std::fabs(qr) < 2e-15) qr = 0;
+    if (qi == 0 && std::fabs(std::fabs(qr) - 1.0) < 2e-15) return 0;
+    if (qr == 0 && std::fabs(std::fabs(qi) - 1.0) < 2e-15) return 0;
+    return (qi == 0 || qr == 0) ? 2 : 4;
+  }
+  return structure_2x2(G.m, true).cost;
+}
+
+// Merge runs of uncontrolled single-qubit gates on one tile bit into one
+// 2x2 (their product); a gate touching that bit in any other way ends the
+// run. With `cost_aware` (compiled kernels, which exploit 0/+-1 entries) a
+// gate joins the run only if the product is no more expensive than the two
+// factors apart. Gates on other bits commute with the run, so program order
+// of the remaining list is still a valid order of the part.
+void fuse_single_qubit_runs(std::vector<Gate>& gs, int T, bool cost_aware) {
   std::vector<Gate> out;
   out.reserve(gs.size());
   std::vector<int> open(T, -1);
@@ -188,11 +287,13 @@ void fuse_single_qubit_runs(std::vector<Gate>& gs, int T) {
     if (G.cls != C_SWAP && G.nctl == 0 && G.par < 0) {
       int& o = open[G.tgt];
       if (o >= 0) {
-        double c[8];
-        mat_mul(G.m, out[o].m, c);
-        std::memcpy(out[o].m, c, sizeof(c));
-        classify(out[o]);
-        continue;
+        Gate F = out[o];
+        mat_mul(G.m, out[o].m, F.m);
+        classify(F);
+        if (!cost_aware || compiled_cost(F) <= compiled_cost(out[o]) + compiled_cost(G)) {
+          out[o] = F;
+          continue;
+        }
       }
       o = (int)out.size();
       out.push_back(G);
@@ -283,7 +384,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     classify(G);
   }
   const int input_gates = num_gates;
-  if (options & HS_PLAN_FUSE_1Q) fuse_single_qubit_runs(gs, T);
+  if (options & HS_PLAN_FUSE_1Q) fuse_single_qubit_runs(gs, T, (options & HS_PLAN_JIT) != 0);
   if (options & HS_PLAN_PARITY) fuse_parity_diagonals(gs);
   num_gates = (int)gs.size();
 

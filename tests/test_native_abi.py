@@ -44,7 +44,8 @@ def _emulate_parts(circuit, parts, tile_bits, dtype=0, rows=1, initial=None, opt
     return psi
 
 
-@pytest.mark.parametrize("tile_bits,options", [(12, 5), (13, 5), (6, 5), (12, 0), (12, 7), (13, 2), (12, 4)])
+@pytest.mark.parametrize("tile_bits,options",
+                         [(12, 5), (13, 5), (6, 5), (12, 0), (12, 7), (13, 2), (12, 4), (12, 0x15), (10, 0x17)])
 def test_planned_programs_match_oracle_on_corpus(golden, tile_bits, options):
     docs, states = golden.json("corpus"), golden.npz("corpus")
     for i, doc in enumerate(docs[:40]):
@@ -200,3 +201,43 @@ def test_compiled_part_sources_build_for_sm100a(tmp_path, name, dtype):
                               "-Xptxas", "-v"], capture_output=True, text=True)
         assert res.returncode == 0, res.stderr[-2000:]
         assert "hs_jit_part" in res.stderr
+
+
+def _structure(m, allow_scale=True):
+    import ctypes
+
+    D8 = ctypes.c_double * 8
+    a = D8(*np.asarray([[z.real, z.imag] for z in np.asarray(m).ravel()]).ravel())
+    s_out, m_out = (ctypes.c_double * 2)(), D8()
+    cost = _native.load().hs_structure_2x2(a, int(allow_scale), s_out, m_out)
+    mm = np.array([complex(m_out[2 * k], m_out[2 * k + 1]) for k in range(4)]).reshape(2, 2)
+    return complex(s_out[0], s_out[1]), mm, cost
+
+
+def test_structured_2x2_factorisation():
+    """Compiled kernels apply M as s * M' with M' snapped to 0/+-1 entries:
+    s * M' must equal M to rounding, and the c2/c4 gate set must get cheap."""
+    from paper_2205_06973_b200.statevec import gate_matrix
+
+    rng = np.random.default_rng(7)
+    cases = {
+        "sqrtX": (gate_matrix(GateKind.U3, (np.pi / 2, -np.pi / 2, np.pi / 2)), 4),
+        "sqrtY": (gate_matrix(GateKind.U3, (np.pi / 2, 0.0, 0.0)), 4),
+        "sqrtW": (gate_matrix(GateKind.U3, (np.pi / 2, -np.pi / 4, np.pi / 4)), 8),
+        "H": (gate_matrix(GateKind.H, ()), 4),
+        "RX": (gate_matrix(GateKind.RX, (0.37,)), 4),
+        "X": (gate_matrix(GateKind.X, ()), 0),
+        "Y": (gate_matrix(GateKind.Y, ()), 0),
+    }
+    for name, (m, want) in cases.items():
+        s, mm, cost = _structure(m)
+        assert np.max(np.abs(s * mm - m)) < 1e-15, name
+        assert cost == want, (name, cost)
+    for _ in range(200):
+        th, ph, la = rng.uniform(0, 2 * np.pi, 3)
+        m = gate_matrix(GateKind.U3, (th, ph, la)) * np.exp(1j * rng.uniform(0, 2 * np.pi))
+        s, mm, cost = _structure(m)
+        assert np.max(np.abs(s * mm - m)) < 1e-14
+        assert cost <= 12  # one entry normalised to 1: 2+2+4+4
+        s0, mm0, cost0 = _structure(m, allow_scale=False)
+        assert s0 == 1 and cost0 <= 16 and np.max(np.abs(mm0 - m)) < 1e-15
