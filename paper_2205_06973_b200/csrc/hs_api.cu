@@ -212,10 +212,11 @@ static int run_range(hs_program* prog, void* state, int64_t batch, int first, in
       long long ntiles = (long long)(batch << (prog->n_local - pl.launch.T));
       void* psi = state;
       void* args[] = {&psi, &ntiles};
-      const size_t smem = size_t(prog->dtype == HS_C128 ? 16 : 8) << pl.launch.T;
-      long long grid = (long long)eng->num_sms * 2;
-      if (grid > ntiles) grid = ntiles;
-      HS_CUDA(cudaLaunchKernel((const void*)pl.jit, dim3((unsigned)grid), dim3(1u << (pl.launch.T - pl.launch.RB)),
+      // one CTA per SM, two teams, three tile buffers + their mbarriers (hs_jit.cpp)
+      const size_t smem = 3 * (size_t(prog->dtype == HS_C128 ? 16 : 8) << pl.launch.T) + 64;
+      long long grid = (long long)eng->num_sms;
+      if (grid > (ntiles + 1) / 2) grid = (ntiles + 1) / 2;
+      HS_CUDA(cudaLaunchKernel((const void*)pl.jit, dim3((unsigned)grid), dim3(2u << (pl.launch.T - pl.launch.RB)),
                                args, smem, s),
               "compiled part kernel launch");
       continue;

@@ -36,6 +36,8 @@ uint32_t swz_host(uint32_t s, bool c128) {
   return s ^ (((s >> 4) ^ (s >> 8) ^ (s >> 12)) & 15u);
 }
 
+int sizeof_amp(bool c128) { return c128 ? 16 : 8; }
+
 std::string lit(double v, bool c128) {
   char buf[64];
   std::snprintf(buf, sizeof(buf), "%a", v);
@@ -347,40 +349,84 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "__device__ __forceinline__ unsigned swz(unsigned s) { return s ^ "
     << (g.c128 ? "(((s >> 3) ^ (s >> 6) ^ (s >> 9) ^ (s >> 12)) & 7u)" : "(((s >> 4) ^ (s >> 8) ^ (s >> 12)) & 15u)")
     << "; }\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", 2) hs_jit_part(C* __restrict__ psi, long long ntiles) {\n";
-  o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n  C* sm = reinterpret_cast<C*>(smem_raw);\n";
-  o << "  const unsigned tid = threadIdx.x;\n";
+  // One CTA per SM: two teams of NT threads each run the part on their own
+  // tiles (team 0 takes the CTA's even tiles, team 1 the odd ones) in one of
+  // three shared-memory tile buffers; the third buffer receives the tile
+  // after next while both teams compute. Tile i of the CTA lives in buffer
+  // i % 3; whichever team finishes tile i refills that buffer with tile
+  // i + 3 (cp.async, completion counted on the buffer's mbarrier by
+  // cp.async.mbarrier.arrive.noinc), so loads stay in flight across tiles.
+  // Teams synchronise with named barriers (1 + team).
+  const int tile_bytes = (g.c128 ? 16 : 8) << T;
+  if (NT >= 32)
+    o << "#define TEAM_SYNC() asm volatile(\"bar.sync %0, " << NT << ";\" :: \"r\"(bar_id) : \"memory\")\n";
+  else  // tiny tiles: both teams share warp 0
+    o << "#define TEAM_SYNC() __syncwarp(" << ((1ull << NT) - 1) << "u << (team * " << NT << "u))\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * NT << ", 1) hs_jit_part(C* __restrict__ psi, long long ntiles) {\n";
+  o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
+  o << "  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + " << 3 * tile_bytes << ");\n";
+  o << "  volatile int* issued = reinterpret_cast<volatile int*>(smem_raw + " << 3 * tile_bytes + 32 << ");\n";
+  o << "  const unsigned team = threadIdx.x >> " << low << ";\n";
+  o << "  const unsigned tid = threadIdx.x & " << (NT - 1) << "u;\n";
+  o << "  const unsigned bar_id = 1u + team;\n";
+  o << "  if (threadIdx.x == 0) {\n";
+  o << "    for (int b = 0; b < 3; ++b) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << NT
+    << ";\" :: \"r\"((unsigned)__cvta_generic_to_shared(&full[b])) : \"memory\");\n";
+  o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+  o << "    for (int b = 0; b < 3; ++b) issued[b] = 0;\n  }\n";
+  o << "  __syncthreads();\n";
   // canonical load order: slot s = tid + (j << low); global offset of tid part
   o << "  unsigned long long ga_tid = 0ull";
   for (int b = 0; b < low; ++b) o << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << (int)pl.launch.tpos[b] << ")";
   o << ";\n  const unsigned sw_tid = swz(tid);\n";
-  uint64_t tile_mask = 0;
-  for (int b = 0; b < T; ++b) tile_mask |= 1ull << pl.launch.tpos[b];
-  o << "  for (long long tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {\n";
+  // tile -> global offset of its slot 0 (zero bits inserted at the tile positions)
+  o << "  auto tile_base = [&](long long tt) -> unsigned long long {\n";
   o << "    const unsigned long long row = (unsigned long long)tt >> " << (n_local - T) << ";\n";
   o << "    unsigned long long f = (unsigned long long)tt & " << ((1ull << (n_local - T)) - 1) << "ull;\n";
   for (int b = 0; b < T; ++b) {
     int p = pl.launch.tpos[b];
     o << "    { const unsigned long long lo = f & " << ((1ull << p) - 1) << "ull; f = ((f ^ lo) << 1) | lo; }\n";
   }
-  o << "    const unsigned long long base = (row << " << n_local << ") | f | ga_tid;\n";
-  auto io = [&](bool load) {
-    for (int j = 0; j < g.nreg; ++j) {
-      uint64_t hi = 0;
-      for (int k = 0; k < RB; ++k)
-        if (j >> k & 1) hi |= 1ull << pl.launch.tpos[low + k];
-      const uint32_t sx = swz_host(uint32_t(j) << low, g.c128);
-      if (load)
-        o << "    { const unsigned s = (unsigned)__cvta_generic_to_shared(&sm[sw_tid ^ " << sx << "u]);\n"
-          << "      asm volatile(\"cp.async." << (g.c128 ? "cg" : "ca") << ".shared.global [%0], [%1], "
-          << (g.c128 ? 16 : 8) << ";\" :: \"r\"(s), \"l\"(psi + (base | " << hi << "ull))); }\n";
-      else
-        o << "    psi[base | " << hi << "ull] = sm[sw_tid ^ " << sx << "u];\n";
-    }
+  o << "    return (row << " << n_local << ") | f | ga_tid;\n  };\n";
+  auto hi_of = [&](int j) {
+    uint64_t hi = 0;
+    for (int k = 0; k < RB; ++k)
+      if (j >> k & 1) hi |= 1ull << pl.launch.tpos[low + k];
+    return hi;
   };
-  io(true);
-  o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\" ::: \"memory\");\n";
-  o << "    __syncthreads();\n";
+  // issue the loads of CTA tile i into buffer i % 3 (this thread's share)
+  o << "  auto issue = [&](long long i) {\n";
+  o << "    const long long tt = blockIdx.x + i * (long long)gridDim.x;\n";
+  o << "    if (tt >= ntiles) return;\n";
+  o << "    const unsigned long long base = tile_base(tt);\n";
+  o << "    const int b = (int)(i % 3);\n";
+  o << "    const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_raw) + b * " << tile_bytes << "u;\n";
+  for (int j = 0; j < g.nreg; ++j) {
+    const uint32_t sx = swz_host(uint32_t(j) << low, g.c128);
+    o << "    asm volatile(\"cp.async." << (g.c128 ? "cg" : "ca") << ".shared.global [%0], [%1], "
+      << (g.c128 ? 16 : 8) << ";\" :: \"r\"(sb + (sw_tid ^ " << sx << "u) * " << sizeof_amp(g.c128)
+      << "u), \"l\"(psi + (base | " << hi_of(j) << "ull)) : \"memory\");\n";
+  }
+  o << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"((unsigned)__cvta_generic_to_shared(&full[b])) : \"memory\");\n";
+  o << "    if (tid == 0) issued[b] = (int)(i / 3);\n";
+  o << "  };\n";
+  o << "  issue(team);\n  if (team == 0) issue(2);\n";
+  o << "  for (long long i = team;; i += 2) {\n";
+  o << "    const long long tt = blockIdx.x + i * (long long)gridDim.x;\n";
+  o << "    if (tt >= ntiles) break;\n";
+  o << "    const unsigned long long base = tile_base(tt);\n";
+  o << "    const int b = (int)(i % 3);\n";
+  o << "    C* sm = reinterpret_cast<C*>(smem_raw + b * " << tile_bytes << ");\n";
+  // Fill k = i / 3 of buffer b. This team can get here before the other
+  // team has even issued fill k (it is still on tile i - 3), and a parity
+  // wait cannot tell phase k from phase k - 2. The producer publishes the
+  // fill number it issued (issued[b]); once it reads k, phase k is the
+  // newest phase that can complete and the parity wait is unambiguous.
+  o << "    { const long long k = i / 3;\n";
+  o << "      if (k > 0) while (issued[b] < (int)k) __nanosleep(20);\n";
+  o << "      const unsigned mb = (unsigned)__cvta_generic_to_shared(&full[b]); const unsigned par = (unsigned)(k & 1);\n";
+  o << "      unsigned done = 0;\n";
+  o << "      while (!done) asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\" : \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\"); }\n";
   o << "    " << g.R() << " ";
   for (int i = 0; i < g.nreg; ++i) o << (i ? ", " : "") << "r" << i << ", q" << i;
   o << ";\n    unsigned t, st;\n";
@@ -392,7 +438,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
     if (in.op == I_PHASE) {
       if (cur) {
         g.store_regs(cur->rpos);
-        o << "    __syncthreads();\n";
+        o << "    TEAM_SYNC();\n";
       }
       g.emit_tdep("t", in.npos);
       o << "    st = swz(t);\n";
@@ -412,13 +458,18 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   }
   g.flush(true);  // pending diagonal run + the part's scalar
   if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
-  if (pl.launch.fin_sync) o << "    __syncthreads();\n";
+  if (pl.launch.fin_sync) o << "    TEAM_SYNC();\n";
   g.emit_tdep("t", pl.launch.fin_npos);
   o << "    st = swz(t);\n";
   g.store_regs(pl.launch.fin_rpos);
-  o << "    __syncthreads();\n";
-  io(false);
-  o << "    __syncthreads();\n  }\n}\n";
+  o << "    TEAM_SYNC();\n";
+  for (int j = 0; j < g.nreg; ++j) {
+    const uint32_t sx = swz_host(uint32_t(j) << low, g.c128);
+    o << "    psi[base | " << hi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
+  }
+  o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
+  o << "    issue(i + 3);\n";
+  o << "  }\n}\n";
   return o.str();
 }
 
