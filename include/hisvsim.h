@@ -115,6 +115,16 @@ typedef struct {
  * are compiled in parallel and cached per process); if NVRTC fails the
  * interpreter kernel runs the same program */
 #define HS_PLAN_JIT 0x10u
+/* with HS_PLAN_LAYOUT: the program expects its initial state in a planned
+ * layout (hs_program_initial_layout) instead of natural order. Meant for
+ * basis-state starts, which are one amplitude in any layout. */
+#define HS_PLAN_INIT_LAYOUT 0x20u
+/* with HS_PLAN_LAYOUT: parts run out of place, alternating between the state
+ * and a scratch buffer of the same size (hs_program_bind_scratch), so each
+ * part can write any layout: the next part's qubits on the lowest bits, and
+ * the last part natural order (no restore launches). An odd part count runs
+ * part 0 in place. */
+#define HS_PLAN_PINGPONG 0x40u
 #define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
 
 typedef struct hs_engine hs_engine;
@@ -141,6 +151,13 @@ int hs_program_num_parts(hs_program* prog);
 int hs_program_num_launches(hs_program* prog);
 /* per launch (index < num_launches) */
 int hs_program_part_info(hs_program* prog, int part, hs_part_info* out);
+/* physical bit of each logical position in the state the program expects
+ * (phys[n_local]; identity unless HS_PLAN_INIT_LAYOUT). Basis state |x>
+ * lives at index sum_q bit_q(x) << phys[q]. */
+int hs_program_initial_layout(hs_program* prog, int32_t* phys);
+/* scratch buffer for HS_PLAN_PINGPONG programs: device memory of at least
+ * the state's size, owned by the caller, used by every later run */
+int hs_program_bind_scratch(hs_program* prog, void* scratch, size_t bytes);
 /* empty unless HS_PLAN_JIT compilation failed (the interpreter then runs) */
 const char* hs_program_jit_error(hs_program* prog);
 /* device instructions of one launch, copied to host (test/debug); returns the

@@ -28,7 +28,9 @@ HS_MAX_STAGED = 24
 EXPORTS = (
     "hs_last_error", "hs_abi_version", "hs_engine_create", "hs_engine_destroy",
     "hs_engine_query", "hs_engine_set_options", "hs_program_create", "hs_program_destroy",
-    "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_jit_error",
+    "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_initial_layout",
+    "hs_program_bind_scratch",
+    "hs_program_jit_error",
     "hs_program_dump",
     "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_jit_source", "hs_structure_2x2", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
@@ -94,6 +96,8 @@ def _declare(lib) -> None:
         "hs_program_num_parts": (I, [P]),
         "hs_program_num_launches": (I, [P]),
         "hs_program_jit_error": (ctypes.c_char_p, [P]),
+        "hs_program_initial_layout": (I, [P, ctypes.POINTER(ctypes.c_int32)]),
+        "hs_program_bind_scratch": (I, [P, P, ctypes.c_size_t]),
         "hs_program_part_info": (I, [P, I, ctypes.POINTER(HsPartInfo)]),
         "hs_program_dump": (I, [P, I, P, ctypes.c_size_t, ctypes.POINTER(I),
                                 ctypes.POINTER(ctypes.c_size_t)]),
@@ -181,6 +185,7 @@ def engine_query(device: int) -> dict:
 
 
 HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY, HS_PLAN_LAYOUT, HS_PLAN_JIT = 0x1, 0x2, 0x4, 0x8, 0x10
+HS_PLAN_INIT_LAYOUT, HS_PLAN_PINGPONG = 0x20, 0x40
 HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY
 
 

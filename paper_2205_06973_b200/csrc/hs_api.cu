@@ -13,7 +13,7 @@
 
 namespace hs {
 cudaError_t prepare_kernels(int smem_optin);
-cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void* psi, int n_local,
+cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void* psi, void* psi_out, int n_local,
                         int64_t batch, int num_sms, cudaStream_t stream);
 cudaError_t launch_set_basis(void* psi, int dtype, int64_t index, cudaStream_t s);
 cudaError_t launch_bit_permute(const void* in, void* out, int nbits, int dtype, const int32_t* dst_of,
@@ -42,11 +42,15 @@ struct hs_program {
   int n_local = 0;
   int dtype = 0;
   int user_parts = 0;            // plans beyond this are layout-restore launches
+  std::vector<int32_t> init_phys; // layout the program expects its input in
+  void* scratch = nullptr;        // HS_PLAN_PINGPONG partner buffer (caller-owned)
+  size_t scratch_bytes = 0;
   std::string jit_error;         // why HS_PLAN_JIT fell back to the interpreter
   std::vector<PartPlan> plans;
   Instr* d_prog = nullptr;
   cudaGraphExec_t graph = nullptr;
   void* graph_state = nullptr;
+  void* graph_scratch = nullptr;
   int64_t graph_batch = 0;
   cudaStream_t graph_stream = nullptr;
 };
@@ -139,7 +143,7 @@ int hs_program_create(hs_engine* eng, int n_local, int dtype, const hs_part* par
   {
     std::string err;
     int s = plan_program(n_local, dtype, tile_for(eng, dtype), eng->options, parts, num_parts, gates, num_gates,
-                         prog->plans, err);
+                         prog->plans, err, &prog->init_phys);
     if (s != HS_OK) return fail(s, err);
   }
   prog->user_parts = num_parts;
@@ -206,12 +210,18 @@ int hs_program_dump(hs_program* prog, int part, void* buf, size_t buf_bytes, int
 
 static int run_range(hs_program* prog, void* state, int64_t batch, int first, int count, cudaStream_t s) {
   hs_engine* eng = prog->eng;
+  const size_t need = size_t(batch) << prog->n_local;
   for (int i = first; i < first + count; ++i) {
     const PartPlan& pl = prog->plans[i];
+    if ((pl.launch.in_buf || pl.launch.out_buf) &&
+        (!prog->scratch || prog->scratch_bytes < need * (prog->dtype == HS_C128 ? 16 : 8)))
+      return fail(HS_ERR_INVALID, "ping-pong program: bind a scratch buffer of the state's size first");
+    void* bufs[2] = {state, prog->scratch};
+    void* psi = bufs[pl.launch.in_buf];
+    void* psi_out = bufs[pl.launch.out_buf];
     if (pl.jit) {
       long long ntiles = (long long)(batch << (prog->n_local - pl.launch.T));
-      void* psi = state;
-      void* args[] = {&psi, &ntiles};
+      void* args[] = {&psi, &psi_out, &ntiles};
       // one CTA per SM, two teams, three tile buffers + their mbarriers (hs_jit.cpp)
       const size_t smem = 3 * (size_t(prog->dtype == HS_C128 ? 16 : 8) << pl.launch.T) + 64;
       long long grid = (long long)eng->num_sms;
@@ -221,9 +231,23 @@ static int run_range(hs_program* prog, void* state, int64_t batch, int first, in
               "compiled part kernel launch");
       continue;
     }
-    HS_CUDA(launch_part(prog->dtype, pl.launch, prog->d_prog, state, prog->n_local, batch, eng->num_sms, s),
+    HS_CUDA(launch_part(prog->dtype, pl.launch, prog->d_prog, psi, psi_out, prog->n_local, batch, eng->num_sms, s),
             "part kernel launch");
   }
+  return HS_OK;
+}
+
+int hs_program_bind_scratch(hs_program* prog, void* scratch, size_t bytes) {
+  if (!prog) return fail(HS_ERR_INVALID, "program is NULL");
+  prog->scratch = scratch;
+  prog->scratch_bytes = scratch ? bytes : 0;
+  return HS_OK;
+}
+
+int hs_program_initial_layout(hs_program* prog, int32_t* phys) {
+  if (!prog || !phys) return fail(HS_ERR_INVALID, "program/phys is NULL");
+  for (int q = 0; q < prog->n_local; ++q)
+    phys[q] = q < (int)prog->init_phys.size() ? prog->init_phys[q] : q;
   return HS_OK;
 }
 
@@ -242,7 +266,7 @@ int hs_program_run_graph(hs_program* prog, void* state, int64_t batch, void* str
   if (!prog || !state) return fail(HS_ERR_INVALID, "program/state is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   HS_CUDA(cudaSetDevice(prog->eng->device), "cudaSetDevice");
-  if (prog->graph && (prog->graph_state != state || prog->graph_batch != batch)) {
+  if (prog->graph && (prog->graph_state != state || prog->graph_batch != batch || prog->graph_scratch != prog->scratch)) {
     cudaGraphExecDestroy(prog->graph);
     prog->graph = nullptr;
   }
@@ -265,6 +289,7 @@ int hs_program_run_graph(hs_program* prog, void* state, int64_t batch, void* str
     if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
     prog->graph_state = state;
     prog->graph_batch = batch;
+    prog->graph_scratch = prog->scratch;
   }
   HS_CUDA(cudaGraphLaunch(prog->graph, s), "graph launch");
   return HS_OK;

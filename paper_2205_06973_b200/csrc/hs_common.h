@@ -51,7 +51,17 @@ struct PartLaunch {
   uint8_t tpos[16];     // ascending physical positions of the tile
   uint8_t fin_rpos[MAX_RB];
   uint8_t fin_npos[MAX_NPOS];
+  // out-of-place launches (HS_PLAN_PINGPONG): the tile is read from buffer
+  // in_buf and written to buffer out_buf (0 = state, 1 = scratch) under the
+  // next layout: store slot bit r goes to physical position opos[r]
+  // (ascending) and free (tile index) bit j to fpos[j]
+  int32_t oop;
+  int32_t in_buf, out_buf;
+  int32_t pad_;
+  uint8_t opos[16];
+  uint8_t fpos[56];
 };
+static_assert(sizeof(PartLaunch) == 144, "PartLaunch layout");
 
 struct PartPlan {
   PartLaunch launch;
@@ -69,7 +79,8 @@ std::string jit_source_for(const PartPlan& pl, int dtype, int n_local);
 // Program-level qubit layout: logical position q (what parts stage) lives at
 // physical bit phys[q] of the buffer. A part's write-back may permute the
 // positions inside its tile (see hs_planner.cpp); inv is phys^-1.
-enum { LAYOUT_KEEP = 0, LAYOUT_PRIORITY = 1, LAYOUT_TARGET = 2 };
+// LAYOUT_OOP: out-of-place launch, target = the complete next layout
+enum { LAYOUT_KEEP = 0, LAYOUT_PRIORITY = 1, LAYOUT_TARGET = 2, LAYOUT_OOP = 3 };
 struct LayoutIO {
   const int32_t* phys_in = nullptr;   // null = identity
   const int32_t* inv_in = nullptr;
@@ -87,7 +98,8 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
 // Plan a whole part sequence (with HS_PLAN_LAYOUT: evolving layout plus the
 // restore launches that bring every qubit home at the end).
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
-                 const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err);
+                 const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
+                 std::vector<int32_t>* init_phys = nullptr);
 
 // 2x2 base matrix of a gate kind (controls handled by masking), row-major
 // complex: m[0..7] = m00 re/im, m01, m10, m11. Mirrors statevec.py:33-98.

@@ -362,7 +362,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
     o << "#define TEAM_SYNC() asm volatile(\"bar.sync %0, " << NT << ";\" :: \"r\"(bar_id) : \"memory\")\n";
   else  // tiny tiles: both teams share warp 0
     o << "#define TEAM_SYNC() __syncwarp(" << ((1ull << NT) - 1) << "u << (team * " << NT << "u))\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * NT << ", 1) hs_jit_part(C* __restrict__ psi, long long ntiles) {\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * NT << ", 1) hs_jit_part(C* psi, C* psi_out, long long ntiles) {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
   o << "  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + " << 3 * tile_bytes << ");\n";
   o << "  volatile int* issued = reinterpret_cast<volatile int*>(smem_raw + " << 3 * tile_bytes + 32 << ");\n";
@@ -388,6 +388,23 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
     o << "    { const unsigned long long lo = f & " << ((1ull << p) - 1) << "ull; f = ((f ^ lo) << 1) | lo; }\n";
   }
   o << "    return (row << " << n_local << ") | f | ga_tid;\n  };\n";
+  const bool oop = pl.launch.oop != 0;
+  if (oop) {  // out of place: the same tile under the next layout
+    o << "  unsigned long long go_tid = 0ull";
+    for (int b = 0; b < low; ++b) o << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << (int)pl.launch.opos[b] << ")";
+    o << ";\n";
+    o << "  auto out_base = [&](long long tt) -> unsigned long long {\n";
+    o << "    const unsigned long long f = (unsigned long long)tt;\n";
+    o << "    return ((f >> " << (n_local - T) << ") << " << n_local << ") | go_tid";
+    for (int j = 0; j < n_local - T; ++j) o << "\n      | (((f >> " << j << ") & 1ull) << " << (int)pl.launch.fpos[j] << ")";
+    o << ";\n  };\n";
+  }
+  auto ohi_of = [&](int j) {
+    uint64_t hi = 0;
+    for (int k = 0; k < RB; ++k)
+      if (j >> k & 1) hi |= 1ull << (oop ? pl.launch.opos[low + k] : pl.launch.tpos[low + k]);
+    return hi;
+  };
   auto hi_of = [&](int j) {
     uint64_t hi = 0;
     for (int k = 0; k < RB; ++k)
@@ -458,14 +475,16 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   }
   g.flush(true);  // pending diagonal run + the part's scalar
   if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
+  o << "    // fp64_instr_per_amp " << g.ops / g.nreg << "\n";
   if (pl.launch.fin_sync) o << "    TEAM_SYNC();\n";
   g.emit_tdep("t", pl.launch.fin_npos);
   o << "    st = swz(t);\n";
   g.store_regs(pl.launch.fin_rpos);
   o << "    TEAM_SYNC();\n";
+  if (oop) o << "    const unsigned long long obase = out_base(tt);\n";
   for (int j = 0; j < g.nreg; ++j) {
     const uint32_t sx = swz_host(uint32_t(j) << low, g.c128);
-    o << "    psi[base | " << hi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
+    o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
   }
   o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
   o << "    issue(i + 3);\n";

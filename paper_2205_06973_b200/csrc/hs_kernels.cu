@@ -55,6 +55,10 @@ __constant__ Instr c_prog[CPROG_MAX];
 
 struct KParams {
   void* psi;
+  void* psi_out;       // == psi unless out of place
+  int32_t oop;
+  uint64_t opos0, opos1;  // out of place: store slot bit r -> physical position
+  uint64_t fpos[7];       // out of place: free bit j -> physical position (byte j)
   const Instr* prog;
   int64_t ntiles;      // batch * 2^(n_local - T)
   int32_t nprog;
@@ -297,8 +301,27 @@ hs_part_kernel(const KParams p) {
 #pragma unroll
   for (int k = 0; k < RB; ++k) ga_hi[k] = uint64_t(1) << byte_of(p.tpos0, p.tpos1, lowbits + k);
 
+  uint64_t go_tid = ga_tid;
+  uint64_t go_hi[RB];
+#pragma unroll
+  for (int k = 0; k < RB; ++k) go_hi[k] = ga_hi[k];
+  if (p.oop) {
+    go_tid = 0;
+    for (int b = 0; b < lowbits; ++b) go_tid |= uint64_t((tid >> b) & 1u) << byte_of(p.opos0, p.opos1, b);
+#pragma unroll
+    for (int k = 0; k < RB; ++k) go_hi[k] = uint64_t(1) << byte_of(p.opos0, p.opos1, lowbits + k);
+  }
+  C* psi_out = reinterpret_cast<C*>(p.psi_out);
+
   for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
     const uint64_t base = tile_base((uint64_t)t, p) | ga_tid;
+    uint64_t obase = base;
+    if (p.oop) {
+      const int fb = p.n_local - p.T;
+      obase = ((uint64_t(t) >> fb) << p.n_local) | go_tid;
+      for (int j = 0; j < fb; ++j)
+        obase |= ((uint64_t(t) >> j) & 1ull) << ((p.fpos[j >> 3] >> (8 * (j & 7))) & 0xFF);
+    }
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
       uint64_t off = base;
@@ -340,12 +363,12 @@ hs_part_kernel(const KParams p) {
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) {
-      uint64_t off = base;
+      uint64_t off = obase;
 #pragma unroll
       for (int k = 0; k < RB; ++k)
-        if (j & (1 << k)) off |= ga_hi[k];
+        if (j & (1 << k)) off |= go_hi[k];
       const uint32_t s = tid + (uint32_t(j) << lowbits);
-      psi[off] = sm[swz<R>(s)];
+      psi_out[off] = sm[swz<R>(s)];
     }
     __syncthreads();
   }
@@ -389,10 +412,18 @@ cudaError_t prepare_kernels(int smem_optin) {
   return cudaSuccess;
 }
 
-cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void* psi,
+cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void* psi, void* psi_out,
                         int n_local, int64_t batch, int num_sms, cudaStream_t stream) {
   KParams p;
   p.psi = psi;
+  p.psi_out = psi_out;
+  p.oop = L.oop;
+  p.opos0 = p.opos1 = 0;
+  for (int b = 0; b < 16; ++b) (b < 8 ? p.opos0 : p.opos1) |= uint64_t(L.opos[b]) << (8 * (b & 7));
+  for (int w = 0; w < 7; ++w) {
+    p.fpos[w] = 0;
+    for (int b = 0; b < 8; ++b) p.fpos[w] |= uint64_t(L.fpos[8 * w + b]) << (8 * b);
+  }
   p.prog = dprog + L.prog_offset;
   p.nprog = L.nprog;
   p.n_local = n_local;

@@ -530,7 +530,17 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       auto it = std::find(tile.begin(), tile.end(), p);
       return it == tile.end() ? -1 : int(it - tile.begin());
     };
-    if (lay->mode == LAYOUT_PRIORITY) {
+    if (lay->mode == LAYOUT_OOP) {
+      // out of place: store slot bit r = the r-th lowest output position
+      // among the tile's qubits
+      std::vector<int> outp(T);
+      for (int b = 0; b < T; ++b) outp[b] = lay->target[occ[b]];
+      for (int b = 0; b < T; ++b) {
+        int r = 0;
+        for (int c = 0; c < T; ++c) r += outp[c] < outp[b];
+        rho[b] = r;
+      }
+    } else if (lay->mode == LAYOUT_PRIORITY) {
       // the lowest 3 tile positions (the coalescing bits when they are the
       // physical bits 0..2) go to the qubits staged soonest; qubits never
       // staged again go home when home is in the tile (less to restore at
@@ -574,8 +584,12 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         taken[next] = 1;
       }
     }
-    if (lay->phys_out)
-      for (int b = 0; b < T; ++b) lay->phys_out[occ[b]] = tile[rho[b]];
+    if (lay->phys_out) {
+      if (lay->mode == LAYOUT_OOP)
+        for (int q = 0; q < n_local; ++q) lay->phys_out[q] = lay->target[q];
+      else
+        for (int b = 0; b < T; ++b) lay->phys_out[occ[b]] = tile[rho[b]];
+    }
   }
   // final store: register k holds location R[k] of the last phase, which is
   // tile bit bit_at[R[k]]; it is written to tile position rho[bit_at[R[k]]]
@@ -592,6 +606,22 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   L.fin_sync = ident ? 0 : 1;
   for (int k = 0; k < RB; ++k) L.fin_rpos[k] = (uint8_t)rho[bit_at[last->rpos[k]]];
   for (int m = 0; m < T - RB; ++m) L.fin_npos[m] = (uint8_t)rho[bit_at[last->npos[m]]];
+  if (lay && lay->mode == LAYOUT_OOP) {
+    L.oop = 1;
+    std::vector<int> outp;
+    for (int b = 0; b < T; ++b) {
+      const int q = lay->inv_in ? lay->inv_in[tile[b]] : tile[b];
+      outp.push_back(lay->target[q]);
+    }
+    std::sort(outp.begin(), outp.end());
+    for (int r = 0; r < T; ++r) L.opos[r] = (uint8_t)outp[r];
+    int j = 0;
+    for (int p = 0; p < n_local; ++p) {
+      if (std::find(tile.begin(), tile.end(), p) != tile.end()) continue;
+      const int q = lay->inv_in ? lay->inv_in[p] : p;
+      L.fpos[j++] = (uint8_t)lay->target[q];
+    }
+  }
 
   hs_part_info& I = P.info;
   I.tile_bits = T;
@@ -662,11 +692,31 @@ int plan_restore(int n_local, int dtype, int tile_max, uint32_t options, std::ve
 }  // namespace
 
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
-                 const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err) {
+                 const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
+                 std::vector<int32_t>* init_phys) {
   plans.assign(num_parts, PartPlan());
   const bool layout = (options & HS_PLAN_LAYOUT) && num_parts > 0 && n_local > 0;
   std::vector<int32_t> phys(std::max(n_local, 1)), inv(std::max(n_local, 1));
   for (int q = 0; q < n_local; ++q) phys[q] = inv[q] = q;
+  if (layout && (options & HS_PLAN_INIT_LAYOUT)) {
+    // the state starts as a basis state, which is one amplitude in any
+    // layout: start with part 0's qubits on the lowest positions (its reads
+    // become one contiguous run per tile); qubits whose home they take move
+    // to the homes those qubits vacate
+    const hs_part& p0 = parts[0];
+    std::vector<char> in0(n_local, 0);
+    for (int j = 0; j < p0.num_staged; ++j)
+      if (p0.staged[j] >= 0 && p0.staged[j] < n_local) in0[p0.staged[j]] = 1;
+    std::vector<int32_t> vacated;
+    int pos = 0;
+    for (int q = 0; q < n_local; ++q)
+      if (in0[q]) { phys[q] = pos++; if (q >= p0.num_staged) vacated.push_back(q); }
+    size_t v = 0;
+    for (int q = 0; q < p0.num_staged && q < n_local; ++q)
+      if (!in0[q]) phys[q] = vacated[v++];
+    for (int q = 0; q < n_local; ++q) inv[phys[q]] = q;
+  }
+  if (init_phys) init_phys->assign(phys.begin(), phys.begin() + n_local);
   // next_use[i][q]: parts after i until q is staged again (large = never)
   std::vector<std::vector<int32_t>> next_use;
   if (layout) {
@@ -684,6 +734,24 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
   }
   std::vector<int32_t> home(std::max(n_local, 1));
   for (int q = 0; q < n_local; ++q) home[q] = q;
+  // ping-pong: out-of-place parts alternate state -> scratch -> state; an
+  // odd part count runs part 0 in place so the last part lands in the state
+  const bool pp = layout && (options & HS_PLAN_PINGPONG) && num_parts >= 2;
+  const int hot = std::min(dtype == HS_C128 ? 3 : 4, n_local);  // lowest positions = 128 B runs
+  // the last part writes natural order directly only if qubits 0..hot-1 are
+  // among its own (coalesced stores); otherwise it writes a coalesced layout
+  // and one gate-free out-of-place launch permutes into natural order
+  bool need_restore = false;
+  if (pp) {
+    const hs_part& pl = parts[num_parts - 1];
+    for (int q = 0; q < hot; ++q) {
+      bool in = false;
+      for (int j = 0; j < pl.num_staged; ++j) in |= pl.staged[j] == q;
+      need_restore |= !in;
+    }
+  }
+  const bool first_inplace = pp && ((num_parts + (need_restore ? 1 : 0)) % 2 == 1);
+  int cur_buf = 0;
   for (int i = 0; i < num_parts; ++i) {
     const hs_part& p = parts[i];
     if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates) {
@@ -692,13 +760,60 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     }
     LayoutIO lay;
     std::vector<int32_t> next(phys);
-    if (layout) {
+    std::vector<int32_t> tgt(phys);
+    const bool oop = pp && !(first_inplace && i == 0);
+    if (oop) {
+      lay.phys_in = phys.data();
+      lay.inv_in = inv.data();
+      lay.phys_out = next.data();
+      lay.mode = LAYOUT_OOP;
+      if (i + 1 == num_parts && !need_restore) {
+        for (int q = 0; q < n_local; ++q) tgt[q] = q;  // the last part writes natural order
+      } else {
+        // the next layout: this tile's qubits that the next part stages go
+        // to the lowest positions (coalesced stores now, coalesced loads
+        // next), then other tile qubits; everything else stays put (swaps)
+        const int w = std::max(0, std::min(p.num_staged, HS_MAX_STAGED));
+        const int T = std::min(std::max(tile_max, w), n_local);
+        std::vector<int> tpos;
+        for (int j = 0; j < w; ++j)
+          if (p.staged[j] >= 0 && p.staged[j] < n_local) tpos.push_back(phys[p.staged[j]]);
+        for (int q = 0; (int)tpos.size() < T && q < n_local; ++q)
+          if (std::find(tpos.begin(), tpos.end(), q) == tpos.end()) tpos.push_back(q);
+        std::sort(tpos.begin(), tpos.end());
+        std::vector<char> nxt(n_local, 0);
+        if (i + 1 < num_parts) {
+          const hs_part& p1 = parts[i + 1];
+          for (int j = 0; j < p1.num_staged; ++j)
+            if (p1.staged[j] >= 0 && p1.staged[j] < n_local) nxt[p1.staged[j]] = 1;
+        } else {
+          for (int q = 0; q < hot; ++q) nxt[q] = 1;  // the restore launch stages 0..hot-1
+        }
+        std::vector<int> cand;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int pp_ : tpos)
+            if ((nxt[inv[pp_]] != 0) == (pass == 0)) cand.push_back(inv[pp_]);
+        std::vector<int32_t> tinv(inv);
+        for (int r = 0; r < hot && r < (int)cand.size(); ++r) {
+          const int q = cand[r], pq = tgt[q];
+          if (pq == r) continue;
+          const int o = tinv[r];
+          tgt[o] = pq;
+          tinv[pq] = o;
+          tgt[q] = r;
+          tinv[r] = q;
+        }
+      }
+      lay.target = tgt.data();
+    } else if (layout) {
       lay.phys_in = phys.data();
       lay.inv_in = inv.data();
       lay.phys_out = next.data();
       lay.next_use = next_use[i].data();
       lay.target = home.data();
-      lay.mode = (i + 1 == num_parts) ? LAYOUT_TARGET : LAYOUT_PRIORITY;
+      // in place: the last part sends its qubits home, restore launches
+      // fix the rest (ping-pong part 0 only prepares the next layout)
+      lay.mode = (!pp && i + 1 == num_parts) ? LAYOUT_TARGET : LAYOUT_PRIORITY;
     }
     std::string e;
     int s = plan_part(n_local, dtype, tile_max, options, p.staged, p.num_staged, gates + p.gate_offset, p.num_gates,
@@ -707,11 +822,39 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       err = "part " + std::to_string(i) + ": " + e;
       return s;
     }
+    plans[i].launch.in_buf = cur_buf;
+    if (oop) cur_buf ^= 1;
+    plans[i].launch.out_buf = cur_buf;
     if (layout) {
       phys = next;
       for (int q = 0; q < n_local; ++q) inv[phys[q]] = q;
     }
   }
+  if (pp && need_restore) {
+    // stage qubits 0..hot-1 and the qubits on positions 0..hot-1: loads and
+    // stores both run over 128 B lines; every other bit is a free bit
+    std::vector<int32_t> st;
+    for (int q = 0; q < hot; ++q) st.push_back(q);
+    for (int pos = 0; pos < hot; ++pos)
+      if (std::find(st.begin(), st.end(), inv[pos]) == st.end()) st.push_back(inv[pos]);
+    std::sort(st.begin(), st.end());
+    std::vector<int32_t> ident(n_local), next(phys);
+    for (int q = 0; q < n_local; ++q) ident[q] = q;
+    LayoutIO lay;
+    lay.phys_in = phys.data();
+    lay.inv_in = inv.data();
+    lay.phys_out = next.data();
+    lay.target = ident.data();
+    lay.mode = LAYOUT_OOP;
+    PartPlan pl;
+    int s = plan_part(n_local, dtype, tile_max, options, st.data(), (int)st.size(), nullptr, 0, pl, err, &lay);
+    if (s != HS_OK) return s;
+    pl.info.restore = 1;
+    pl.launch.in_buf = cur_buf;
+    pl.launch.out_buf = cur_buf ^ 1;
+    plans.push_back(pl);
+  }
+  if (pp) return HS_OK;  // natural order, in the state
   if (layout) return plan_restore(n_local, dtype, tile_max, options, phys, plans, err);
   return HS_OK;
 }

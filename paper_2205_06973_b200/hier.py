@@ -44,6 +44,8 @@ _KIND_CODE = {k: i for i, k in enumerate(GateKind)}
 JIT_MIN_QUBITS = 20
 #: ... and plan the coalescing layout (HS_PLAN_LAYOUT) from this size on
 LAYOUT_MIN_QUBITS = 23
+#: free HBM left over after the ping-pong scratch buffer is allocated
+PINGPONG_HEADROOM = 2 << 30
 
 
 # --- addressing (host) --------------------------------------------------------
@@ -214,9 +216,12 @@ class PartProgram:
     once; ``run`` only launches."""
 
     def __init__(self, n_local: int, exes: Sequence[ExecutablePart], dtype="complex128", device=None,
-                 options: int | None = None):
+                 options: int | None = None, basis_start: bool = False):
         """``options``: planner bits (``_native.HS_PLAN_*``); default: the
-        engine default plus ``HS_PLAN_LAYOUT`` (whole-program runs)."""
+        engine default plus ``HS_PLAN_JIT`` / ``HS_PLAN_LAYOUT`` by state
+        size. ``basis_start``: the program will only be run on basis states
+        prepared with :meth:`init_basis`, so it may pick its initial layout
+        (``HS_PLAN_INIT_LAYOUT``; ``run`` then expects that layout)."""
         import torch
 
         self.n_local = n_local
@@ -236,6 +241,14 @@ class PartProgram:
                 # coalescing layout + restore launches pay off once the state
                 # streams from HBM (measured: c2/c3 win, the L2-resident c1 loses)
                 options |= _native.HS_PLAN_LAYOUT
+                if basis_start:
+                    options |= _native.HS_PLAN_INIT_LAYOUT
+                # out-of-place parts (any next layout, no restore launches)
+                # when a scratch copy of the state fits next to it
+                amp = 16 if self.dtype == torch.complex128 else 8
+                free, _ = torch.cuda.mem_get_info(self.device)
+                if (amp << n_local) + PINGPONG_HEADROOM <= free:
+                    options |= _native.HS_PLAN_PINGPONG
         self.options = options
         parts, gates, total = _pack(exes)
         out = ctypes.c_void_p()
@@ -251,6 +264,21 @@ class PartProgram:
         self._lib = lib
         self.num_launches = lib.hs_program_num_launches(self._h)
         self.jit_error = lib.hs_program_jit_error(self._h).decode(errors="replace")
+        self._scratch = None
+        phys = (ctypes.c_int32 * max(1, n_local))()
+        _native.check(lib.hs_program_initial_layout(self._h, phys))
+        #: physical bit of each qubit in the state ``run`` expects
+        self.initial_layout = tuple(int(phys[q]) for q in range(n_local))
+
+    def basis_index(self, index: int) -> int:
+        """Where basis state |index> lives in the program's initial layout."""
+        return sum(((index >> q) & 1) << p for q, p in enumerate(self.initial_layout))
+
+    def init_basis(self, data, index: int = 0) -> None:
+        """Prepare |index> in the layout ``run`` expects."""
+        from .statevec import init_basis
+
+        init_basis(data, self.basis_index(index))
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
@@ -309,7 +337,20 @@ class PartProgram:
         rows = self._check(data)
         count = self.num_launches - first if count is None else count
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._bind_scratch(data)
         _native.check(self._lib.hs_program_run(self._h, data.data_ptr(), rows, first, count, s))
+
+    def _bind_scratch(self, data) -> None:
+        """HS_PLAN_PINGPONG: a device buffer like ``data`` the parts alternate
+        with (allocated once per shape, kept by the program)."""
+        if not self.options & _native.HS_PLAN_PINGPONG:
+            return
+        sc = self._scratch
+        if sc is None or sc.numel() < data.numel() or sc.dtype != data.dtype or sc.device != data.device:
+            import torch
+
+            self._scratch = sc = torch.empty(data.numel(), dtype=data.dtype, device=data.device)
+        _native.check(self._lib.hs_program_bind_scratch(self._h, sc.data_ptr(), sc.numel() * sc.element_size()))
 
     def run_graph(self, data, stream=None) -> None:
         """All parts as one CUDA graph launch (captured on first use)."""
@@ -317,6 +358,7 @@ class PartProgram:
 
         rows = self._check(data)
         s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._bind_scratch(data)
         _native.check(self._lib.hs_program_run_graph(self._h, data.data_ptr(), rows, s))
 
 
@@ -476,12 +518,16 @@ class HierarchicalRun:
     """Plan once, run many times: the device program of a partitioned
     circuit (the reusable core of ``execute_hierarchical``)."""
 
-    def __init__(self, circuit: Circuit, partition: PartitionResult, dtype="complex128", device=None):
+    def __init__(self, circuit: Circuit, partition: PartitionResult, dtype="complex128", device=None,
+                 options: int | None = None, basis_start: bool = False):
+        """``basis_start``: runs start from basis states prepared with
+        ``program.init_basis`` (lets the planner choose the initial layout)."""
         _check_covers(circuit, partition.parts)
         self.circuit = circuit
         self.partition = partition
         self.exes = [remap_part(circuit, p) for p in partition.parts]
-        self.program = PartProgram(circuit.num_qubits, self.exes, dtype=dtype, device=device)
+        self.program = PartProgram(circuit.num_qubits, self.exes, dtype=dtype, device=device, options=options,
+                                   basis_start=basis_start)
 
     def trace(self) -> ExecutionTrace:
         return hierarchical_trace(self.circuit, self.partition)
@@ -500,8 +546,10 @@ def execute_hierarchical(
     """Run a partitioned circuit part by part on one device state
     (hier.py:342-368): parts in the given order, one kernel pass each.
     Returns a device ``StateVector`` (and the ``ExecutionTrace``)."""
-    run = HierarchicalRun(circuit, partition, dtype=dtype, device=device)
     state = start_state(circuit, initial, max_qubits, dtype, device)
+    # from |0..0> (one amplitude, the same in every layout) the planner may
+    # choose the initial layout; a caller's state arrives in natural order
+    run = HierarchicalRun(circuit, partition, dtype=dtype, device=device, basis_start=initial is None)
     run.program.run(state.data)
     if with_trace:
         return state, run.trace()

@@ -19,10 +19,12 @@ F_D0_ONE, F_D1_ONE, F_SIGN, F_PARITY = 1, 2, 4, 32
 K_NONE = 0xFF
 
 LAUNCH = np.dtype([("prog_offset", "<i8"), ("nprog", "<i4"), ("T", "<i4"), ("RB", "<i4"), ("fin_sync", "<i4"),
-                   ("tpos", "u1", 16), ("fin_rpos", "u1", 4), ("fin_npos", "u1", 12)])
+                   ("tpos", "u1", 16), ("fin_rpos", "u1", 4), ("fin_npos", "u1", 12),
+                   ("oop", "<i4"), ("in_buf", "<i4"), ("out_buf", "<i4"), ("pad", "<i4"),
+                   ("opos", "u1", 16), ("fpos", "u1", 56)])
 INSTR = np.dtype([("op", "<u2"), ("k", "u1"), ("flags", "u1"), ("creg", "<u4"), ("ctid", "<u4"), ("qtid", "<u4"),
                   ("rpos", "u1", 4), ("npos", "u1", 12), ("m", "<f8", 8)])
-assert LAUNCH.itemsize == 56 and INSTR.itemsize == 96
+assert LAUNCH.itemsize == 144 and INSTR.itemsize == 96
 
 
 def plan(native, n_local, dtype, tile_bits, staged, ops, op_slots, options=1):
@@ -53,8 +55,9 @@ def _deposit(x: np.ndarray, pos) -> np.ndarray:
     return out
 
 
-def emulate(psi: np.ndarray, n_local: int, launch, prog) -> None:
-    """Run one planned part in place on ``psi`` (rows x 2^n_local)."""
+def emulate(psi: np.ndarray, n_local: int, launch, prog, out: np.ndarray | None = None) -> None:
+    """Run one planned part on ``psi`` (rows x 2^n_local): in place, or
+    into ``out`` under the launch's next layout when it is out of place."""
     T, RB = int(launch["T"]), int(launch["RB"])
     tpos = [int(x) for x in launch["tpos"][:T]]
     flat = psi.reshape(-1)
@@ -120,6 +123,13 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog) -> None:
     fin = slot_of([int(x) for x in launch["fin_rpos"]], [int(x) for x in launch["fin_npos"]])
     for i, s in enumerate(fin[1]):
         smem[:, s] = regs[i]
+    if int(launch["oop"]):
+        opos = [int(x) for x in launch["opos"][:T]]
+        fpos = [int(x) for x in launch["fpos"][: len(free)]]
+        obase_f = _deposit(fix, fpos)
+        obases = (np.arange(rows, dtype=np.int64)[:, None] << n_local | obase_f[None, :]).reshape(-1)
+        out.reshape(-1)[obases[:, None] + _deposit(slots, opos)[None, :]] = smem
+        return
     flat[bases[:, None] + ga[None, :]] = smem
 
 
@@ -145,3 +155,17 @@ def plan_program(native, n_local, dtype, tile_bits, exes, options):
         off += n * INSTR.itemsize
         out.append((launch, prog))
     return out
+
+
+def run_program(psi: np.ndarray, n_local: int, launches) -> np.ndarray:
+    """Run a planned program (ping-pong aware) on ``psi``; returns the state
+    buffer (``psi`` itself, written in place)."""
+    bufs = [psi, np.zeros_like(psi)]
+    for launch, prog in launches:
+        src, dst = bufs[int(launch["in_buf"])], bufs[int(launch["out_buf"])]
+        if int(launch["oop"]):
+            emulate(src, n_local, launch, prog, out=dst)
+        else:
+            assert src is dst
+            emulate(src, n_local, launch, prog)
+    return psi

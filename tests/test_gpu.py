@@ -259,3 +259,29 @@ def test_compiled_full_size_c2_matches_c_oracle():
     run.program.run(st.data)
     ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
     assert max_abs_diff(st, ref) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["c3@24", "c2@24"])
+def test_initial_layout_for_basis_starts(name):
+    """HS_PLAN_INIT_LAYOUT: a program that only ever starts from basis states
+    picks its own initial layout (part 0's qubits lowest); |x> prepared with
+    init_basis in that layout gives the natural-order result of |x>."""
+    from paper_2205_06973_b200.statevec import allocate
+
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), 12)
+    run = HierarchicalRun(c, part, basis_start=True)
+    n = c.num_qubits
+    assert run.program.initial_layout != tuple(range(n))
+    assert sorted(run.program.initial_layout) == list(range(n))
+    x = 0b1011001110001011010110 & ((1 << n) - 1)
+    st = allocate(n)
+    run.program.init_basis(st, x)
+    run.program.run(st)
+    init = np.zeros(1 << n, dtype=np.complex128)
+    init[x] = 1.0
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts], initial=init)
+    assert float(np.max(np.abs(st.cpu().numpy() - ref))) < 1e-10
+    # a caller's natural-order state goes through a program without one
+    plain = HierarchicalRun(c, part, basis_start=False)
+    assert plain.program.initial_layout == tuple(range(n))

@@ -166,6 +166,33 @@ def test_program_layout_and_restore_match_oracle(name, limit):
     assert sum(x == 0 for x in low) >= sum(x == 0 for x in plain)
 
 
+@pytest.mark.parametrize("name,limit", [("c2@13", 8), ("c3@14", 9), ("c1@12", 6), ("c2@14", 10), ("c4@13", 6)])
+def test_pingpong_programs_match_oracle(name, limit):
+    """HS_PLAN_PINGPONG: parts alternate state -> scratch -> state, each
+    writing the next part's qubits onto the lowest positions; the last part
+    writes natural order into the state (no restore launches). Odd and even
+    part counts, several tile widths."""
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), limit)
+    exes = [remap_part(c, p) for p in part.parts]
+    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    for tile_bits in (limit, limit + 1, 12):
+        launches = emu.plan_program(_native, c.num_qubits, 0, tile_bits, exes, options=5 | 8 | 0x40)
+        # at most one gate-free permutation launch at the end
+        assert len(launches) - len(exes) == int(not {0, 1, 2} <= set(part.parts[-1].qubits))
+        assert int(launches[-1][0]["out_buf"]) == 0
+        oop = [int(l["oop"]) for l, _ in launches]
+        assert oop[0] == (len(launches) % 2 == 0) and all(oop[1:])
+        psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
+        psi[0, 0] = 1
+        emu.run_program(psi, c.num_qubits, launches)
+        assert np.max(np.abs(psi[0] - want)) < 1e-12, tile_bits
+    # every part after the first reads 128 B runs when the parts overlap enough
+    launches = emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=5 | 8 | 0x40)
+    low = [sum(int(l["tpos"][b]) == b for b in range(3)) for l, _ in launches[1:]]
+    assert sum(x == 3 for x in low) >= len(low) // 2
+
+
 def _jit_source(c, p, dtype=0, options=5, tile_bits=12):
     import ctypes
 
