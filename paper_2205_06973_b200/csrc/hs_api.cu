@@ -219,6 +219,30 @@ static int run_range(hs_program* prog, void* state, int64_t batch, int first, in
     void* bufs[2] = {state, prog->scratch};
     void* psi = bufs[pl.launch.in_buf];
     void* psi_out = bufs[pl.launch.out_buf];
+    if (pl.jit && pl.launch.cluster_log > 0) {
+      // cluster tile: 2^cluster_log CTAs of 2^(T - cluster_log) slots, two per SM
+      long long ntiles = (long long)(batch << (prog->n_local - pl.launch.T));
+      void* args[] = {&psi, &psi_out, &ntiles};
+      const int csize = 1 << pl.launch.cluster_log;
+      const int TC = pl.launch.T - pl.launch.cluster_log;
+      const int per_sm = (TC - pl.launch.RB) >= 9 ? 1 : 2;  // as the kernel's __launch_bounds__
+      long long nclusters = (long long)eng->num_sms * per_sm / csize;
+      if (nclusters > ntiles) nclusters = ntiles;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(nclusters * csize));
+      cfg.blockDim = dim3(1u << (TC - pl.launch.RB));
+      cfg.dynamicSmemBytes = size_t(prog->dtype == HS_C128 ? 16 : 8) << TC;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = csize;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      HS_CUDA(cudaLaunchKernelExC(&cfg, (const void*)pl.jit, args), "compiled cluster-tile part launch");
+      continue;
+    }
     if (pl.jit) {
       long long ntiles = (long long)(batch << (prog->n_local - pl.launch.T));
       void* args[] = {&psi, &psi_out, &ntiles};

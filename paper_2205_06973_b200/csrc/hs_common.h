@@ -23,7 +23,8 @@ enum : uint8_t { F_D0_ONE = 1, F_D1_ONE = 2, F_SIGN = 4, F_PLAIN = 8, F_REAL = 1
 
 constexpr uint8_t K_NONE = 0xFF;
 constexpr int MAX_RB = 4;       // register bits per thread
-constexpr int MAX_TILE = 13;    // tile bits the kernels support
+constexpr int MAX_TILE = 13;    // tile bits the single-CTA kernels support
+constexpr int MAX_CLUSTER_LOG = 2;  // compiled parts: tiles over clusters of up to 4 CTAs
 constexpr int MAX_NPOS = 12;    // non-register tile bits (T - RB)
 
 // One device instruction, 96 bytes. Location bits are positions inside the
@@ -57,7 +58,7 @@ struct PartLaunch {
   // (ascending) and free (tile index) bit j to fpos[j]
   int32_t oop;
   int32_t in_buf, out_buf;
-  int32_t pad_;
+  int32_t cluster_log;  // tile spread over a cluster of 2^cluster_log CTAs (compiled parts only)
   uint8_t opos[16];
   uint8_t fpos[56];
 };

@@ -70,15 +70,24 @@ struct Gen {
         if (i >> k & 1) u[i] ^= swz_host(1u << rpos[k], c128);
     return u;
   }
+  bool cluster = false;  // slots live in the shared memory of the cluster's CTAs (CL_LD / CL_ST)
   void load_regs(const uint8_t* rpos) {
     auto u = slot_xor(rpos);
-    for (int i = 0; i < nreg; ++i)
-      o << "    { const C v = sm[st ^ " << u[i] << "u]; " << re(i) << " = v.x; " << im(i) << " = v.y; }\n";
+    for (int i = 0; i < nreg; ++i) {
+      if (cluster)
+        o << "    CL_LD(st ^ " << u[i] << "u, " << re(i) << ", " << im(i) << ");\n";
+      else
+        o << "    { const C v = sm[st ^ " << u[i] << "u]; " << re(i) << " = v.x; " << im(i) << " = v.y; }\n";
+    }
   }
   void store_regs(const uint8_t* rpos) {
     auto u = slot_xor(rpos);
-    for (int i = 0; i < nreg; ++i)
-      o << "    { C v; v.x = " << re(i) << "; v.y = " << im(i) << "; sm[st ^ " << u[i] << "u] = v; }\n";
+    for (int i = 0; i < nreg; ++i) {
+      if (cluster)
+        o << "    CL_ST(st ^ " << u[i] << "u, " << re(i) << ", " << im(i) << ");\n";
+      else
+        o << "    { C v; v.x = " << re(i) << "; v.y = " << im(i) << "; sm[st ^ " << u[i] << "u] = v; }\n";
+    }
   }
   void cmul_into(int i, const std::string& dr, const std::string& di) {
     o << "      { const " << R() << " x = " << re(i) << ", y = " << im(i) << "; " << re(i) << " = fma(x, " << dr
@@ -333,7 +342,157 @@ struct Gen {
   }
 };
 
+// The part's program on one tile: register declarations, phases (shared
+// memory exchanges separated by `sync`), gates, the part's scalar, and the
+// final write of the registers into the tile's store order (ending in `sync`)
+void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per_amp) {
+  std::ostringstream& o = g.o;
+  o << "    " << g.R() << " ";
+  for (int i = 0; i < g.nreg; ++i) o << (i ? ", " : "") << "r" << i << ", q" << i;
+  o << ";\n    unsigned t, st;\n";
+  const Instr* cur = nullptr;
+  g.reset_pending();
+  for (const Instr& in : pl.prog) {
+    if (in.op == I_DIAG && g.fold_diag(in)) continue;
+    if (in.op != I_DIAG) g.flush();  // a non-diagonal step: apply the pending run first
+    if (in.op == I_PHASE) {
+      if (cur) {
+        g.store_regs(cur->rpos);
+        o << "    " << sync << "\n";
+      }
+      g.emit_tdep("t", in.npos);
+      o << "    st = swz(t);\n";
+      g.load_regs(in.rpos);
+      cur = &in;
+      continue;
+    }
+    const bool ctl_t = in.ctid != 0;
+    if (ctl_t) o << "    if ((t & " << in.ctid << "u) == " << in.ctid << "u) {\n";
+    else o << "    {\n";
+    g.wgt = 1.0 / double(1u << __builtin_popcount(in.ctid));
+    if (in.op == I_DENSE) g.dense(in);
+    else if (in.op == I_PERM) g.perm(in, !ctl_t);
+    else g.diag(in);
+    g.wgt = 1.0;
+    o << "    }\n";
+  }
+  g.flush(true);  // pending diagonal run + the part's scalar
+  if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
+  o << "    // fp64_instr_per_amp " << g.ops / g.nreg << "\n";
+  if (pl.launch.fin_sync) o << "    " << sync << "\n";
+  g.emit_tdep("t", pl.launch.fin_npos);
+  o << "    st = swz(t);\n";
+  g.store_regs(pl.launch.fin_rpos);
+  o << "    " << sync << "\n";
+}
+
+// Parts wider than one CTA's tile (c128 w = 13, 14; c64 w = 14, 15): the
+// 2^T tile is spread over a thread-block cluster of 2^cl CTAs, 2^TC slots
+// each (slot s lives in CTA s >> TC). Each CTA loads and stores its own
+// slots; phase exchanges read and write any CTA's slots through distributed
+// shared memory (mapa + ld/st.shared::cluster) between cluster barriers.
+// A thread's tile-global index is threadIdx.x | rank << (TC - RB).
+std::string jit_source_cluster(const PartPlan& pl, int dtype, int n_local, double* fp64_per_amp) {
+  Gen g;
+  g.c128 = dtype == HS_C128;
+  g.RB = pl.launch.RB;
+  g.T = pl.launch.T;
+  g.n_local = n_local;
+  g.nreg = 1 << g.RB;
+  g.var.resize(g.nreg);
+  for (int i = 0; i < g.nreg; ++i) g.var[i] = i;
+  g.cluster = true;
+  const int T = g.T, RB = g.RB, cl = pl.launch.cluster_log, TC = T - cl, lowc = TC - RB, NT = 1 << lowc;
+  const int amp = g.c128 ? 16 : 8;
+  const char* C = g.c128 ? "double2" : "float2";
+  const char* V = g.c128 ? "v2.f64" : "v2.f32";
+  const char* RC = g.c128 ? "d" : "f";
+  std::ostringstream& o = g.o;
+  o << "typedef " << C << " C;\n";
+  o << "__device__ __forceinline__ unsigned swz(unsigned s) { return s ^ "
+    << (g.c128 ? "(((s >> 3) ^ (s >> 6) ^ (s >> 9) ^ (s >> 12)) & 7u)" : "(((s >> 4) ^ (s >> 8) ^ (s >> 12)) & 15u)")
+    << "; }\n";
+  // the swizzle only changes bits below 4, so slot s and swz(s) share a CTA
+  o << "__device__ __forceinline__ unsigned cl_addr(unsigned sbase, unsigned sl) {\n  unsigned ra;\n"
+    << "  asm volatile(\"mapa.shared::cluster.u32 %0, %1, %2;\" : \"=r\"(ra) : \"r\"(sbase + (sl & "
+    << ((1u << TC) - 1) << "u) * " << amp << "u), \"r\"(sl >> " << TC << "));\n  return ra;\n}\n";
+  o << "#define CL_ADDR(sl) cl_addr(sbase, (sl))\n";
+  o << "#define CL_ST(sl, x, y) asm volatile(\"st.shared::cluster." << V << " [%0], {%1, %2};\" :: \"r\"(CL_ADDR(sl)), \""
+    << RC << "\"(x), \"" << RC << "\"(y) : \"memory\")\n";
+  o << "#define CL_LD(sl, x, y) asm volatile(\"ld.shared::cluster." << V << " {%0, %1}, [%2];\" : \"=" << RC << "\"(x), \"="
+    << RC << "\"(y) : \"r\"(CL_ADDR(sl)) : \"memory\")\n";
+  o << "#define CL_SYNC() asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\")\n";
+  // two CTAs per SM while 2 x NT threads keep 128 registers each
+  o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << (NT >= 512 ? 1 : 2)
+    << ") hs_jit_part(C* psi, C* psi_out, long long ntiles) {\n";
+  o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
+  o << "  C* sm = reinterpret_cast<C*>(smem_raw);\n";
+  o << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);\n";
+  o << "  unsigned rank, cid, ncl;\n";
+  o << "  asm(\"mov.u32 %0, %%cluster_ctarank;\" : \"=r\"(rank));\n";
+  o << "  asm(\"mov.u32 %0, %%clusterid.x;\" : \"=r\"(cid));\n";
+  o << "  asm(\"mov.u32 %0, %%nclusterid.x;\" : \"=r\"(ncl));\n";
+  o << "  const unsigned ltid = threadIdx.x;\n";
+  o << "  const unsigned tid0 = ltid | (rank << " << lowc << ");\n";
+  // this CTA's slots in canonical order: local l = ltid + (j << lowc), slot
+  // s = l | rank << TC; global offsets of the ltid and rank parts
+  auto dep = [&](const uint8_t* pos, const char* what, int from, int cnt) {
+    std::string e = "0ull";
+    for (int b = 0; b < cnt; ++b)
+      e += " | ((unsigned long long)((" + std::string(what) + " >> " + std::to_string(b) + ") & 1u) << " +
+           std::to_string((int)pos[from + b]) + ")";
+    return e;
+  };
+  const bool oop = pl.launch.oop != 0;
+  o << "  const unsigned long long ga_l = " << dep(pl.launch.tpos, "ltid", 0, lowc) << " | "
+    << dep(pl.launch.tpos, "rank", TC, cl) << ";\n";
+  if (oop)
+    o << "  const unsigned long long go_l = " << dep(pl.launch.opos, "ltid", 0, lowc) << " | "
+      << dep(pl.launch.opos, "rank", TC, cl) << ";\n";
+  o << "  const unsigned sw_l = swz(ltid);\n";  // swz of the ltid part (linear, no rank bits)
+  auto hi = [&](const uint8_t* pos, int j) {
+    uint64_t h = 0;
+    for (int k = 0; k < RB; ++k)
+      if (j >> k & 1) h |= 1ull << pos[lowc + k];
+    return h;
+  };
+  o << "  for (long long tt = cid; tt < ntiles; tt += ncl) {\n";
+  o << "    unsigned tid = tid0; asm volatile(\"\" : \"+r\"(tid));  // keep phase addresses in the loop\n";
+  o << "    const unsigned long long row = (unsigned long long)tt >> " << (n_local - T) << ";\n";
+  o << "    unsigned long long f = (unsigned long long)tt & " << ((1ull << (n_local - T)) - 1) << "ull;\n";
+  for (int b = 0; b < T; ++b) {
+    int p = pl.launch.tpos[b];
+    o << "    { const unsigned long long lo = f & " << ((1ull << p) - 1) << "ull; f = ((f ^ lo) << 1) | lo; }\n";
+  }
+  o << "    const unsigned long long base = (row << " << n_local << ") | f | ga_l;\n";
+  for (int j = 0; j < g.nreg; ++j) {
+    // local index of slot (ltid + (j << lowc)) | rank << TC after the swizzle
+    const uint32_t sx = swz_host(uint32_t(j) << lowc, g.c128) & ((1u << TC) - 1);
+    o << "    asm volatile(\"cp.async." << (g.c128 ? "cg" : "ca") << ".shared.global [%0], [%1], " << amp
+      << ";\" :: \"r\"(sbase + ((sw_l ^ " << sx << "u ^ (swz(rank << " << TC << ") & " << ((1u << TC) - 1)
+      << "u)) * " << amp << "u)), \"l\"(psi + (base | " << hi(pl.launch.tpos, j) << "ull)) : \"memory\");\n";
+  }
+  o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\" ::: \"memory\");\n";
+  o << "    CL_SYNC();\n";
+  emit_program(g, pl, "CL_SYNC();", fp64_per_amp);
+  if (oop) {
+    o << "    const unsigned long long obase = ((unsigned long long)tt >> " << (n_local - T) << " << " << n_local
+      << ") | go_l";
+    for (int j = 0; j < n_local - T; ++j)
+      o << "\n      | ((((unsigned long long)tt >> " << j << ") & 1ull) << " << (int)pl.launch.fpos[j] << ")";
+    o << ";\n";
+  }
+  for (int j = 0; j < g.nreg; ++j) {
+    const uint32_t sx = swz_host(uint32_t(j) << lowc, g.c128) & ((1u << TC) - 1);
+    o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << hi(oop ? pl.launch.opos : pl.launch.tpos, j)
+      << "ull] = sm[sw_l ^ " << sx << "u ^ (swz(rank << " << TC << ") & " << ((1u << TC) - 1) << "u)];\n";
+  }
+  o << "    __syncthreads();\n  }\n}\n";
+  return o.str();
+}
+
 std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_per_amp = nullptr) {
+  if (pl.launch.cluster_log > 0) return jit_source_cluster(pl, dtype, n_local, fp64_per_amp);
   Gen g;
   g.c128 = dtype == HS_C128;
   g.RB = pl.launch.RB;
@@ -367,7 +526,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + " << 3 * tile_bytes << ");\n";
   o << "  volatile int* issued = reinterpret_cast<volatile int*>(smem_raw + " << 3 * tile_bytes + 32 << ");\n";
   o << "  const unsigned team = threadIdx.x >> " << low << ";\n";
-  o << "  const unsigned tid = threadIdx.x & " << (NT - 1) << "u;\n";
+  o << "  const unsigned tid0 = threadIdx.x & " << (NT - 1) << "u;\n  const unsigned tid = tid0;\n";
   o << "  const unsigned bar_id = 1u + team;\n";
   o << "  if (threadIdx.x == 0) {\n";
   o << "    for (int b = 0; b < 3; ++b) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << NT
@@ -432,6 +591,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "    const long long tt = blockIdx.x + i * (long long)gridDim.x;\n";
   o << "    if (tt >= ntiles) break;\n";
   o << "    const unsigned long long base = tile_base(tt);\n";
+  o << "    unsigned tid = tid0; asm volatile(\"\" : \"+r\"(tid));  // keep phase addresses in the loop\n";
   o << "    const int b = (int)(i % 3);\n";
   o << "    C* sm = reinterpret_cast<C*>(smem_raw + b * " << tile_bytes << ");\n";
   // Fill k = i / 3 of buffer b. This team can get here before the other
@@ -444,43 +604,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "      const unsigned mb = (unsigned)__cvta_generic_to_shared(&full[b]); const unsigned par = (unsigned)(k & 1);\n";
   o << "      unsigned done = 0;\n";
   o << "      while (!done) asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\" : \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\"); }\n";
-  o << "    " << g.R() << " ";
-  for (int i = 0; i < g.nreg; ++i) o << (i ? ", " : "") << "r" << i << ", q" << i;
-  o << ";\n    unsigned t, st;\n";
-  const Instr* cur = nullptr;
-  g.reset_pending();
-  for (const Instr& in : pl.prog) {
-    if (in.op == I_DIAG && g.fold_diag(in)) continue;
-    if (in.op != I_DIAG) g.flush();  // a non-diagonal step: apply the pending run first
-    if (in.op == I_PHASE) {
-      if (cur) {
-        g.store_regs(cur->rpos);
-        o << "    TEAM_SYNC();\n";
-      }
-      g.emit_tdep("t", in.npos);
-      o << "    st = swz(t);\n";
-      g.load_regs(in.rpos);
-      cur = &in;
-      continue;
-    }
-    const bool ctl_t = in.ctid != 0;
-    if (ctl_t) o << "    if ((t & " << in.ctid << "u) == " << in.ctid << "u) {\n";
-    else o << "    {\n";
-    g.wgt = 1.0 / double(1u << __builtin_popcount(in.ctid));
-    if (in.op == I_DENSE) g.dense(in);
-    else if (in.op == I_PERM) g.perm(in, !ctl_t);
-    else g.diag(in);
-    g.wgt = 1.0;
-    o << "    }\n";
-  }
-  g.flush(true);  // pending diagonal run + the part's scalar
-  if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
-  o << "    // fp64_instr_per_amp " << g.ops / g.nreg << "\n";
-  if (pl.launch.fin_sync) o << "    TEAM_SYNC();\n";
-  g.emit_tdep("t", pl.launch.fin_npos);
-  o << "    st = swz(t);\n";
-  g.store_regs(pl.launch.fin_rpos);
-  o << "    TEAM_SYNC();\n";
+  emit_program(g, pl, "TEAM_SYNC();", fp64_per_amp);
   if (oop) o << "    const unsigned long long obase = out_base(tt);\n";
   for (int j = 0; j < g.nreg; ++j) {
     const uint32_t sx = swz_host(uint32_t(j) << low, g.c128);

@@ -336,12 +336,14 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     if (j && staged[j] <= staged[j - 1]) { err = "staged positions not strictly ascending"; return HS_ERR_INVALID; }
   }
   const int T = std::min(std::max(tile_max, w), n_local);
-  if (T > tile_max) {
-    err = "part stages " + std::to_string(w) + " qubits; the on-chip tile holds " +
-          std::to_string(tile_max);
+  // a part wider than one CTA's tile runs as a cluster tile (compiled parts)
+  const int cluster_log = T > tile_max ? T - tile_max : 0;
+  if (cluster_log > 0 && (!(options & HS_PLAN_JIT) || cluster_log > MAX_CLUSTER_LOG)) {
+    err = "part stages " + std::to_string(w) + " qubits; the on-chip tile holds " + std::to_string(tile_max) +
+          ((options & HS_PLAN_JIT) ? " (x4 over a CTA cluster)" : " (compiled parts span CTA clusters: HS_PLAN_JIT)");
     return HS_ERR_TOO_WIDE;
   }
-  if (T > MAX_TILE) { err = "tile wider than the kernels support"; return HS_ERR_TOO_WIDE; }
+  if (T - cluster_log > MAX_TILE) { err = "tile wider than the kernels support"; return HS_ERR_TOO_WIDE; }
   const int RB = std::min((options & HS_PLAN_RB3) ? 3 : MAX_RB, T);
 
   // physical positions of the staged qubits under the program's layout
@@ -600,6 +602,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   L.nprog = (int32_t)P.prog.size();
   L.T = T;
   L.RB = RB;
+  L.cluster_log = cluster_log;
   for (int b = 0; b < T; ++b) L.tpos[b] = (uint8_t)tile[b];
   bool ident = true;
   for (int loc = 0; loc < T; ++loc) ident &= (rho[bit_at[loc]] == loc);

@@ -233,7 +233,9 @@ class PartProgram:
         eng = _native.engine(dev)
         if options is None:
             options = _native.default_options()
-            if n_local >= JIT_MIN_QUBITS:
+            widest = max((e.num_slots for e in exes), default=0)
+            if n_local >= JIT_MIN_QUBITS or widest > (12 if self.dtype == torch.complex128 else 13):
+                # (parts wider than one CTA's tile only run as compiled cluster tiles)
                 # compiling a part costs ~0.5-1 s of host time (parallel over
                 # parts, cached); worth it once a pass moves >= 32 MiB
                 options |= _native.HS_PLAN_JIT

@@ -285,3 +285,19 @@ def test_initial_layout_for_basis_starts(name):
     # a caller's natural-order state goes through a program without one
     plain = HierarchicalRun(c, part, basis_start=False)
     assert plain.program.initial_layout == tuple(range(n))
+
+
+@pytest.mark.parametrize("name,limit,dtype", [("c2@22", 14, "complex128"), ("c2@24", 13, "complex128"),
+                                              ("c2@17", 14, "complex128"), ("c2@22", 15, "complex64")])
+def test_cluster_tile_parts_match_c_oracle(name, limit, dtype):
+    """c5's k = 14 parts (256 KB of complex128 per tile) run as cluster
+    tiles: 2 or 4 CTAs share one tile through distributed shared memory."""
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), limit)
+    assert max(len(p.qubits) for p in part.parts) == limit
+    run = HierarchicalRun(c, part, dtype=dtype)
+    assert run.program.jit_error == ""
+    st = from_numpy(np.eye(1, 1 << c.num_qubits, 0).ravel().astype(np.complex128), dtype=dtype)
+    run.program.run(st.data)
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert float(np.max(np.abs(st.to_numpy() - ref))) < TOL[dtype]

@@ -268,3 +268,39 @@ def test_structured_2x2_factorisation():
         assert cost <= 12  # one entry normalised to 1: 2+2+4+4
         s0, mm0, cost0 = _structure(m, allow_scale=False)
         assert s0 == 1 and cost0 <= 16 and np.max(np.abs(mm0 - m)) < 1e-15
+
+
+@pytest.mark.parametrize("name,limit,dtype", [("c2@16", 14, 0), ("c2@15", 13, 0), ("c2@17", 15, 1)])
+def test_cluster_tile_parts(tmp_path, name, limit, dtype):
+    """Parts wider than one CTA's tile (c5's k = 14: 256 KB of complex128)
+    are planned as cluster tiles for compiled kernels: the emulated program
+    matches the oracle (ping-pong included), the interpreter refuses them,
+    and the generated cluster kernel compiles for sm_100a."""
+    import shutil
+    import subprocess
+
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), limit)
+    assert max(len(p.qubits) for p in part.parts) == limit
+    exes = [remap_part(c, p) for p in part.parts]
+    tile = 12 if dtype == 0 else 13
+    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    for opts in (0x15, 0x15 | 8 | 0x40):
+        launches = emu.plan_program(_native, c.num_qubits, dtype, tile, exes, options=opts)
+        assert max(int(l["cluster_log"]) for l, _ in launches) == limit - tile
+        psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
+        psi[0, 0] = 1
+        emu.run_program(psi, c.num_qubits, launches)
+        assert np.max(np.abs(psi[0] - want)) < 1e-12
+    with pytest.raises(PartTooWideForLayoutError):
+        emu.plan_program(_native, c.num_qubits, dtype, tile, exes, options=5)
+    wide = next(p for p in part.parts if len(p.qubits) == limit)
+    src = tmp_path / "cl.cu"
+    src.write_text(_jit_source(c, wide, dtype, options=0x15, tile_bits=tile))
+    assert "barrier.cluster" in src.read_text()
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    res = subprocess.run([nvcc, "-arch=sm_100a", "-cubin", "-o", str(tmp_path / "cl.cubin"), str(src), "-Xptxas", "-v"],
+                         capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr[-3000:]
+    spill = int(re.search(r"(\d+) bytes spill stores", res.stderr).group(1))
+    assert spill <= 64, res.stderr  # a few words at most, outside the gate code
