@@ -180,6 +180,9 @@ CONFIGS = {
     "c5": Config("c5", "36-qubit random circuit, 6x6 grid, depth 24, complex128, k=14, 8 GPUs", 36, 14, 8),
     "c5_35": Config("c5_35", "35-qubit random circuit (6x6 minus corner (5,5)), depth 24, 4 GPUs", 35, 14, 4),
     "c5_34": Config("c5_34", "34-qubit random circuit (6x6 minus corners (5,5),(0,5)), depth 24, 2 GPUs", 34, 14, 2),
+    # one GPU's share of c5: 33 local qubits (128 GiB), the same k = 14 parts
+    "c5_33": Config("c5_33", "33-qubit random circuit (6x6 minus corners (5,5),(0,5),(5,0)), depth 24, k=14: "
+                    "the per-GPU state size of c5 on 8 GPUs", 33, 14, 1),
 }
 
 
@@ -207,6 +210,8 @@ def build(name: str, seed: int = 0) -> Circuit:
         return random_grid_circuit(6, 6, 24, seed, drop=((5, 5),))
     if base == "c5_34":
         return random_grid_circuit(6, 6, 24, seed, drop=((5, 5), (0, 5)))
+    if base == "c5_33":
+        return random_grid_circuit(6, 6, 24, seed, drop=((5, 5), (0, 5), (5, 0)))
     raise KeyError(f"unknown config {name!r}")
 
 

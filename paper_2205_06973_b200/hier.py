@@ -246,10 +246,11 @@ class PartProgram:
                 if basis_start:
                     options |= _native.HS_PLAN_INIT_LAYOUT
                 # out-of-place parts (any next layout, no restore launches)
-                # when a scratch copy of the state fits next to it
+                # when a scratch copy of the state fits next to it (counted
+                # as if the state were not allocated yet)
                 amp = 16 if self.dtype == torch.complex128 else 8
                 free, _ = torch.cuda.mem_get_info(self.device)
-                if (amp << n_local) + PINGPONG_HEADROOM <= free:
+                if 2 * (amp << n_local) + PINGPONG_HEADROOM <= free:
                     options |= _native.HS_PLAN_PINGPONG
         self.options = options
         parts, gates, total = _pack(exes)
