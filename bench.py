@@ -114,7 +114,7 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def build_workload(config: str, strategy: str, extra_bits: int = 0):
+def build_workload(config: str, strategy: str, extra_bits: int = 0, limit: int | None = None):
     from paper_2205_06973_b200 import build_dag, configs, partition_dagp, partition_dfs, partition_nat
 
     cfg = configs.CONFIGS[config.split("@")[0]]
@@ -124,7 +124,7 @@ def build_workload(config: str, strategy: str, extra_bits: int = 0):
     circuit = configs.build(name)
     t0 = time.perf_counter()
     fn = {"nat": partition_nat, "dfs": partition_dfs, "dagp": partition_dagp}[strategy]
-    part = fn(build_dag(circuit), cfg.limit)
+    part = fn(build_dag(circuit), limit or cfg.limit)
     t_part = time.perf_counter() - t0
     return cfg, circuit, part, t_part
 
@@ -221,7 +221,8 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         run = HierarchicalRun(circuit, part, device=dev, options=args.plan_options, basis_start=True)
         n_local = n
     num_parts = part.num_parts
-    num_launches = run.program.num_launches if not dist else len(run.exes)
+    num_launches = (run.program.num_launches if not dist
+                    else sum(pr.num_launches for pr in run.programs if pr is not None))
     bytes_per_pass = 2 * (1 << n_local) * 16
     state = allocate(n_local, "complex128", dev)
     stream = torch.cuda.current_stream(dev)
@@ -237,7 +238,10 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
             timed_events.append(torch.cuda.Event(enable_timing=True))
             timed_events[-1].record(stream)
         if dist:
-            run.run(state, events=timed_events)
+            marks_ = []
+            run.run(state, events=marks_)
+            if timed_events is not None:
+                timed_events += marks_
         elif timed_events is None:
             run.program.run(state)
         else:
@@ -266,9 +270,19 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     torch.cuda.synchronize()
     total_ms = start.elapsed_time(stop)
     clk = clocks.stop()
-    # per-launch durations of the part kernel (events between launches)
-    durs, restore_ms = [], 0.0
+    # per-launch durations of the part kernel (events between launches);
+    # distributed: per segment ("parts") and per layout switch ("switch")
+    durs, restore_ms, switch_ms, seg_ms = [], 0.0, 0.0, 0.0
     for ev in marks:
+        if dist:
+            for i in range(1, len(ev)):
+                kind, e = ev[i]
+                prev = ev[i - 1][1] if isinstance(ev[i - 1], tuple) else ev[i - 1]
+                if kind == "switch":
+                    switch_ms += prev.elapsed_time(e)
+                else:
+                    seg_ms += prev.elapsed_time(e)
+            continue
         d = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)]
         durs += d[:num_parts]
         restore_ms += sum(d[num_parts:])
@@ -324,7 +338,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     peak = ctypes.c_double()
     _native.check(_native.load().hs_fp64_peak(ctypes.byref(peak), stream.cuda_stream))
     fp64_instr = sum(i["fp64_instr_per_amp"] for i in info) * (1 << n_local)
-    part_ms = sum(durs) / args.steps if durs else ms_step
+    part_ms = sum(durs) / args.steps if durs else (seg_ms / args.steps if dist else ms_step)
     fp64 = {"bound_note": "random-circuit parts are FP64-bound, not HBM-bound (SURVEY.md 7.3)",
             "instr_per_step": fp64_instr, "achieved_tflops": 2 * fp64_instr / (part_ms / 1e3) / 1e12,
             "peak_tflops_measured": peak.value,
@@ -334,7 +348,11 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         "ms_step": ms_step, "value": value, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
         "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
         "num_launches": num_launches, "restore_ms_per_step": restore_ms / args.steps, "fp64": fp64,
-        "comm": run.comm_summary() if dist else None,
+        "comm": (dict(run.comm_summary(), switch_ms_per_step=switch_ms / args.steps,
+                      parts_ms_per_step=seg_ms / args.steps,
+                      nvlink_gbs_per_rank=(run.stats.total_bytes / world / (switch_ms / args.steps / 1e3) / 1e9
+                                           if switch_ms > 0 else None))
+                 if dist else None),
     }
 
 
@@ -346,6 +364,7 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
     ap.add_argument("--config", default="c2")
     ap.add_argument("--strategy", default="dfs", choices=["nat", "dfs", "dagp"])
+    ap.add_argument("--limit", type=int, default=None, help="part size k (default: the config's)")
     ap.add_argument("--cpu-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -368,10 +387,10 @@ def main(argv=None):
         else:
             tdist.init_process_group("nccl")
     extra = int(math.log2(world)) if world > 1 else 0
-    cfg, circuit, part, t_part = build_workload(args.config, args.strategy, extra)
+    cfg, circuit, part, t_part = build_workload(args.config, args.strategy, extra, args.limit)
     n = circuit.num_qubits
     config = {"workload": f"{args.config}: {cfg.description}" + (f", scaled to {n} qubits" if extra else ""),
-              "num_qubits": n, "limit": cfg.limit, "strategy": args.strategy, "parts": part.num_parts,
+              "num_qubits": n, "limit": args.limit or cfg.limit, "strategy": args.strategy, "parts": part.num_parts,
               "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
               "state_bytes_per_gpu": (1 << (n - extra)) * 16,
               "l2_policy": "inputs larger than L2: the state (>= 1 GiB) exceeds the 126 MB L2",

@@ -145,6 +145,14 @@ int hs_engine_set_options(hs_engine* eng, uint32_t options);
 int hs_program_create(hs_engine* eng, int n_local, int dtype,
                       const hs_part* parts, int num_parts,
                       const hs_gate* gates, int num_gates, hs_program** out);
+/* the same for a buffer that arrives in a given layout: logical position q
+ * at physical bit init_phys[q] (a permutation; needs HS_PLAN_LAYOUT set on
+ * the engine). The program still ends in natural order. Used after an
+ * in-place layout switch (hs_pack/unpack_segments_range). */
+int hs_program_create_from_layout(hs_engine* eng, int n_local, int dtype,
+                                  const hs_part* parts, int num_parts,
+                                  const hs_gate* gates, int num_gates,
+                                  const int32_t* init_phys, hs_program** out);
 int hs_program_destroy(hs_program* prog);
 int hs_program_num_parts(hs_program* prog);
 /* launches = parts + layout-restore launches (HS_PLAN_LAYOUT) */
@@ -228,6 +236,16 @@ int hs_pack_segments(const void* src, void* dst, int num_bits, int dtype,
                      const int32_t* seg_pos, int num_seg_bits, void* stream);
 int hs_unpack_segments(const void* src, void* dst, int num_bits, int dtype,
                        const int32_t* seg_pos, int num_seg_bits, void* stream);
+
+/* Ranged forms for in-place chunked switches: only inner offsets
+ * [inner_begin, inner_begin + inner_count) of every segment move; packed
+ * index = k * inner_count + (m - inner_begin). */
+int hs_pack_segments_range(const void* src, void* dst, int num_bits, int dtype,
+                           const int32_t* seg_pos, int num_seg_bits,
+                           int64_t inner_begin, int64_t inner_count, void* stream);
+int hs_unpack_segments_range(const void* src, void* dst, int num_bits, int dtype,
+                             const int32_t* seg_pos, int num_seg_bits,
+                             int64_t inner_begin, int64_t inner_count, void* stream);
 
 #ifdef __cplusplus
 }

@@ -27,14 +27,15 @@ HS_MAX_STAGED = 24
 #: every symbol include/hisvsim.h declares (checked by the CPU test suite)
 EXPORTS = (
     "hs_last_error", "hs_abi_version", "hs_engine_create", "hs_engine_destroy",
-    "hs_engine_query", "hs_engine_set_options", "hs_program_create", "hs_program_destroy",
+    "hs_engine_query", "hs_engine_set_options", "hs_program_create", "hs_program_create_from_layout",
+    "hs_program_destroy",
     "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_initial_layout",
     "hs_program_bind_scratch",
     "hs_program_jit_error",
     "hs_program_dump",
     "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_jit_source", "hs_structure_2x2", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
-    "hs_pack_segments", "hs_unpack_segments",
+    "hs_pack_segments", "hs_unpack_segments", "hs_pack_segments_range", "hs_unpack_segments_range",
 )
 
 
@@ -92,6 +93,8 @@ def _declare(lib) -> None:
         "hs_engine_set_options": (I, [P, ctypes.c_uint32]),
         "hs_program_create": (I, [P, I, I, ctypes.POINTER(HsPart), I,
                                   ctypes.POINTER(HsGate), I, ctypes.POINTER(P)]),
+        "hs_program_create_from_layout": (I, [P, I, I, ctypes.POINTER(HsPart), I, ctypes.POINTER(HsGate), I,
+                                              ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(P)]),
         "hs_program_destroy": (I, [P]),
         "hs_program_num_parts": (I, [P]),
         "hs_program_num_launches": (I, [P]),
@@ -118,6 +121,8 @@ def _declare(lib) -> None:
         "hs_max_abs_diff": (I, [P, I, P, I64, ctypes.POINTER(D), P]),
         "hs_pack_segments": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, P]),
         "hs_unpack_segments": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, P]),
+        "hs_pack_segments_range": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, I64, I64, P]),
+        "hs_unpack_segments_range": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, I64, I64, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

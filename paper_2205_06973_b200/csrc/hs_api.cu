@@ -18,6 +18,8 @@ cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void
 cudaError_t launch_set_basis(void* psi, int dtype, int64_t index, cudaStream_t s);
 cudaError_t launch_bit_permute(const void* in, void* out, int nbits, int dtype, const int32_t* dst_of,
                                int num_sms, cudaStream_t s);
+cudaError_t launch_segments_range(bool pack, const void* in, void* out, int nbits, int dtype, const int32_t* seg_pos,
+                                  int nseg, int64_t begin, int64_t count, int num_sms, cudaStream_t s);
 cudaError_t launch_segments(bool pack, const void* in, void* out, int nbits, int dtype,
                             const int32_t* seg_pos, int nseg, int num_sms, cudaStream_t s);
 cudaError_t launch_maxdiff(const void* a, int dtype, const void* b, int64_t n, unsigned long long* dres,
@@ -129,8 +131,30 @@ int hs_engine_query(hs_engine* eng, int* num_sms, int* tile_c128, int* tile_c64)
   return HS_OK;
 }
 
+static int program_create(hs_engine* eng, int n_local, int dtype, const hs_part* parts, int num_parts,
+                          const hs_gate* gates, int num_gates, const int32_t* init_phys, hs_program** out);
+
 int hs_program_create(hs_engine* eng, int n_local, int dtype, const hs_part* parts, int num_parts,
                       const hs_gate* gates, int num_gates, hs_program** out) {
+  return program_create(eng, n_local, dtype, parts, num_parts, gates, num_gates, nullptr, out);
+}
+
+int hs_program_create_from_layout(hs_engine* eng, int n_local, int dtype, const hs_part* parts, int num_parts,
+                                  const hs_gate* gates, int num_gates, const int32_t* init_phys, hs_program** out) {
+  if (!init_phys) return fail(HS_ERR_INVALID, "init_phys is NULL");
+  if (!eng || !(eng->options & HS_PLAN_LAYOUT)) return fail(HS_ERR_INVALID, "a given initial layout needs HS_PLAN_LAYOUT");
+  if (n_local < 1 || n_local > 62) return fail(HS_ERR_INVALID, "n_local outside [1, 62]");
+  std::vector<char> seen(n_local, 0);
+  for (int q = 0; q < n_local; ++q) {
+    if (init_phys[q] < 0 || init_phys[q] >= n_local || seen[init_phys[q]])
+      return fail(HS_ERR_INVALID, "init_phys is not a permutation of 0..n_local-1");
+    seen[init_phys[q]] = 1;
+  }
+  return program_create(eng, n_local, dtype, parts, num_parts, gates, num_gates, init_phys, out);
+}
+
+static int program_create(hs_engine* eng, int n_local, int dtype, const hs_part* parts, int num_parts,
+                          const hs_gate* gates, int num_gates, const int32_t* init_phys, hs_program** out) {
   if (!eng || !out) return fail(HS_ERR_INVALID, "engine/out is NULL");
   *out = nullptr;
   if (int s = check_dtype(dtype)) return s;
@@ -143,7 +167,7 @@ int hs_program_create(hs_engine* eng, int n_local, int dtype, const hs_part* par
   {
     std::string err;
     int s = plan_program(n_local, dtype, tile_for(eng, dtype), eng->options, parts, num_parts, gates, num_gates,
-                         prog->plans, err, &prog->init_phys);
+                         prog->plans, err, &prog->init_phys, init_phys);
     if (s != HS_OK) return fail(s, err);
   }
   prog->user_parts = num_parts;
@@ -476,6 +500,37 @@ int hs_pack_segments(const void* src, void* dst, int num_bits, int dtype, const 
 int hs_unpack_segments(const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos, int nseg,
                        void* stream) {
   return segments(false, src, dst, num_bits, dtype, seg_pos, nseg, stream);
+}
+
+static int segments_range(bool pack, const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos,
+                          int nseg, int64_t inner_begin, int64_t inner_count, void* stream) {
+  if (!src || !dst || (nseg && !seg_pos)) return fail(HS_ERR_INVALID, "NULL argument");
+  if (src == dst) return fail(HS_ERR_INVALID, "pack/unpack are out-of-place");
+  if (int s = check_dtype(dtype)) return s;
+  if (nseg < 0 || nseg > 8 || num_bits < nseg || num_bits > 62)
+    return fail(HS_ERR_INVALID, "segment bits outside range");
+  for (int k = 0; k < nseg; ++k) {
+    if (seg_pos[k] < 0 || seg_pos[k] >= num_bits) return fail(HS_ERR_INVALID, "segment position outside state");
+    if (k && seg_pos[k] <= seg_pos[k - 1]) return fail(HS_ERR_INVALID, "segment positions not ascending");
+  }
+  const int64_t inner = int64_t(1) << (num_bits - nseg);
+  if (inner_begin < 0 || inner_count < 0 || inner_begin + inner_count > inner)
+    return fail(HS_ERR_INVALID, "inner range outside the segments");
+  if (inner_count == 0) return HS_OK;
+  HS_CUDA(launch_segments_range(pack, src, dst, num_bits, dtype, seg_pos, nseg, inner_begin, inner_count,
+                                sms_of_current(), (cudaStream_t)stream),
+          "segment range kernel");
+  return HS_OK;
+}
+
+int hs_pack_segments_range(const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos, int nseg,
+                           int64_t inner_begin, int64_t inner_count, void* stream) {
+  return segments_range(true, src, dst, num_bits, dtype, seg_pos, nseg, inner_begin, inner_count, stream);
+}
+
+int hs_unpack_segments_range(const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos, int nseg,
+                             int64_t inner_begin, int64_t inner_count, void* stream) {
+  return segments_range(false, src, dst, num_bits, dtype, seg_pos, nseg, inner_begin, inner_count, stream);
 }
 
 int hs_fp64_peak(double* tflops, void* stream) {

@@ -70,23 +70,46 @@ struct Gen {
         if (i >> k & 1) u[i] ^= swz_host(1u << rpos[k], c128);
     return u;
   }
-  bool cluster = false;  // slots live in the shared memory of the cluster's CTAs (CL_LD / CL_ST)
-  void load_regs(const uint8_t* rpos) {
+  // Cluster tiles: slot s lives in CTA s >> TC. A register's slot is this
+  // CTA's own when the thread bits that carry the CTA rank (lowc..) map onto
+  // the top tile locations TC.. and the register's own bits stay below TC;
+  // own slots take plain shared-memory accesses, the rest go through DSMEM.
+  bool cluster = false;
+  int TC = 0, cl = 0, lowc = 0;
+  bool rank_aligned(const uint8_t* npos) const {
+    for (int r = 0; r < cl; ++r)
+      if (npos[lowc + r] != TC + r) return false;
+    return true;
+  }
+  bool reg_local(const uint8_t* npos, uint32_t u) const {
+    return !cluster || (rank_aligned(npos) && (u >> TC) == 0);
+  }
+  bool phase_local(const uint8_t* rpos, const uint8_t* npos) {
+    auto u = slot_xor(rpos);
+    for (int i = 0; i < nreg; ++i)
+      if (!reg_local(npos, u[i])) return false;
+    return true;
+  }
+  std::string local_slot(uint32_t u) const {
+    return cluster ? "(st ^ " + std::to_string(u) + "u) & " + std::to_string((1u << TC) - 1) + "u"
+                   : "st ^ " + std::to_string(u) + "u";
+  }
+  void load_regs(const uint8_t* rpos, const uint8_t* npos) {
     auto u = slot_xor(rpos);
     for (int i = 0; i < nreg; ++i) {
-      if (cluster)
+      if (!reg_local(npos, u[i]))
         o << "    CL_LD(st ^ " << u[i] << "u, " << re(i) << ", " << im(i) << ");\n";
       else
-        o << "    { const C v = sm[st ^ " << u[i] << "u]; " << re(i) << " = v.x; " << im(i) << " = v.y; }\n";
+        o << "    { const C v = sm[" << local_slot(u[i]) << "]; " << re(i) << " = v.x; " << im(i) << " = v.y; }\n";
     }
   }
-  void store_regs(const uint8_t* rpos) {
+  void store_regs(const uint8_t* rpos, const uint8_t* npos) {
     auto u = slot_xor(rpos);
     for (int i = 0; i < nreg; ++i) {
-      if (cluster)
+      if (!reg_local(npos, u[i]))
         o << "    CL_ST(st ^ " << u[i] << "u, " << re(i) << ", " << im(i) << ");\n";
       else
-        o << "    { C v; v.x = " << re(i) << "; v.y = " << im(i) << "; sm[st ^ " << u[i] << "u] = v; }\n";
+        o << "    { C v; v.x = " << re(i) << "; v.y = " << im(i) << "; sm[" << local_slot(u[i]) << "] = v; }\n";
     }
   }
   void cmul_into(int i, const std::string& dr, const std::string& di) {
@@ -347,6 +370,13 @@ struct Gen {
 // final write of the registers into the tile's store order (ending in `sync`)
 void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per_amp) {
   std::ostringstream& o = g.o;
+  // cluster tiles: an exchange whose writes and reads all stay in this CTA's
+  // slots (for every CTA alike: the mapping is the same) needs only a CTA
+  // barrier; otherwise the cluster barrier
+  auto xsync = [&](const uint8_t* r0, const uint8_t* n0, const uint8_t* r1, const uint8_t* n1) -> std::string {
+    if (g.cluster && g.phase_local(r0, n0) && g.phase_local(r1, n1)) return "__syncthreads();";
+    return sync;
+  };
   o << "    " << g.R() << " ";
   for (int i = 0; i < g.nreg; ++i) o << (i ? ", " : "") << "r" << i << ", q" << i;
   o << ";\n    unsigned t, st;\n";
@@ -357,12 +387,12 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
     if (in.op != I_DIAG) g.flush();  // a non-diagonal step: apply the pending run first
     if (in.op == I_PHASE) {
       if (cur) {
-        g.store_regs(cur->rpos);
-        o << "    " << sync << "\n";
+        g.store_regs(cur->rpos, cur->npos);
+        o << "    " << xsync(cur->rpos, cur->npos, in.rpos, in.npos) << "\n";
       }
       g.emit_tdep("t", in.npos);
       o << "    st = swz(t);\n";
-      g.load_regs(in.rpos);
+      g.load_regs(in.rpos, in.npos);
       cur = &in;
       continue;
     }
@@ -379,11 +409,14 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   g.flush(true);  // pending diagonal run + the part's scalar
   if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
   o << "    // fp64_instr_per_amp " << g.ops / g.nreg << "\n";
-  if (pl.launch.fin_sync) o << "    " << sync << "\n";
+  // the final write goes to the store order; the read-out after it is local
+  const std::string fs = xsync(cur->rpos, cur->npos, pl.launch.fin_rpos, pl.launch.fin_npos);
+  if (pl.launch.fin_sync) o << "    " << fs << "\n";
   g.emit_tdep("t", pl.launch.fin_npos);
   o << "    st = swz(t);\n";
-  g.store_regs(pl.launch.fin_rpos);
-  o << "    " << sync << "\n";
+  g.store_regs(pl.launch.fin_rpos, pl.launch.fin_npos);
+  o << "    " << (g.cluster && g.phase_local(pl.launch.fin_rpos, pl.launch.fin_npos) ? "__syncthreads();" : sync)
+    << "\n";
 }
 
 // Parts wider than one CTA's tile (c128 w = 13, 14; c64 w = 14, 15): the
@@ -403,6 +436,9 @@ std::string jit_source_cluster(const PartPlan& pl, int dtype, int n_local, doubl
   for (int i = 0; i < g.nreg; ++i) g.var[i] = i;
   g.cluster = true;
   const int T = g.T, RB = g.RB, cl = pl.launch.cluster_log, TC = T - cl, lowc = TC - RB, NT = 1 << lowc;
+  g.TC = TC;
+  g.cl = cl;
+  g.lowc = lowc;
   const int amp = g.c128 ? 16 : 8;
   const char* C = g.c128 ? "double2" : "float2";
   const char* V = g.c128 ? "v2.f64" : "v2.f32";
@@ -473,7 +509,10 @@ std::string jit_source_cluster(const PartPlan& pl, int dtype, int n_local, doubl
       << "u)) * " << amp << "u)), \"l\"(psi + (base | " << hi(pl.launch.tpos, j) << "ull)) : \"memory\");\n";
   }
   o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\" ::: \"memory\");\n";
-  o << "    CL_SYNC();\n";
+  const Instr* first = nullptr;
+  for (const Instr& in : pl.prog)
+    if (in.op == I_PHASE) { first = &in; break; }
+  o << "    " << (first && g.phase_local(first->rpos, first->npos) ? "__syncthreads();" : "CL_SYNC();") << "\n";
   emit_program(g, pl, "CL_SYNC();", fp64_per_amp);
   if (oop) {
     o << "    const unsigned long long obase = ((unsigned long long)tt >> " << (n_local - T) << " << " << n_local

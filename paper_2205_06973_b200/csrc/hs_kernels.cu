@@ -552,6 +552,54 @@ cudaError_t launch_segments(bool pack, const void* in, void* out, int nbits, int
   return cudaGetLastError();
 }
 
+// ranged segment pack/unpack (in-place chunked layout switches): element m
+// of segment k for inner offsets [begin, begin + count) <-> packed[k * count + m]
+struct SegRangeParams {
+  int8_t seg_pos[8];
+  int32_t nseg;
+  int32_t nbits;
+  int64_t begin, count;
+};
+
+template <typename C, bool PACK>
+__global__ void seg_range_kernel(const C* __restrict__ in, C* __restrict__ out, SegRangeParams p) {
+  const uint64_t total = uint64_t(p.count) << p.nseg;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = i / uint64_t(p.count), m = i - k * uint64_t(p.count);
+    uint64_t idx = uint64_t(p.begin) + m;
+    for (int b = 0; b < p.nseg; ++b) {  // insert segment bit b at seg_pos[b] (ascending)
+      const int q = p.seg_pos[b];
+      const uint64_t lo = idx & ((1ull << q) - 1);
+      idx = ((idx ^ lo) << 1) | lo | (((k >> b) & 1ull) << q);
+    }
+    if (PACK) out[i] = in[idx];
+    else out[idx] = in[i];
+  }
+}
+
+cudaError_t launch_segments_range(bool pack, const void* in, void* out, int nbits, int dtype, const int32_t* seg_pos,
+                                  int nseg, int64_t begin, int64_t count, int num_sms, cudaStream_t s) {
+  SegRangeParams p;
+  p.nbits = nbits;
+  p.nseg = nseg;
+  p.begin = begin;
+  p.count = count;
+  for (int k = 0; k < nseg; ++k) p.seg_pos[k] = (int8_t)seg_pos[k];
+  const uint64_t n = uint64_t(count) << nseg;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
+  if (blocks < 1) blocks = 1;
+  if (dtype == HS_C128) {
+    if (pack) seg_range_kernel<double2, true><<<(unsigned)blocks, 256, 0, s>>>((const double2*)in, (double2*)out, p);
+    else seg_range_kernel<double2, false><<<(unsigned)blocks, 256, 0, s>>>((const double2*)in, (double2*)out, p);
+  } else {
+    if (pack) seg_range_kernel<float2, true><<<(unsigned)blocks, 256, 0, s>>>((const float2*)in, (float2*)out, p);
+    else seg_range_kernel<float2, false><<<(unsigned)blocks, 256, 0, s>>>((const float2*)in, (float2*)out, p);
+  }
+  return cudaGetLastError();
+}
+
 // max |a - b|: non-negative doubles order like their bit patterns
 template <typename C>
 __global__ void maxdiff_kernel(const C* __restrict__ a, const double2* __restrict__ b, int64_t n,

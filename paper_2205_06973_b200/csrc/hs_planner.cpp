@@ -696,12 +696,15 @@ int plan_restore(int n_local, int dtype, int tile_max, uint32_t options, std::ve
 
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                  const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
-                 std::vector<int32_t>* init_phys) {
+                 std::vector<int32_t>* init_phys, const int32_t* given_init) {
   plans.assign(num_parts, PartPlan());
   const bool layout = (options & HS_PLAN_LAYOUT) && num_parts > 0 && n_local > 0;
   std::vector<int32_t> phys(std::max(n_local, 1)), inv(std::max(n_local, 1));
   for (int q = 0; q < n_local; ++q) phys[q] = inv[q] = q;
-  if (layout && (options & HS_PLAN_INIT_LAYOUT)) {
+  if (given_init) {  // the caller's buffer arrives in this layout (e.g. after an in-place switch)
+    for (int q = 0; q < n_local; ++q) phys[q] = given_init[q];
+    for (int q = 0; q < n_local; ++q) inv[phys[q]] = q;
+  } else if (layout && (options & HS_PLAN_INIT_LAYOUT)) {
     // the state starts as a basis state, which is one amplitude in any
     // layout: start with part 0's qubits on the lowest positions (its reads
     // become one contiguous run per tile); qubits whose home they take move

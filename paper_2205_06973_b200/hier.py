@@ -216,12 +216,15 @@ class PartProgram:
     once; ``run`` only launches."""
 
     def __init__(self, n_local: int, exes: Sequence[ExecutablePart], dtype="complex128", device=None,
-                 options: int | None = None, basis_start: bool = False):
+                 options: int | None = None, basis_start: bool = False, init_layout: Sequence[int] | None = None):
         """``options``: planner bits (``_native.HS_PLAN_*``); default: the
         engine default plus ``HS_PLAN_JIT`` / ``HS_PLAN_LAYOUT`` by state
         size. ``basis_start``: the program will only be run on basis states
         prepared with :meth:`init_basis`, so it may pick its initial layout
-        (``HS_PLAN_INIT_LAYOUT``; ``run`` then expects that layout)."""
+        (``HS_PLAN_INIT_LAYOUT``; ``run`` then expects that layout).
+        ``init_layout``: the buffer arrives with logical position q on
+        physical bit ``init_layout[q]`` (after an in-place layout switch);
+        the program ends in natural order."""
         import torch
 
         self.n_local = n_local
@@ -252,6 +255,11 @@ class PartProgram:
                 free, _ = torch.cuda.mem_get_info(self.device)
                 if 2 * (amp << n_local) + PINGPONG_HEADROOM <= free:
                     options |= _native.HS_PLAN_PINGPONG
+        if init_layout is not None and tuple(init_layout) != tuple(range(n_local)):
+            options |= _native.HS_PLAN_LAYOUT
+            options &= ~_native.HS_PLAN_INIT_LAYOUT
+        else:
+            init_layout = None
         self.options = options
         parts, gates, total = _pack(exes)
         out = ctypes.c_void_p()
@@ -259,8 +267,13 @@ class PartProgram:
         with torch.cuda.device(self.device):
             _native.check(lib.hs_engine_set_options(eng, options))
             try:
-                _native.check(lib.hs_program_create(eng, n_local, code, parts, len(exes), gates, total,
-                                                    ctypes.byref(out)))
+                if init_layout is None:
+                    _native.check(lib.hs_program_create(eng, n_local, code, parts, len(exes), gates, total,
+                                                        ctypes.byref(out)))
+                else:
+                    phys = (ctypes.c_int32 * n_local)(*[int(x) for x in init_layout])
+                    _native.check(lib.hs_program_create_from_layout(eng, n_local, code, parts, len(exes), gates,
+                                                                    total, phys, ctypes.byref(out)))
             finally:
                 lib.hs_engine_set_options(eng, _native.default_options())
         self._h = out.value

@@ -97,25 +97,68 @@ class DeviceOps:
 
         return torch.empty_like(t)
 
+    def empty(self, count, like):
+        import torch
+
+        return torch.empty(count, dtype=like.dtype, device=like.device)
+
+    def _range(self, fn, src, dst, num_bits, seg_pos, begin, count):
+        import ctypes
+
+        import torch
+
+        from .statevec import native_dtype
+
+        lib = _native.load()
+        sp = (ctypes.c_int32 * max(1, len(seg_pos)))(*seg_pos)
+        t = src if src.is_cuda else dst
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+        _native.check(getattr(lib, fn)(src.data_ptr(), dst.data_ptr(), num_bits, native_dtype(t), sp, len(seg_pos),
+                                       begin, count, stream))
+
+    def pack_range(self, shard, staging, num_bits, seg_pos, begin, count):
+        """staging[k * count + m] = shard[segment k, inner offset begin + m]"""
+        self._range("hs_pack_segments_range", shard, staging, num_bits, seg_pos, begin, count)
+
+    def unpack_range(self, staging, shard, num_bits, seg_pos, begin, count):
+        self._range("hs_unpack_segments_range", staging, shard, num_bits, seg_pos, begin, count)
+
+
+#: staging for one chunk of an in-place switch, all segments together
+SWITCH_CHUNK_BYTES = 256 << 20
+
 
 class ShardedRun:
-    """Plan once (layouts, switch schedules, one device program over all
-    parts in rank-local coordinates), run many times."""
+    """Plan once (layouts, switch schedules, one device program per run of
+    parts between switches, in rank-local coordinates), run many times.
+
+    Switches are in place and chunked (``switch``), so a rank needs its shard
+    plus a small staging buffer: 36 qubits over 8 GPUs (128 GiB shards) fit.
+    After a switch the incoming rank qubits sit on the bit positions of the
+    outgoing ones; the next segment's program takes that physical layout as
+    its initial layout and ends in natural order."""
 
     def __init__(self, circuit, partition, num_rank_bits: int, group=None, device=None, ops=None,
-                 dtype="complex128", program=True):
+                 dtype="complex128", program=True, chunk_bytes: int = SWITCH_CHUNK_BYTES, basis_start: bool = True,
+                 loopback: bool = False):
+        """``loopback``: all ranks live in this process on one device
+        (``run_loopback``); no process group is used."""
         import torch.distributed as dist
 
         self.circuit = circuit
         self.partition = partition
         self.p = num_rank_bits
         self.group = group
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if loopback:
+            self.rank, self.world = 0, 1 << num_rank_bits
+        else:
+            self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+            self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         if self.world != 1 << num_rank_bits:
             raise ValueError(f"{self.world} ranks cannot hold {num_rank_bits} rank bits")
         self.n = circuit.num_qubits
         self.n_local = self.n - num_rank_bits
+        self.chunk_bytes = int(chunk_bytes)
         self.first, self.layouts, switches = plan_layouts(circuit, partition, num_rank_bits)
         self.switch_at = {i: (old, new, st) for i, old, new, st in switches}
         self.exes, self.bounds = [], []
@@ -123,25 +166,55 @@ class ShardedRun:
             e = _part_exes(circuit, partition, i, lay)
             self.bounds.append((len(self.exes), len(e)))
             self.exes += e
-        self.program = (PartProgram(self.n_local, self.exes, dtype=dtype, device=device,
-                                    options=_native.default_options() & ~_native.HS_PLAN_LAYOUT)
-                        if program and self.exes else None)
+        # segments: runs of parts between switches, each one device program
+        starts = [0] + sorted(i for i in self.switch_at if i > 0)
+        ends = starts[1:] + [len(self.layouts)]
+        self.segments = list(zip(starts, ends))
         self.ops = ops or DeviceOps()
+        self.programs = []
+        if program:
+            for si, (a, b) in enumerate(self.segments):
+                ex = self.exes[self.bounds[a][0]:self.bounds[b - 1][0] + self.bounds[b - 1][1]] if b > a else []
+                if not ex:
+                    self.programs.append(None)
+                    continue
+                init = None if si == 0 else self.arrival_layout(*self.switch_at[a][:2])
+                self.programs.append(PartProgram(self.n_local, ex, dtype=dtype, device=device, init_layout=init,
+                                                 basis_start=basis_start and si == 0))
+        self.program = self.programs[0] if self.programs else None
         self.stats = CommStats(self.n, num_rank_bits, len(self.layouts),
                                [st for _, _, st in self.switch_at.values()])
 
     def part_infos(self):
-        return [self.program.info(i) for i in range(len(self.exes))]
+        return [pr.info(i) for pr in self.programs if pr is not None for i in range(pr.num_parts)]
 
     def comm_summary(self) -> dict:
         return {"switches": self.stats.num_switches, "bytes_remote_total": self.stats.total_bytes,
                 "remote_fraction_of_state": self.stats.total_bytes / float((1 << self.n) * 16)}
 
-    def _exchange(self, packed, recv, out_segs, incoming, c):
+    @staticmethod
+    def switch_plan(old: RankLayout, new: RankLayout):
+        """Offset positions of the outgoing qubits A (ascending) and the
+        incoming qubits B, bit i of a segment / slot index = A[i] / B[i]."""
+        A = [q for q in old.local if q in new.process]
+        B = [q for q in old.process if q in new.local]
+        pa = [old.local.index(q) for q in A]
+        return A, B, pa
+
+    @classmethod
+    def arrival_layout(cls, old: RankLayout, new: RankLayout):
+        """Physical offset bit of each of ``new.local``'s qubits after the
+        in-place switch: kept qubits stay, B[i] lands on A[i]'s position."""
+        A, B, pa = cls.switch_plan(old, new)
+        where = {q: j for j, q in enumerate(old.local)}
+        for i, q in enumerate(B):
+            where[q] = pa[i]
+        return tuple(where[q] for q in new.local)
+
+    def _exchange(self, packed, recv, out_segs, incoming, seg):
         """Batched P2P: my segment k -> peer; slot j of recv <- source."""
         import torch.distributed as dist
 
-        seg = packed.numel() >> c
         reqs = []
         for s in out_segs:
             chunk = packed[s.index * seg:(s.index + 1) * seg]
@@ -158,35 +231,92 @@ class ShardedRun:
                 w.wait()
 
     def switch(self, shard, old: RankLayout, new: RankLayout):
-        """Layout switch of this rank's shard; returns the new shard."""
-        packed_order, out_segs, incoming, recv_order, c = switch_schedule(old, new, self.rank)
-        old_order = tuple(old.local)
-        packed = self.ops.permute(shard, old_order, packed_order)
-        recv = shard  # the old shard is dead once packed: receive into it
-        self._exchange(packed, recv, out_segs, incoming, c)
-        return self.ops.permute(recv, recv_order, tuple(new.local))
+        """In-place, chunked layout switch of this rank's shard (dist.py:520-526).
+
+        Segment k of the shard (the A qubits spell k) goes to one peer; the
+        data arriving from the source whose B qubits spell j lands in the
+        positions of segment j, which were just sent. Chunk by chunk of inner
+        offsets: pack every segment's chunk into staging, one batched
+        send/recv, unpack into the same offsets. Returns the shard (same
+        buffer) in ``arrival_layout(old, new)``."""
+        _, out_segs, incoming, _, c = switch_schedule(old, new, self.rank)
+        A, B, pa = self.switch_plan(old, new)
+        l = self.n_local
+        inner = 1 << (l - c)
+        amp = shard.element_size()
+        chunk = max(1, min(inner, self.chunk_bytes // (amp << c)))
+        send = self.ops.empty(chunk << c, shard)
+        recv = self.ops.empty(chunk << c, shard)
+        for begin in range(0, inner, chunk):
+            cnt = min(chunk, inner - begin)
+            self.ops.pack_range(shard, send, l, pa, begin, cnt)
+            self._exchange(send, recv, out_segs, incoming, cnt)
+            self.ops.unpack_range(recv, shard, l, pa, begin, cnt)
+        return shard
 
     def run(self, shard, events=None, run_part=None):
         """All parts in order on this rank's shard (switches included);
-        returns the final shard (a new tensor after any switch)."""
+        returns the final shard in natural order of the last layout.
+        ``events`` receives ("switch" | "parts", cuda event) marks."""
         import torch
 
-        for i in range(len(self.layouts)):
-            if i in self.switch_at:
-                old, new, _ = self.switch_at[i]
-                shard = self.switch(shard, old, new)
-            start, count = self.bounds[i]
-            if count:
-                if run_part is not None:
-                    for j in range(start, start + count):
-                        run_part(shard, self.exes[j])
-                else:
-                    self.program.run(shard, start, count)
+        def mark(kind):
             if events is not None:
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record()
-                events.append(ev)
+                events.append((kind, ev))
+
+        for si, (a, b) in enumerate(self.segments):
+            if a in self.switch_at:
+                old, new, _ = self.switch_at[a]
+                shard = self.switch(shard, old, new)
+                mark("switch")
+                if run_part is not None:  # host stand-ins run parts in natural order
+                    shard = self.ops.to_natural(shard, self.arrival_layout(old, new))
+            if run_part is not None:
+                for i in range(a, b):
+                    start, count = self.bounds[i]
+                    for j in range(start, start + count):
+                        run_part(shard, self.exes[j])
+            elif self.programs[si] is not None:
+                self.programs[si].run(shard)
+            mark("parts")
         return shard
+
+
+def run_loopback(run: ShardedRun, shards):
+    """Every rank of ``run`` (built with ``loopback=True``) on one device:
+    the same in-place chunked switches (pack / unpack kernels, chunk by
+    chunk) with the peer transfers done as device copies, and the same
+    segment programs. For checking the distributed path's device pieces on
+    one GPU; returns the final shards (natural order of the last layout)."""
+    R = 1 << run.p
+    l = run.n_local
+    for si, (a, b) in enumerate(run.segments):
+        if a in run.switch_at:
+            old, new, _ = run.switch_at[a]
+            sched = [switch_schedule(old, new, r) for r in range(R)]
+            c = sched[0][4]
+            _, _, pa = run.switch_plan(old, new)
+            inner = 1 << (l - c)
+            amp = shards[0].element_size()
+            chunk = max(1, min(inner, run.chunk_bytes // (amp << c)))
+            send = [run.ops.empty(chunk << c, shards[0]) for _ in range(R)]
+            recv = [run.ops.empty(chunk << c, shards[0]) for _ in range(R)]
+            for begin in range(0, inner, chunk):
+                cnt = min(chunk, inner - begin)
+                for r in range(R):
+                    run.ops.pack_range(shards[r], send[r], l, pa, begin, cnt)
+                for r in range(R):
+                    for seg in sched[r][1]:
+                        slot = sched[seg.peer][2][r]
+                        recv[seg.peer][slot * cnt:(slot + 1) * cnt].copy_(send[r][seg.index * cnt:(seg.index + 1) * cnt])
+                for r in range(R):
+                    run.ops.unpack_range(recv[r], shards[r], l, pa, begin, cnt)
+        if run.programs[si] is not None:
+            for r in range(R):
+                run.programs[si].run(shards[r])
+    return shards
 
 
 def _wire(t):
@@ -241,5 +371,5 @@ def shard_positions(layout: RankLayout, rank: int):
     return g
 
 
-__all__ = ["ShardedRun", "ShardedState", "DeviceOps", "switch_schedule", "simulate_distributed_group",
+__all__ = ["ShardedRun", "ShardedState", "DeviceOps", "switch_schedule", "simulate_distributed_group", "run_loopback",
            "shard_positions", "storage_order", "math"]

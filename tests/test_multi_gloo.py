@@ -18,7 +18,40 @@ import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
 
+def _compose(k, m, seg_pos, nbits):
+    """index with segment bits k at seg_pos (ascending) and inner offset m elsewhere"""
+    idx = np.asarray(m, dtype=np.int64).copy()
+    for b, q in enumerate(seg_pos):
+        lo = idx & ((1 << q) - 1)
+        idx = ((idx ^ lo) << 1) | lo | (((k >> b) & 1) << q)
+    return idx
+
+
 class HostOps:
+    """numpy stand-ins for the rank-local device kernels"""
+
+    def empty(self, count, like):
+        return torch.empty(count, dtype=like.dtype)
+
+    def pack_range(self, shard, staging, nbits, seg_pos, begin, count):
+        m = np.arange(begin, begin + count, dtype=np.int64)
+        for k in range(1 << len(seg_pos)):
+            staging[k * count:(k + 1) * count] = shard[torch.from_numpy(_compose(k, m, seg_pos, nbits))]
+
+    def unpack_range(self, staging, shard, nbits, seg_pos, begin, count):
+        m = np.arange(begin, begin + count, dtype=np.int64)
+        for k in range(1 << len(seg_pos)):
+            shard[torch.from_numpy(_compose(k, m, seg_pos, nbits))] = staging[k * count:(k + 1) * count]
+
+    def to_natural(self, shard, phys):
+        """logical position q sits on physical bit phys[q]: gather into natural order"""
+        n = len(phys)
+        i = np.arange(1 << n, dtype=np.int64)
+        src = np.zeros_like(i)
+        for q, b in enumerate(phys):
+            src |= ((i >> q) & 1) << b
+        return shard[torch.from_numpy(src)].clone()
+
     def permute(self, src, old_order, new_order):
         n = len(old_order)
         where = {q: b for b, q in enumerate(new_order)}
@@ -53,7 +86,8 @@ def _worker(rank, world, port, qasm, parts, p, out):
         from paper_2205_06973_b200.qasm import parse_qasm
 
         c = parse_qasm(qasm)
-        run = ShardedRun(c, partition_of(parts), p, ops=HostOps(), program=False)
+        # a tiny chunk so each switch takes several pack/exchange/unpack rounds
+        run = ShardedRun(c, partition_of(parts), p, ops=HostOps(), program=False, chunk_bytes=64)
         shard = torch.zeros(1 << run.n_local, dtype=torch.complex128)
         if rank == 0:
             shard[0] = 1.0
