@@ -545,6 +545,50 @@ class HierarchicalRun:
         self.program = PartProgram(circuit.num_qubits, self.exes, dtype=dtype, device=device, options=options,
                                    basis_start=basis_start)
 
+    def run_stream(self, inputs, outputs, buffers=None, stream=None) -> None:
+        """Simulate the circuit on a sequence of host states: ``inputs[i]``
+        (pinned host tensors, natural order, e.g. many initial states) ->
+        ``outputs[i]``. Uploads, part passes and downloads run on three
+        streams over two device buffers, so step i + 1's upload and step
+        i - 1's download overlap step i's part passes. Returns when the last
+        download is queued (synchronize to read outputs). The program must
+        accept natural-order input (``basis_start=False``)."""
+        import torch
+
+        if self.program.initial_layout != tuple(range(self.program.n_local)):
+            raise ValueError("run_stream needs a program without its own initial layout (basis_start=False)")
+        if len(inputs) != len(outputs):
+            raise ValueError("inputs and outputs differ in length")
+        dev = self.program.device
+        compute = stream or torch.cuda.current_stream(dev)
+        if buffers is None:
+            like = inputs[0]
+            buffers = [torch.empty(like.shape, dtype=self.program.dtype, device=dev) for _ in range(2)]
+        up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        loaded = [torch.cuda.Event() for _ in buffers]
+        done = [torch.cuda.Event() for _ in buffers]
+        free = [None for _ in buffers]
+        for i, (src, dst) in enumerate(zip(inputs, outputs)):
+            b = i % len(buffers)
+            buf = buffers[b]
+            with torch.cuda.stream(up):
+                if free[b] is not None:
+                    up.wait_event(free[b])  # the buffer's previous result is downloaded
+                buf.copy_(src, non_blocking=True)
+                loaded[b].record(up)
+            compute.wait_event(loaded[b])
+            self.program.run(buf, stream=compute)
+            done[b].record(compute)
+            with torch.cuda.stream(down):
+                down.wait_event(done[b])
+                dst.copy_(buf, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(down)
+                free[b] = ev
+        for ev in free:
+            if ev is not None:
+                compute.wait_event(ev)
+
     def trace(self) -> ExecutionTrace:
         return hierarchical_trace(self.circuit, self.partition)
 

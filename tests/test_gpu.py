@@ -387,3 +387,26 @@ def test_sharded_run_loopback_on_one_gpu(golden):
             assert np.max(np.abs(full - states[f"c{i}"])) < 1e-10, (i, d["p"])
             checked += 1
     assert checked >= 5
+
+
+def test_run_stream_many_initial_states():
+    """HierarchicalRun.run_stream: several host initial states through the
+    overlapped upload / parts / download pipeline, each against the oracle."""
+    c = configs.build("c2@20")
+    part = partition_dfs(build_dag(c), 12)
+    run = HierarchicalRun(c, part, basis_start=False)
+    n = c.num_qubits
+    rng = np.random.default_rng(5)
+    ins, outs, refs = [], [], []
+    parts = [(p.gate_indices, p.qubits) for p in part.parts]
+    for k in range(5):
+        x = np.zeros(1 << n, dtype=np.complex128)
+        x[rng.integers(0, 1 << n, 3)] = rng.standard_normal(3)
+        x /= np.linalg.norm(x)
+        ins.append(torch.from_numpy(x).pin_memory())
+        outs.append(torch.empty(1 << n, dtype=torch.complex128).pin_memory())
+        refs.append(c_oracle.execute_parts(c, parts, initial=x))
+    run.run_stream(ins, outs)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert float(np.max(np.abs(o.numpy() - r))) < 1e-10
