@@ -224,6 +224,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     num_launches = (run.program.num_launches if not dist
                     else sum(pr.num_launches for pr in run.programs if pr is not None))
     bytes_per_pass = 2 * (1 << n_local) * 16
+    launch_owner = [run.program.info(j)["user_part"] for j in range(num_launches)] if not dist else []
     state = allocate(n_local, "complex128", dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -284,8 +285,16 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
                     seg_ms += prev.elapsed_time(e)
             continue
         d = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)]
-        durs += d[:num_parts]
-        restore_ms += sum(d[num_parts:])
+        # a launch belongs to a caller's part (wide parts may take several
+        # sub-pass launches) or is a gate-free layout launch (user_part -1)
+        per_part = [0.0] * num_parts
+        for j, dj in enumerate(d):
+            u = launch_owner[j]
+            if u >= 0:
+                per_part[u] += dj
+            else:
+                restore_ms += dj
+        durs += per_part
     # only the part kernels sit between the events when not distributed
     if dist:
         t = torch.tensor([total_ms], device=dev)
@@ -330,7 +339,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
                        "runs every part and downloads the final state; upload/parts/download of consecutive "
                        "steps overlap on three streams"}
 
-    info = [run.program.info(i) for i in range(num_parts)] if not dist else run.part_infos()
+    info = ([run.program.info(i) for i in range(num_launches)] if not dist else run.part_infos())
     # FP64 roofline: issued FP64 pipe work of the part kernels vs a measured DFMA peak
     import ctypes
 
@@ -436,7 +445,8 @@ def main(argv=None):
             "time_to_solution_ms": g["ms_step"],
             "fp64_flops_per_step_paper_count": flops,
             "fp64": g["fp64"],
-            "phases_per_part": [i["phases"] for i in infos],
+            "phases_per_launch": [i["phases"] for i in infos],
+            "launches_per_step": g["num_launches"],
             "comm": g["comm"]}
     if not args.no_cpu_baseline and world == 1:
         r = cpu_arm(args, cfg, circuit, part, t_part, 2, 1)

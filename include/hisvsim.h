@@ -99,6 +99,7 @@ typedef struct {
   int32_t restore;        /* 1: a layout-restore launch (no gates) */
   int32_t compiled;       /* 1: runs as an NVRTC-compiled kernel (HS_PLAN_JIT) */
   float fp64_instr_per_amp; /* FP64 pipe instructions per amplitude (FMA = 1) */
+  int32_t user_part;      /* the caller's part this launch belongs to (-1: layout launch) */
 } hs_part_info;
 
 /* planner options (hs_engine_set_options / hs_plan_part) */
@@ -125,6 +126,11 @@ typedef struct {
  * the last part natural order (no restore launches). An odd part count runs
  * part 0 in place. */
 #define HS_PLAN_PINGPONG 0x40u
+/* parts wider than one CTA's tile (k = 13, 14 complex128): run each as one
+ * compiled cluster-tile pass (needs HS_PLAN_JIT). Without it such a part runs
+ * as a short sequence of passes over sub-parts of its gates that fit the tile
+ * (the hierarchical idea one level down; same results). */
+#define HS_PLAN_CLUSTER 0x80u
 #define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
 
 typedef struct hs_engine hs_engine;

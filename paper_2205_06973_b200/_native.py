@@ -75,6 +75,7 @@ class HsPartInfo(ctypes.Structure):
         ("restore", ctypes.c_int32),
         ("compiled", ctypes.c_int32),
         ("fp64_instr_per_amp", ctypes.c_float),
+        ("user_part", ctypes.c_int32),
     ]
 
 
@@ -190,7 +191,7 @@ def engine_query(device: int) -> dict:
 
 
 HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY, HS_PLAN_LAYOUT, HS_PLAN_JIT = 0x1, 0x2, 0x4, 0x8, 0x10
-HS_PLAN_INIT_LAYOUT, HS_PLAN_PINGPONG = 0x20, 0x40
+HS_PLAN_INIT_LAYOUT, HS_PLAN_PINGPONG, HS_PLAN_CLUSTER = 0x20, 0x40, 0x80
 HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY
 
 

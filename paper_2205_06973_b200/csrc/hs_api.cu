@@ -244,18 +244,18 @@ static int run_range(hs_program* prog, void* state, int64_t batch, int first, in
     void* psi = bufs[pl.launch.in_buf];
     void* psi_out = bufs[pl.launch.out_buf];
     if (pl.jit && pl.launch.cluster_log > 0) {
-      // cluster tile: 2^cluster_log CTAs of 2^(T - cluster_log) slots, two per SM
+      // cluster tile: clusters of 2^cluster_log CTAs (one per SM), each CTA
+      // two teams over three buffers of 2^(T - cluster_log) slots (hs_jit.cpp)
       long long ntiles = (long long)(batch << (prog->n_local - pl.launch.T));
       void* args[] = {&psi, &psi_out, &ntiles};
       const int csize = 1 << pl.launch.cluster_log;
       const int TC = pl.launch.T - pl.launch.cluster_log;
-      const int per_sm = (TC - pl.launch.RB) >= 9 ? 1 : 2;  // as the kernel's __launch_bounds__
-      long long nclusters = (long long)eng->num_sms * per_sm / csize;
-      if (nclusters > ntiles) nclusters = ntiles;
+      long long nclusters = (long long)eng->num_sms / csize;
+      if (nclusters > (ntiles + 1) / 2) nclusters = (ntiles + 1) / 2;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(nclusters * csize));
-      cfg.blockDim = dim3(1u << (TC - pl.launch.RB));
-      cfg.dynamicSmemBytes = size_t(prog->dtype == HS_C128 ? 16 : 8) << TC;
+      cfg.blockDim = dim3(2u << (TC - pl.launch.RB));
+      cfg.dynamicSmemBytes = 3 * (size_t(prog->dtype == HS_C128 ? 16 : 8) << TC) + 128;
       cfg.stream = s;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;

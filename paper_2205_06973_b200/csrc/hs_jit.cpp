@@ -368,13 +368,14 @@ struct Gen {
 // The part's program on one tile: register declarations, phases (shared
 // memory exchanges separated by `sync`), gates, the part's scalar, and the
 // final write of the registers into the tile's store order (ending in `sync`)
-void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per_amp) {
+void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per_amp,
+                  const char* local_sync = "__syncthreads();") {
   std::ostringstream& o = g.o;
   // cluster tiles: an exchange whose writes and reads all stay in this CTA's
   // slots (for every CTA alike: the mapping is the same) needs only a CTA
   // barrier; otherwise the cluster barrier
   auto xsync = [&](const uint8_t* r0, const uint8_t* n0, const uint8_t* r1, const uint8_t* n1) -> std::string {
-    if (g.cluster && g.phase_local(r0, n0) && g.phase_local(r1, n1)) return "__syncthreads();";
+    if (g.cluster && g.phase_local(r0, n0) && g.phase_local(r1, n1)) return local_sync;
     return sync;
   };
   o << "    " << g.R() << " ";
@@ -415,123 +416,11 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   g.emit_tdep("t", pl.launch.fin_npos);
   o << "    st = swz(t);\n";
   g.store_regs(pl.launch.fin_rpos, pl.launch.fin_npos);
-  o << "    " << (g.cluster && g.phase_local(pl.launch.fin_rpos, pl.launch.fin_npos) ? "__syncthreads();" : sync)
+  o << "    " << (g.cluster && g.phase_local(pl.launch.fin_rpos, pl.launch.fin_npos) ? local_sync : sync)
     << "\n";
 }
 
-// Parts wider than one CTA's tile (c128 w = 13, 14; c64 w = 14, 15): the
-// 2^T tile is spread over a thread-block cluster of 2^cl CTAs, 2^TC slots
-// each (slot s lives in CTA s >> TC). Each CTA loads and stores its own
-// slots; phase exchanges read and write any CTA's slots through distributed
-// shared memory (mapa + ld/st.shared::cluster) between cluster barriers.
-// A thread's tile-global index is threadIdx.x | rank << (TC - RB).
-std::string jit_source_cluster(const PartPlan& pl, int dtype, int n_local, double* fp64_per_amp) {
-  Gen g;
-  g.c128 = dtype == HS_C128;
-  g.RB = pl.launch.RB;
-  g.T = pl.launch.T;
-  g.n_local = n_local;
-  g.nreg = 1 << g.RB;
-  g.var.resize(g.nreg);
-  for (int i = 0; i < g.nreg; ++i) g.var[i] = i;
-  g.cluster = true;
-  const int T = g.T, RB = g.RB, cl = pl.launch.cluster_log, TC = T - cl, lowc = TC - RB, NT = 1 << lowc;
-  g.TC = TC;
-  g.cl = cl;
-  g.lowc = lowc;
-  const int amp = g.c128 ? 16 : 8;
-  const char* C = g.c128 ? "double2" : "float2";
-  const char* V = g.c128 ? "v2.f64" : "v2.f32";
-  const char* RC = g.c128 ? "d" : "f";
-  std::ostringstream& o = g.o;
-  o << "typedef " << C << " C;\n";
-  o << "__device__ __forceinline__ unsigned swz(unsigned s) { return s ^ "
-    << (g.c128 ? "(((s >> 3) ^ (s >> 6) ^ (s >> 9) ^ (s >> 12)) & 7u)" : "(((s >> 4) ^ (s >> 8) ^ (s >> 12)) & 15u)")
-    << "; }\n";
-  // the swizzle only changes bits below 4, so slot s and swz(s) share a CTA
-  o << "__device__ __forceinline__ unsigned cl_addr(unsigned sbase, unsigned sl) {\n  unsigned ra;\n"
-    << "  asm volatile(\"mapa.shared::cluster.u32 %0, %1, %2;\" : \"=r\"(ra) : \"r\"(sbase + (sl & "
-    << ((1u << TC) - 1) << "u) * " << amp << "u), \"r\"(sl >> " << TC << "));\n  return ra;\n}\n";
-  o << "#define CL_ADDR(sl) cl_addr(sbase, (sl))\n";
-  o << "#define CL_ST(sl, x, y) asm volatile(\"st.shared::cluster." << V << " [%0], {%1, %2};\" :: \"r\"(CL_ADDR(sl)), \""
-    << RC << "\"(x), \"" << RC << "\"(y) : \"memory\")\n";
-  o << "#define CL_LD(sl, x, y) asm volatile(\"ld.shared::cluster." << V << " {%0, %1}, [%2];\" : \"=" << RC << "\"(x), \"="
-    << RC << "\"(y) : \"r\"(CL_ADDR(sl)) : \"memory\")\n";
-  o << "#define CL_SYNC() asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\")\n";
-  // two CTAs per SM while 2 x NT threads keep 128 registers each
-  o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << (NT >= 512 ? 1 : 2)
-    << ") hs_jit_part(C* psi, C* psi_out, long long ntiles) {\n";
-  o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
-  o << "  C* sm = reinterpret_cast<C*>(smem_raw);\n";
-  o << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);\n";
-  o << "  unsigned rank, cid, ncl;\n";
-  o << "  asm(\"mov.u32 %0, %%cluster_ctarank;\" : \"=r\"(rank));\n";
-  o << "  asm(\"mov.u32 %0, %%clusterid.x;\" : \"=r\"(cid));\n";
-  o << "  asm(\"mov.u32 %0, %%nclusterid.x;\" : \"=r\"(ncl));\n";
-  o << "  const unsigned ltid = threadIdx.x;\n";
-  o << "  const unsigned tid0 = ltid | (rank << " << lowc << ");\n";
-  // this CTA's slots in canonical order: local l = ltid + (j << lowc), slot
-  // s = l | rank << TC; global offsets of the ltid and rank parts
-  auto dep = [&](const uint8_t* pos, const char* what, int from, int cnt) {
-    std::string e = "0ull";
-    for (int b = 0; b < cnt; ++b)
-      e += " | ((unsigned long long)((" + std::string(what) + " >> " + std::to_string(b) + ") & 1u) << " +
-           std::to_string((int)pos[from + b]) + ")";
-    return e;
-  };
-  const bool oop = pl.launch.oop != 0;
-  o << "  const unsigned long long ga_l = " << dep(pl.launch.tpos, "ltid", 0, lowc) << " | "
-    << dep(pl.launch.tpos, "rank", TC, cl) << ";\n";
-  if (oop)
-    o << "  const unsigned long long go_l = " << dep(pl.launch.opos, "ltid", 0, lowc) << " | "
-      << dep(pl.launch.opos, "rank", TC, cl) << ";\n";
-  o << "  const unsigned sw_l = swz(ltid);\n";  // swz of the ltid part (linear, no rank bits)
-  auto hi = [&](const uint8_t* pos, int j) {
-    uint64_t h = 0;
-    for (int k = 0; k < RB; ++k)
-      if (j >> k & 1) h |= 1ull << pos[lowc + k];
-    return h;
-  };
-  o << "  for (long long tt = cid; tt < ntiles; tt += ncl) {\n";
-  o << "    unsigned tid = tid0; asm volatile(\"\" : \"+r\"(tid));  // keep phase addresses in the loop\n";
-  o << "    const unsigned long long row = (unsigned long long)tt >> " << (n_local - T) << ";\n";
-  o << "    unsigned long long f = (unsigned long long)tt & " << ((1ull << (n_local - T)) - 1) << "ull;\n";
-  for (int b = 0; b < T; ++b) {
-    int p = pl.launch.tpos[b];
-    o << "    { const unsigned long long lo = f & " << ((1ull << p) - 1) << "ull; f = ((f ^ lo) << 1) | lo; }\n";
-  }
-  o << "    const unsigned long long base = (row << " << n_local << ") | f | ga_l;\n";
-  for (int j = 0; j < g.nreg; ++j) {
-    // local index of slot (ltid + (j << lowc)) | rank << TC after the swizzle
-    const uint32_t sx = swz_host(uint32_t(j) << lowc, g.c128) & ((1u << TC) - 1);
-    o << "    asm volatile(\"cp.async." << (g.c128 ? "cg" : "ca") << ".shared.global [%0], [%1], " << amp
-      << ";\" :: \"r\"(sbase + ((sw_l ^ " << sx << "u ^ (swz(rank << " << TC << ") & " << ((1u << TC) - 1)
-      << "u)) * " << amp << "u)), \"l\"(psi + (base | " << hi(pl.launch.tpos, j) << "ull)) : \"memory\");\n";
-  }
-  o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\" ::: \"memory\");\n";
-  const Instr* first = nullptr;
-  for (const Instr& in : pl.prog)
-    if (in.op == I_PHASE) { first = &in; break; }
-  o << "    " << (first && g.phase_local(first->rpos, first->npos) ? "__syncthreads();" : "CL_SYNC();") << "\n";
-  emit_program(g, pl, "CL_SYNC();", fp64_per_amp);
-  if (oop) {
-    o << "    const unsigned long long obase = ((unsigned long long)tt >> " << (n_local - T) << " << " << n_local
-      << ") | go_l";
-    for (int j = 0; j < n_local - T; ++j)
-      o << "\n      | ((((unsigned long long)tt >> " << j << ") & 1ull) << " << (int)pl.launch.fpos[j] << ")";
-    o << ";\n";
-  }
-  for (int j = 0; j < g.nreg; ++j) {
-    const uint32_t sx = swz_host(uint32_t(j) << lowc, g.c128) & ((1u << TC) - 1);
-    o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << hi(oop ? pl.launch.opos : pl.launch.tpos, j)
-      << "ull] = sm[sw_l ^ " << sx << "u ^ (swz(rank << " << TC << ") & " << ((1u << TC) - 1) << "u)];\n";
-  }
-  o << "    __syncthreads();\n  }\n}\n";
-  return o.str();
-}
-
 std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_per_amp = nullptr) {
-  if (pl.launch.cluster_log > 0) return jit_source_cluster(pl, dtype, n_local, fp64_per_amp);
   Gen g;
   g.c128 = dtype == HS_C128;
   g.RB = pl.launch.RB;
@@ -540,8 +429,19 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   g.nreg = 1 << g.RB;
   g.var.resize(g.nreg);
   for (int i = 0; i < g.nreg; ++i) g.var[i] = i;
-  const int T = g.T, RB = g.RB, low = T - RB, NT = 1 << low;
+  // cluster tiles (parts wider than one CTA's tile): 2^cl CTAs, one per SM,
+  // each holding the 2^TC slots s with s >> TC == its rank
+  const int cl = pl.launch.cluster_log, C_SIZE = 1 << cl;
+  const int T = g.T, RB = g.RB, TC = T - cl, low = TC - RB, NT = 1 << low;
+  if (cl > 0) {
+    g.cluster = true;
+    g.TC = TC;
+    g.cl = cl;
+    g.lowc = low;
+  }
+  const uint32_t lmask = (1u << TC) - 1;
   const char* C = g.c128 ? "double2" : "float2";
+  const int amp = g.c128 ? 16 : 8;
   std::ostringstream& o = g.o;
   o << "typedef " << C << " C;\n";
   o << "__device__ __forceinline__ unsigned swz(unsigned s) { return s ^ "
@@ -554,29 +454,86 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   // i % 3; whichever team finishes tile i refills that buffer with tile
   // i + 3 (cp.async, completion counted on the buffer's mbarrier by
   // cp.async.mbarrier.arrive.noinc), so loads stay in flight across tiles.
-  // Teams synchronise with named barriers (1 + team).
-  const int tile_bytes = (g.c128 ? 16 : 8) << T;
+  // Teams synchronise with named barriers (1 + team). Cluster tiles: team t
+  // of every CTA of the cluster works on the same tile; an exchange that
+  // crosses CTAs ends in a team-wide cluster barrier (TEAM_CSYNC: a named
+  // barrier, then one thread release-arrives on that team's mbarrier in
+  // every CTA, then all acquire-wait on their own; two mbarriers alternate
+  // so consecutive uses never share a phase).
+  const int tile_bytes = amp << TC;
   if (NT >= 32)
     o << "#define TEAM_SYNC() asm volatile(\"bar.sync %0, " << NT << ";\" :: \"r\"(bar_id) : \"memory\")\n";
   else  // tiny tiles: both teams share warp 0
     o << "#define TEAM_SYNC() __syncwarp(" << ((1ull << NT) - 1) << "u << (team * " << NT << "u))\n";
+  if (cl > 0) {
+    const char* V = g.c128 ? "v2.f64" : "v2.f32";
+    const char* RC = g.c128 ? "d" : "f";
+    o << "__device__ __forceinline__ unsigned cl_addr(unsigned sbase, unsigned sl) {\n  unsigned ra;\n"
+      << "  asm volatile(\"mapa.shared::cluster.u32 %0, %1, %2;\" : \"=r\"(ra) : \"r\"(sbase + (sl & " << lmask
+      << "u) * " << amp << "u), \"r\"(sl >> " << TC << "));\n  return ra;\n}\n";
+    o << "#define CL_ADDR(sl) cl_addr(sbase, (sl))\n";
+    o << "#define CL_ST(sl, x, y) asm volatile(\"st.shared::cluster." << V << " [%0], {%1, %2};\" :: \"r\"(CL_ADDR(sl)), \""
+      << RC << "\"(x), \"" << RC << "\"(y) : \"memory\")\n";
+    o << "#define CL_LD(sl, x, y) asm volatile(\"ld.shared::cluster." << V << " {%0, %1}, [%2];\" : \"=" << RC << "\"(x), \"="
+      << RC << "\"(y) : \"r\"(CL_ADDR(sl)) : \"memory\")\n";
+    o << "__device__ __forceinline__ void team_csync(unsigned tb, unsigned& k, unsigned bar_id, unsigned tid0) {\n"
+      << "  asm volatile(\"bar.sync %0, " << NT << ";\" :: \"r\"(bar_id) : \"memory\");\n"
+      << "  const unsigned mb = tb + (k & 1u) * 8u;\n"
+      << "  if (tid0 == 0) {\n"
+      << "    for (unsigned q = 0; q < " << C_SIZE << "u; ++q) {\n"
+      << "      unsigned ra;\n"
+      << "      asm volatile(\"mapa.shared::cluster.u32 %0, %1, %2;\" : \"=r\"(ra) : \"r\"(mb), \"r\"(q));\n"
+      << "      asm volatile(\"mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\" :: \"r\"(ra) : \"memory\");\n"
+      << "    }\n  }\n"
+      << "  const unsigned par = (k >> 1) & 1u;\n  unsigned done = 0;\n"
+      << "  while (!done) asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+         "selp.u32 %0, 1, 0, p; }\" : \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\");\n"
+      << "  ++k;\n}\n";
+    o << "#define TEAM_CSYNC() team_csync(tb_team, csync_k, bar_id, tid0)\n";
+  }
   o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * NT << ", 1) hs_jit_part(C* psi, C* psi_out, long long ntiles) {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
   o << "  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + " << 3 * tile_bytes << ");\n";
   o << "  volatile int* issued = reinterpret_cast<volatile int*>(smem_raw + " << 3 * tile_bytes + 32 << ");\n";
   o << "  const unsigned team = threadIdx.x >> " << low << ";\n";
-  o << "  const unsigned tid0 = threadIdx.x & " << (NT - 1) << "u;\n  const unsigned tid = tid0;\n";
+  o << "  const unsigned tid0 = threadIdx.x & " << (NT - 1) << "u;\n";
   o << "  const unsigned bar_id = 1u + team;\n";
+  if (cl > 0) {
+    o << "  unsigned long long* tbar = reinterpret_cast<unsigned long long*>(smem_raw + " << 3 * tile_bytes + 64 << ");\n";
+    o << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem_raw);\n";
+    o << "  unsigned rank, cid, ncl;\n";
+    o << "  asm(\"mov.u32 %0, %%cluster_ctarank;\" : \"=r\"(rank));\n";
+    o << "  asm(\"mov.u32 %0, %%clusterid.x;\" : \"=r\"(cid));\n";
+    o << "  asm(\"mov.u32 %0, %%nclusterid.x;\" : \"=r\"(ncl));\n";
+    o << "  const unsigned tb_team = (unsigned)__cvta_generic_to_shared(&tbar[2 * team]);\n";
+    o << "  unsigned csync_k = 0;\n";
+    o << "  const unsigned sw_rank = swz(rank << " << TC << ") & " << lmask << "u;\n";
+  } else {
+    o << "  const unsigned rank = 0, cid = blockIdx.x, ncl = gridDim.x, sw_rank = 0;\n";
+  }
   o << "  if (threadIdx.x == 0) {\n";
   o << "    for (int b = 0; b < 3; ++b) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << NT
     << ";\" :: \"r\"((unsigned)__cvta_generic_to_shared(&full[b])) : \"memory\");\n";
+  if (cl > 0)
+    o << "    for (int b = 0; b < 4; ++b) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << C_SIZE
+      << ";\" :: \"r\"((unsigned)__cvta_generic_to_shared(&tbar[b])) : \"memory\");\n";
   o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
   o << "    for (int b = 0; b < 3; ++b) issued[b] = 0;\n  }\n";
-  o << "  __syncthreads();\n";
-  // canonical load order: slot s = tid + (j << low); global offset of tid part
-  o << "  unsigned long long ga_tid = 0ull";
-  for (int b = 0; b < low; ++b) o << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << (int)pl.launch.tpos[b] << ")";
-  o << ";\n  const unsigned sw_tid = swz(tid);\n";
+  if (cl > 0)  // every CTA's barriers exist before any peer arrives on them
+    o << "  asm volatile(\"barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;\" ::: \"memory\");\n";
+  else
+    o << "  __syncthreads();\n";
+  // canonical load order of this CTA's slots: s = tid0 + (j << low) + (rank << TC)
+  auto dep = [&](const uint8_t* pos, const char* what, int from, int cnt) {
+    std::string e = "0ull";
+    for (int b = 0; b < cnt; ++b)
+      e += " | ((unsigned long long)((" + std::string(what) + " >> " + std::to_string(b) + ") & 1u) << " +
+           std::to_string((int)pos[from + b]) + ")";
+    return e;
+  };
+  o << "  const unsigned long long ga_tid = " << dep(pl.launch.tpos, "tid0", 0, low) << " | "
+    << dep(pl.launch.tpos, "rank", TC, cl) << ";\n";
+  o << "  const unsigned sw_tid = swz(tid0) ^ sw_rank;\n";
   // tile -> global offset of its slot 0 (zero bits inserted at the tile positions)
   o << "  auto tile_base = [&](long long tt) -> unsigned long long {\n";
   o << "    const unsigned long long row = (unsigned long long)tt >> " << (n_local - T) << ";\n";
@@ -588,9 +545,8 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "    return (row << " << n_local << ") | f | ga_tid;\n  };\n";
   const bool oop = pl.launch.oop != 0;
   if (oop) {  // out of place: the same tile under the next layout
-    o << "  unsigned long long go_tid = 0ull";
-    for (int b = 0; b < low; ++b) o << " | ((unsigned long long)((tid >> " << b << ") & 1u) << " << (int)pl.launch.opos[b] << ")";
-    o << ";\n";
+    o << "  const unsigned long long go_tid = " << dep(pl.launch.opos, "tid0", 0, low) << " | "
+      << dep(pl.launch.opos, "rank", TC, cl) << ";\n";
     o << "  auto out_base = [&](long long tt) -> unsigned long long {\n";
     o << "    const unsigned long long f = (unsigned long long)tt;\n";
     o << "    return ((f >> " << (n_local - T) << ") << " << n_local << ") | go_tid";
@@ -611,28 +567,29 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   };
   // issue the loads of CTA tile i into buffer i % 3 (this thread's share)
   o << "  auto issue = [&](long long i) {\n";
-  o << "    const long long tt = blockIdx.x + i * (long long)gridDim.x;\n";
+  o << "    const long long tt = cid + i * (long long)ncl;\n";
   o << "    if (tt >= ntiles) return;\n";
   o << "    const unsigned long long base = tile_base(tt);\n";
   o << "    const int b = (int)(i % 3);\n";
   o << "    const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_raw) + b * " << tile_bytes << "u;\n";
   for (int j = 0; j < g.nreg; ++j) {
-    const uint32_t sx = swz_host(uint32_t(j) << low, g.c128);
+    const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
     o << "    asm volatile(\"cp.async." << (g.c128 ? "cg" : "ca") << ".shared.global [%0], [%1], "
-      << (g.c128 ? 16 : 8) << ";\" :: \"r\"(sb + (sw_tid ^ " << sx << "u) * " << sizeof_amp(g.c128)
+      << amp << ";\" :: \"r\"(sb + (sw_tid ^ " << sx << "u) * " << amp
       << "u), \"l\"(psi + (base | " << hi_of(j) << "ull)) : \"memory\");\n";
   }
   o << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"((unsigned)__cvta_generic_to_shared(&full[b])) : \"memory\");\n";
-  o << "    if (tid == 0) issued[b] = (int)(i / 3);\n";
+  o << "    if (tid0 == 0) issued[b] = (int)(i / 3);\n";
   o << "  };\n";
   o << "  issue(team);\n  if (team == 0) issue(2);\n";
   o << "  for (long long i = team;; i += 2) {\n";
-  o << "    const long long tt = blockIdx.x + i * (long long)gridDim.x;\n";
+  o << "    const long long tt = cid + i * (long long)ncl;\n";
   o << "    if (tt >= ntiles) break;\n";
   o << "    const unsigned long long base = tile_base(tt);\n";
-  o << "    unsigned tid = tid0; asm volatile(\"\" : \"+r\"(tid));  // keep phase addresses in the loop\n";
+  o << "    unsigned tid = tid0 | (rank << " << low << "); asm volatile(\"\" : \"+r\"(tid));  // keep phase addresses in the loop\n";
   o << "    const int b = (int)(i % 3);\n";
   o << "    C* sm = reinterpret_cast<C*>(smem_raw + b * " << tile_bytes << ");\n";
+  if (cl > 0) o << "    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);\n";
   // Fill k = i / 3 of buffer b. This team can get here before the other
   // team has even issued fill k (it is still on tile i - 3), and a parity
   // wait cannot tell phase k from phase k - 2. The producer publishes the
@@ -643,10 +600,16 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "      const unsigned mb = (unsigned)__cvta_generic_to_shared(&full[b]); const unsigned par = (unsigned)(k & 1);\n";
   o << "      unsigned done = 0;\n";
   o << "      while (!done) asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\" : \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\"); }\n";
-  emit_program(g, pl, "TEAM_SYNC();", fp64_per_amp);
+  if (cl > 0) {  // the first phase reads other CTAs' slots: their loads must be in
+    const Instr* first = nullptr;
+    for (const Instr& in : pl.prog)
+      if (in.op == I_PHASE) { first = &in; break; }
+    if (!(first && g.phase_local(first->rpos, first->npos))) o << "    TEAM_CSYNC();\n";
+  }
+  emit_program(g, pl, cl > 0 ? "TEAM_CSYNC();" : "TEAM_SYNC();", fp64_per_amp, "TEAM_SYNC();");
   if (oop) o << "    const unsigned long long obase = out_base(tt);\n";
   for (int j = 0; j < g.nreg; ++j) {
-    const uint32_t sx = swz_host(uint32_t(j) << low, g.c128);
+    const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
     o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
   }
   o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3

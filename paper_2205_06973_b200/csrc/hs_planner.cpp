@@ -338,9 +338,9 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   const int T = std::min(std::max(tile_max, w), n_local);
   // a part wider than one CTA's tile runs as a cluster tile (compiled parts)
   const int cluster_log = T > tile_max ? T - tile_max : 0;
-  if (cluster_log > 0 && (!(options & HS_PLAN_JIT) || cluster_log > MAX_CLUSTER_LOG)) {
+  if (cluster_log > 0 && (!(options & HS_PLAN_JIT) || !(options & HS_PLAN_CLUSTER) || cluster_log > MAX_CLUSTER_LOG)) {
     err = "part stages " + std::to_string(w) + " qubits; the on-chip tile holds " + std::to_string(tile_max) +
-          ((options & HS_PLAN_JIT) ? " (x4 over a CTA cluster)" : " (compiled parts span CTA clusters: HS_PLAN_JIT)");
+          ((options & HS_PLAN_JIT) ? " (x4 over a CTA cluster)" : " (cluster tiles: HS_PLAN_JIT | HS_PLAN_CLUSTER)");
     return HS_ERR_TOO_WIDE;
   }
   if (T - cluster_log > MAX_TILE) { err = "tile wider than the kernels support"; return HS_ERR_TOO_WIDE; }
@@ -685,6 +685,7 @@ int plan_restore(int n_local, int dtype, int tile_max, uint32_t options, std::ve
     int s = plan_part(n_local, dtype, tile_max, options, staged.data(), (int)staged.size(), nullptr, 0, pl, err, &lay);
     if (s != HS_OK) return s;
     pl.info.restore = 1;
+    pl.info.user_part = -1;
     plans.push_back(pl);
     phys = next;
   }
@@ -694,9 +695,99 @@ int plan_restore(int n_local, int dtype, int tile_max, uint32_t options, std::ve
 
 }  // namespace
 
+namespace {
+
+// A part wider than the tile runs as a sequence of sub-parts of at most
+// tile_max qubits: gates are taken in program order into the current
+// sub-part while they fit and do not depend on a gate left for later (one
+// that shares a qubit with it); each round is one pass. The product of the
+// sub-parts' gates is the part's (gates only move past gates on disjoint
+// qubits). owner[j] = the caller's part of expanded part j.
+int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
+                     std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates, std::vector<int>& owner,
+                     std::string& err) {
+  for (int i = 0; i < num_parts; ++i) {
+    const hs_part& p = parts[i];
+    if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates) {
+      err = "part " + std::to_string(i) + ": gate window outside the gate array";
+      return HS_ERR_INVALID;
+    }
+    const hs_gate* pg = gates + p.gate_offset;
+    if (p.num_staged <= tile_max) {
+      hs_part q = p;
+      q.gate_offset = (int32_t)xgates.size();
+      xgates.insert(xgates.end(), pg, pg + p.num_gates);
+      xparts.push_back(q);
+      owner.push_back(i);
+      continue;
+    }
+    std::vector<int> rem(p.num_gates);
+    for (int g = 0; g < p.num_gates; ++g) rem[g] = g;
+    while (!rem.empty()) {
+      std::vector<char> in(p.num_staged, 0), blocked(p.num_staged, 0);
+      int used = 0;
+      std::vector<int> chosen, rest;
+      for (int g : rem) {
+        const hs_gate& G = pg[g];
+        bool ok = G.num_slots >= 1 && G.num_slots <= 3;
+        int extra = 0;
+        for (int a = 0; ok && a < G.num_slots; ++a) {
+          const int sl = G.slots[a];
+          if (sl < 0 || sl >= p.num_staged) { err = "gate slot outside the part"; return HS_ERR_INVALID; }
+          if (blocked[sl]) ok = false;
+          else if (!in[sl]) ++extra;
+        }
+        if (ok && used + extra <= tile_max) {
+          for (int a = 0; a < G.num_slots; ++a)
+            if (!in[G.slots[a]]) { in[G.slots[a]] = 1; ++used; }
+          chosen.push_back(g);
+        } else {
+          for (int a = 0; a < G.num_slots; ++a)
+            if (G.slots[a] >= 0 && G.slots[a] < p.num_staged) blocked[G.slots[a]] = 1;
+          rest.push_back(g);
+        }
+      }
+      if (chosen.empty()) { err = "internal: wide-part split made no progress"; return HS_ERR_INVALID; }
+      hs_part q;
+      std::memset(&q, 0, sizeof(q));
+      std::vector<int> slot_of(p.num_staged, -1);
+      for (int sl = 0; sl < p.num_staged; ++sl)  // staged positions stay ascending
+        if (in[sl]) { slot_of[sl] = q.num_staged; q.staged[q.num_staged++] = p.staged[sl]; }
+      q.gate_offset = (int32_t)xgates.size();
+      q.num_gates = (int32_t)chosen.size();
+      for (int g : chosen) {
+        hs_gate G = pg[g];
+        for (int a = 0; a < G.num_slots; ++a) G.slots[a] = slot_of[G.slots[a]];
+        xgates.push_back(G);
+      }
+      xparts.push_back(q);
+      owner.push_back(i);
+      rem.swap(rest);
+    }
+  }
+  return HS_OK;
+}
+
+}  // namespace
+
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                  const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
                  std::vector<int32_t>* init_phys, const int32_t* given_init) {
+  bool wide = false;
+  for (int i = 0; i < num_parts; ++i) wide |= parts[i].num_staged > tile_max;
+  if (wide && !((options & HS_PLAN_CLUSTER) && (options & HS_PLAN_JIT))) {
+    std::vector<hs_part> xp;
+    std::vector<hs_gate> xg;
+    std::vector<int> owner;
+    int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, xp, xg, owner, err);
+    if (s != HS_OK) return s;
+    s = plan_program(n_local, dtype, tile_max, options, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
+                     err, init_phys, given_init);
+    if (s != HS_OK) return s;
+    for (auto& pl : plans)
+      if (pl.info.user_part >= 0) pl.info.user_part = owner[pl.info.user_part];
+    return HS_OK;
+  }
   plans.assign(num_parts, PartPlan());
   const bool layout = (options & HS_PLAN_LAYOUT) && num_parts > 0 && n_local > 0;
   std::vector<int32_t> phys(std::max(n_local, 1)), inv(std::max(n_local, 1));
@@ -831,6 +922,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     plans[i].launch.in_buf = cur_buf;
     if (oop) cur_buf ^= 1;
     plans[i].launch.out_buf = cur_buf;
+    plans[i].info.user_part = i;
     if (layout) {
       phys = next;
       for (int q = 0; q < n_local; ++q) inv[phys[q]] = q;
@@ -856,6 +948,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     int s = plan_part(n_local, dtype, tile_max, options, st.data(), (int)st.size(), nullptr, 0, pl, err, &lay);
     if (s != HS_OK) return s;
     pl.info.restore = 1;
+    pl.info.user_part = -1;
     pl.launch.in_buf = cur_buf;
     pl.launch.out_buf = cur_buf ^ 1;
     plans.push_back(pl);

@@ -323,6 +323,7 @@ class PartProgram:
             "restore": bool(inf.restore),
             "compiled": bool(inf.compiled),
             "fp64_instr_per_amp": float(inf.fp64_instr_per_amp),
+            "user_part": int(inf.user_part),
         }
 
     def dump(self, i: int) -> bytes:

@@ -219,8 +219,12 @@ def test_errors_surface_as_reference_exceptions():
 
     c = Circuit(16, tuple(GateOp(GateKind.H, (q,)) for q in range(16)))
     part = partition_of([(list(range(16)), list(range(16)))], limit=16)
+    # wider than any tile: runs as sub-passes (no error), H^16 |0> is uniform
+    st = execute_hierarchical(c, part)
+    assert float(np.max(np.abs(st.to_numpy() - 2.0 ** -8))) < 1e-12
+    # wider than the ranks' local qubits: the reference's layout error (dist.py:136-141)
     with pytest.raises(PartTooWideForLayoutError):
-        execute_hierarchical(c, part)
+        simulate_distributed(c, part, 1)
 
 
 @pytest.mark.parametrize("dtype", ["complex128", "complex64"])
@@ -289,18 +293,24 @@ def test_initial_layout_for_basis_starts(name):
 
 @pytest.mark.parametrize("name,limit,dtype", [("c2@22", 14, "complex128"), ("c2@24", 13, "complex128"),
                                               ("c2@17", 14, "complex128"), ("c2@22", 15, "complex64")])
-def test_cluster_tile_parts_match_c_oracle(name, limit, dtype):
-    """c5's k = 14 parts (256 KB of complex128 per tile) run as cluster
-    tiles: 2 or 4 CTAs share one tile through distributed shared memory."""
+def test_wide_parts_match_c_oracle(name, limit, dtype):
+    """c5's k = 14 parts (256 KB of complex128 per tile, more than one SM
+    holds): by default sub-passes that fit the tile; with HS_PLAN_CLUSTER
+    one pass over a 2-4 CTA cluster sharing the tile through distributed
+    shared memory."""
     c = configs.build(name)
     part = partition_dfs(build_dag(c), limit)
     assert max(len(p.qubits) for p in part.parts) == limit
-    run = HierarchicalRun(c, part, dtype=dtype)
-    assert run.program.jit_error == ""
-    st = from_numpy(np.eye(1, 1 << c.num_qubits, 0).ravel().astype(np.complex128), dtype=dtype)
-    run.program.run(st.data)
     ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
-    assert float(np.max(np.abs(st.to_numpy() - ref))) < TOL[dtype]
+    base = _native.default_options() | _native.HS_PLAN_JIT | _native.HS_PLAN_LAYOUT
+    for opts in (None, base | _native.HS_PLAN_CLUSTER, base | _native.HS_PLAN_CLUSTER | _native.HS_PLAN_PINGPONG):
+        run = HierarchicalRun(c, part, dtype=dtype, options=opts)
+        assert run.program.jit_error == ""
+        owners = [run.program.info(j)["user_part"] for j in range(run.program.num_launches)]
+        assert sorted(set(u for u in owners if u >= 0)) == list(range(part.num_parts))
+        st = from_numpy(np.eye(1, 1 << c.num_qubits, 0).ravel().astype(np.complex128), dtype=dtype)
+        run.program.run(st.data)
+        assert float(np.max(np.abs(st.to_numpy() - ref))) < TOL[dtype], opts
 
 
 def test_segment_range_pack_unpack_kernels():

@@ -285,22 +285,29 @@ def test_cluster_tile_parts(tmp_path, name, limit, dtype):
     exes = [remap_part(c, p) for p in part.parts]
     tile = 12 if dtype == 0 else 13
     want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
-    for opts in (0x15, 0x15 | 8 | 0x40):
+    for opts in (0x95, 0x95 | 8 | 0x40):  # cluster tiles (HS_PLAN_CLUSTER)
         launches = emu.plan_program(_native, c.num_qubits, dtype, tile, exes, options=opts)
         assert max(int(l["cluster_log"]) for l, _ in launches) == limit - tile
         psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
         psi[0, 0] = 1
         emu.run_program(psi, c.num_qubits, launches)
         assert np.max(np.abs(psi[0] - want)) < 1e-12
-    with pytest.raises(PartTooWideForLayoutError):
-        emu.plan_program(_native, c.num_qubits, dtype, tile, exes, options=5)
+    for opts in (0x5, 0x15, 0x15 | 8 | 0x40):  # default: sub-passes that fit the tile
+        launches = emu.plan_program(_native, c.num_qubits, dtype, tile, exes, options=opts)
+        assert max(int(l["cluster_log"]) for l, _ in launches) == 0
+        assert max(int(l["T"]) for l, _ in launches) <= tile
+        assert sum(1 for l, _ in launches) > len(exes)
+        psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
+        psi[0, 0] = 1
+        emu.run_program(psi, c.num_qubits, launches)
+        assert np.max(np.abs(psi[0] - want)) < 1e-12
     wide = next(p for p in part.parts if len(p.qubits) == limit)
     src = tmp_path / "cl.cu"
-    src.write_text(_jit_source(c, wide, dtype, options=0x15, tile_bits=tile))
+    src.write_text(_jit_source(c, wide, dtype, options=0x95, tile_bits=tile))
     assert "barrier.cluster" in src.read_text()
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     res = subprocess.run([nvcc, "-arch=sm_100a", "-cubin", "-o", str(tmp_path / "cl.cubin"), str(src), "-Xptxas", "-v"],
                          capture_output=True, text=True)
     assert res.returncode == 0, res.stderr[-3000:]
     spill = int(re.search(r"(\d+) bytes spill stores", res.stderr).group(1))
-    assert spill <= 64, res.stderr  # a few words at most, outside the gate code
+    assert spill <= 160, res.stderr  # per-tile addresses, outside the gate code
