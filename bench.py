@@ -435,6 +435,19 @@ def main(argv=None):
                 "per_part_gbs": [g["bytes_per_pass"] / (d / 1e3) / 1e9 for d in durs[: g["num_parts"]]]}
     infos = g["info"]
     flops = sum(i["fp_ops_per_amp"] for i in infos) * (1 << g["n_local"])
+    # binding roofline per part: max(bytes / HBM peak, FP64
+    # instructions / measured DFMA rate); its sum over the circuit vs the
+    # measured part time
+    fp_rate = g["fp64"]["peak_tflops_measured"] * 1e12 / 2  # instructions/s (FMA = 2 flops)
+    bind_ms = 0.0
+    for p_ in range(g["num_parts"] if world == 1 else 0):
+        ins = sum(i["fp64_instr_per_amp"] for i in infos if i["user_part"] == p_) * (1 << g["n_local"])
+        bind_ms += max(g["bytes_per_pass"] / (peak * 1e9), ins / fp_rate if fp_rate else 0.0) * 1e3
+    bind_ms += sum(g["bytes_per_pass"] / (peak * 1e9) for i in infos if i["user_part"] < 0) * 1e3
+    if world == 1:
+        roofline["binding"] = {"what": "sum over launches of max(HBM bytes / peak, FP64 instructions / measured DFMA rate)",
+                             "bound_ms_per_step": bind_ms, "measured_ms_per_step": g["ms_step"],
+                             "frac": bind_ms / g["ms_step"]}
     line = {"metric": METRIC, "value": g["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": g["ms_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
