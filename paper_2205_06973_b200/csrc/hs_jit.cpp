@@ -90,9 +90,15 @@ struct Gen {
       if (!reg_local(npos, u[i])) return false;
     return true;
   }
+  // st ^ u with the swizzled low bits XORed and the rest added: st is zero
+  // at the register locations and the swizzle only touches the low 3 (c128)
+  // / 4 (c64) bits, so st ^ u == (st ^ (u & lo)) + (u & ~lo) and the added
+  // part becomes the LDS/STS immediate offset (<= 2^lo distinct bases)
   std::string local_slot(uint32_t u) const {
-    return cluster ? "(st ^ " + std::to_string(u) + "u) & " + std::to_string((1u << TC) - 1) + "u"
-                   : "st ^ " + std::to_string(u) + "u";
+    const uint32_t lo = c128 ? 7u : 15u;
+    const std::string b = "(st ^ " + std::to_string(u & lo) + "u)";
+    const std::string hi = std::to_string(u & ~lo) + "u";
+    return cluster ? "(" + b + " & " + std::to_string((1u << TC) - 1) + "u) + " + hi : b + " + " + hi;
   }
   void load_regs(const uint8_t* rpos, const uint8_t* npos) {
     auto u = slot_xor(rpos);
