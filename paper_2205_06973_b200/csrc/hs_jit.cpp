@@ -74,6 +74,7 @@ struct Gen {
   // CTA's own when the thread bits that carry the CTA rank (lowc..) map onto
   // the top tile locations TC.. and the register's own bits stay below TC;
   // own slots take plain shared-memory accesses, the rest go through DSMEM.
+  bool carry = false;  // leave the part's scalar pending (Sr, Si) for a later launch
   bool cluster = false;
   int TC = 0, cl = 0, lowc = 0;
   bool rank_aligned(const uint8_t* npos) const {
@@ -159,7 +160,8 @@ struct Gen {
   bool scale_ok(double sr, double si) const {
     const double nr = Sr * sr - Si * si, ni = Sr * si + Si * sr;
     const double mag = std::hypot(nr, ni);
-    return mag > 0 && std::fabs(std::log2(mag)) < 300;  // amplitudes stay far from overflow
+    // amplitudes stay far from overflow / underflow (complex64: 2^+-127)
+    return mag > 0 && std::fabs(std::log2(mag)) < (c128 ? 300 : 48);
   }
   void push_scale(double sr, double si) {
     const double nr = Sr * sr - Si * si, ni = Sr * si + Si * sr;
@@ -413,7 +415,10 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
     g.wgt = 1.0;
     o << "    }\n";
   }
-  g.flush(true);  // pending diagonal run + the part's scalar
+  // pending diagonal run + the part's scalar: the scalar is global, so it is
+  // carried to the program's last launch unless it grows large
+  const bool apply = !g.carry || std::fabs(std::log2(std::hypot(g.Sr, g.Si))) > (g.c128 ? 200 : 24);
+  g.flush(apply);
   if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
   o << "    // fp64_instr_per_amp " << g.ops / g.nreg << "\n";
   // the final write goes to the store order; the read-out after it is local
@@ -426,8 +431,14 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
     << "\n";
 }
 
-std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_per_amp = nullptr) {
+std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_per_amp = nullptr,
+                       double* carry_scale = nullptr, bool last = true) {
   Gen g;
+  if (carry_scale) {  // in: scalar owed by earlier launches; out: what this one leaves pending
+    g.carry = !last;
+    g.Sr = carry_scale[0];
+    g.Si = carry_scale[1];
+  }
   g.c128 = dtype == HS_C128;
   g.RB = pl.launch.RB;
   g.T = pl.launch.T;
@@ -621,6 +632,10 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
   o << "    issue(i + 3);\n";
   o << "  }\n}\n";
+  if (carry_scale) {
+    carry_scale[0] = g.Sr;
+    carry_scale[1] = g.Si;
+  }
   return o.str();
 }
 
@@ -673,7 +688,10 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
   const size_t n = plans.size();
   std::vector<std::string> srcs(n);
   std::vector<double> fp64(n, 0.0);
-  for (size_t i = 0; i < n; ++i) srcs[i] = jit_source(plans[i], dtype, n_local, &fp64[i]);
+  // the structured-gate scalars multiply into one global factor, applied by
+  // the last launch (runs of a program's launches must be complete, in order)
+  double scale[2] = {1.0, 0.0};
+  for (size_t i = 0; i < n; ++i) srcs[i] = jit_source(plans[i], dtype, n_local, &fp64[i], scale, i + 1 == n);
   std::vector<int> status(n, HS_OK);
   std::vector<std::string> errs(n);
   unsigned hw = std::thread::hardware_concurrency();
