@@ -659,13 +659,25 @@ int plan_restore(int n_local, int dtype, int tile_max, uint32_t options, std::ve
       cycles.push_back(c);
     }
     if (cycles.empty()) return HS_OK;
-    // one launch: whole cycles first-fit, or a T-long chunk of a long cycle
+    // one launch: whole cycles first-fit, or a chunk of a long cycle. The
+    // tile keeps room for the low positions 0..hot-1 (ride-along when not
+    // displaced) so the permutation pass reads and writes 128 B runs.
+    const int hot = std::min(dtype == HS_C128 ? 3 : 4, T - 1);
+    auto tile_need = [&](const std::vector<int>& st) {
+      int need = (int)st.size();
+      for (int h = 0; h < hot; ++h)
+        if (std::find(st.begin(), st.end(), h) == st.end()) ++need;
+      return need;
+    };
     std::vector<int> set, dest;
     for (auto& c : cycles) {
-      if ((int)c.size() <= T - (int)set.size()) {
+      std::vector<int> trial(set);
+      trial.insert(trial.end(), c.begin(), c.end());
+      if (tile_need(trial) <= T) {
         for (size_t k = 0; k < c.size(); ++k) { set.push_back(c[k]); dest.push_back(c[(k + 1) % c.size()]); }
       } else if (set.empty()) {
-        for (int k = 0; k < T; ++k) { set.push_back(c[k]); dest.push_back(k + 1 < T ? c[k + 1] : c[0]); }
+        const int len = std::max(2, T - hot);
+        for (int k = 0; k < len; ++k) { set.push_back(c[k]); dest.push_back(k + 1 < len ? c[k + 1] : c[0]); }
         break;
       }
     }
