@@ -402,8 +402,50 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   std::vector<int> R;
   double flops = 0, fp64 = 0;
   int phases = 0;
+  // How many non-diagonal gates a phase would take with register locations
+  // restricted to `allow` (a mask; ~0u = first come, up to RB of them).
+  auto phase_yield = [&](uint32_t allow) {
+    std::vector<char> dn(done);
+    std::vector<int> lo(loc_of);
+    int taken = 0, nR = 0;
+    uint32_t Rm = 0;
+    for (;;) {
+      bool progress = false;
+      uint32_t blk_nd = 0, blk_d = 0;
+      for (int g = 0; g < num_gates; ++g) {
+        if (dn[g]) continue;
+        const Gate& G = gs[g];
+        if ((G.nd & (blk_nd | blk_d)) || (G.d & blk_nd)) { blk_nd |= G.nd; blk_d |= G.d; continue; }
+        bool ok = G.cls == C_DIAG || G.cls == C_SWAP;
+        if (!ok) {
+          const int L = lo[G.tgt];
+          if (Rm >> L & 1) ok = true;
+          else if (nR < RB && (allow >> L & 1)) { Rm |= 1u << L; ++nR; ok = true; }
+        }
+        if (!ok) { blk_nd |= G.nd; blk_d |= G.d; continue; }
+        if (G.cls == C_SWAP) std::swap(lo[G.tgt], lo[G.other]);
+        else if (G.cls != C_DIAG) ++taken;
+        dn[g] = 1;
+        progress = true;
+      }
+      if (!progress) break;
+    }
+    return taken;
+  };
   while (remaining > 0) {
     R.clear();
+    // compiled parts pay a shared-memory exchange per phase: pick the
+    // register locations that let the most gates into this phase (all
+    // RB-subsets of the tile), not just the first targets met
+    uint32_t allow = ~0u;
+    if ((options & HS_PLAN_JIT) && T <= 16) {
+      int best = phase_yield(~0u);
+      for (uint32_t m = 0; m < (1u << T); ++m) {
+        if (__builtin_popcount(m) != RB) continue;
+        const int y = phase_yield(m);
+        if (y > best) { best = y; allow = m; }
+      }
+    }
     std::vector<Rec> recs;
     for (;;) {
       bool progress = false;
@@ -417,7 +459,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         else {
           int L = loc_of[G.tgt];
           if (std::find(R.begin(), R.end(), L) != R.end()) ok = true;
-          else if ((int)R.size() < RB) { R.push_back(L); ok = true; }
+          else if ((int)R.size() < RB && (allow >> L & 1)) { R.push_back(L); ok = true; }
         }
         if (!ok) { blk_nd |= G.nd; blk_d |= G.d; continue; }
         if (G.cls == C_SWAP) {
