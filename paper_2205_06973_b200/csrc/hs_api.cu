@@ -166,7 +166,10 @@ static int program_create(hs_engine* eng, int n_local, int dtype, const hs_part*
   prog->dtype = dtype;
   {
     std::string err;
-    int s = plan_program(n_local, dtype, tile_for(eng, dtype), eng->options, parts, num_parts, gates, num_gates,
+    // compiled parts: 256-thread teams (2^(T - 4)) keep 128 registers per
+    // thread, so complex64 tiles are 12 bits there too
+    const int tile = (eng->options & HS_PLAN_JIT) ? std::min(tile_for(eng, dtype), 12) : tile_for(eng, dtype);
+    int s = plan_program(n_local, dtype, tile, eng->options, parts, num_parts, gates, num_gates,
                          prog->plans, err, &prog->init_phys, init_phys);
     if (s != HS_OK) return fail(s, err);
   }

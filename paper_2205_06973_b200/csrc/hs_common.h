@@ -60,7 +60,10 @@ struct PartLaunch {
   int32_t in_buf, out_buf;
   int32_t cluster_log;  // tile spread over a cluster of 2^cluster_log CTAs (compiled parts only)
   uint8_t opos[16];
-  uint8_t fpos[56];
+  uint8_t fpos[52];
+  // compiled parts: the last phase's lanes 0..2 (0..3 for c64) hold store
+  // slots 0..2, so registers go straight to HBM in full 128 B lines
+  int32_t direct_store;
 };
 static_assert(sizeof(PartLaunch) == 144, "PartLaunch layout");
 

@@ -377,8 +377,11 @@ struct Gen {
 // memory exchanges separated by `sync`), gates, the part's scalar, and the
 // final write of the registers into the tile's store order (ending in `sync`)
 void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per_amp,
-                  const char* local_sync = "__syncthreads();") {
+                  const char* local_sync = "__syncthreads();", const char* after_last_load = nullptr) {
   std::ostringstream& o = g.o;
+  const Instr* last_phase = nullptr;
+  for (const Instr& in : pl.prog)
+    if (in.op == I_PHASE) last_phase = &in;
   // cluster tiles: an exchange whose writes and reads all stay in this CTA's
   // slots (for every CTA alike: the mapping is the same) needs only a CTA
   // barrier; otherwise the cluster barrier
@@ -402,6 +405,7 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
       g.emit_tdep("t", in.npos);
       o << "    st = swz(t);\n";
       g.load_regs(in.rpos, in.npos);
+      if (&in == last_phase && after_last_load) o << "    " << after_last_load << "\n";
       cur = &in;
       continue;
     }
@@ -421,6 +425,7 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   g.flush(apply);
   if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
   o << "    // fp64_instr_per_amp " << g.ops / g.nreg << "\n";
+  if (pl.launch.direct_store) return;  // the caller stores the registers to HBM
   // the final write goes to the store order; the read-out after it is local
   const std::string fs = xsync(cur->rpos, cur->npos, pl.launch.fin_rpos, pl.launch.fin_npos);
   if (pl.launch.fin_sync) o << "    " << fs << "\n";
@@ -623,15 +628,37 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       if (in.op == I_PHASE) { first = &in; break; }
     if (!(first && g.phase_local(first->rpos, first->npos))) o << "    TEAM_CSYNC();\n";
   }
-  emit_program(g, pl, cl > 0 ? "TEAM_CSYNC();" : "TEAM_SYNC();", fp64_per_amp, "TEAM_SYNC();");
+  const bool direct = pl.launch.direct_store && cl == 0;
+  // direct stores: the buffer is free once the last phase has loaded its
+  // registers, so its refill (tile i + 3) overlaps the last phase's gates
+  emit_program(g, pl, cl > 0 ? "TEAM_CSYNC();" : "TEAM_SYNC();", fp64_per_amp, "TEAM_SYNC();",
+               direct ? "TEAM_SYNC(); issue(i + 3);" : nullptr);
   if (oop) o << "    const unsigned long long obase = out_base(tt);\n";
-  for (int j = 0; j < g.nreg; ++j) {
-    const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
-    o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
+  if (direct) {
+    // store slot bit r sits at output position pos[r]; lanes 0..2 carry slot
+    // bits 0..2, so each warp instruction writes whole 128 B lines
+    const uint8_t* pos = oop ? pl.launch.opos : pl.launch.tpos;
+    o << "    const unsigned long long dbase = " << (oop ? "(obase ^ go_tid)" : "(base ^ ga_tid)") << " | 0ull";
+    for (int m = 0; m < T - RB; ++m)
+      o << " | ((unsigned long long)((tid >> " << m << ") & 1u) << " << (int)pos[pl.launch.fin_npos[m]] << ")";
+    o << ";\n";
+    for (int i = 0; i < g.nreg; ++i) {
+      uint64_t off = 0;
+      for (int k = 0; k < RB; ++k)
+        if (i >> k & 1) off |= 1ull << pos[pl.launch.fin_rpos[k]];
+      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; " << (oop ? "psi_out" : "psi") << "[dbase | "
+        << off << "ull] = v; }\n";
+    }
+    o << "  }\n}\n";
+  } else {
+    for (int j = 0; j < g.nreg; ++j) {
+      const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
+      o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
+    }
+    o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
+    o << "    issue(i + 3);\n";
+    o << "  }\n}\n";
   }
-  o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
-  o << "    issue(i + 3);\n";
-  o << "  }\n}\n";
   if (carry_scale) {
     carry_scale[0] = g.Sr;
     carry_scale[1] = g.Si;

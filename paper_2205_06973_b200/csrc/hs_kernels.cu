@@ -422,7 +422,7 @@ cudaError_t launch_part(int dtype, const PartLaunch& L, const Instr* dprog, void
   for (int b = 0; b < 16; ++b) (b < 8 ? p.opos0 : p.opos1) |= uint64_t(L.opos[b]) << (8 * (b & 7));
   for (int w = 0; w < 7; ++w) {
     p.fpos[w] = 0;
-    for (int b = 0; b < 8; ++b) p.fpos[w] |= uint64_t(L.fpos[8 * w + b]) << (8 * b);
+    for (int b = 0; b < 8 && 8 * w + b < 52; ++b) p.fpos[w] |= uint64_t(L.fpos[8 * w + b]) << (8 * b);
   }
   p.prog = dprog + L.prog_offset;
   p.nprog = L.nprog;

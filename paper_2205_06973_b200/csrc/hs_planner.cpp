@@ -637,10 +637,40 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   }
   // final store: register k holds location R[k] of the last phase, which is
   // tile bit bit_at[R[k]]; it is written to tile position rho[bit_at[R[k]]]
-  const Instr* last = nullptr;
-  for (const Instr& in : P.prog) if (in.op == I_PHASE) last = &in;
+  Instr* last = nullptr;
+  for (Instr& in : P.prog) if (in.op == I_PHASE) last = &in;
+  // Compiled parts store their registers straight to HBM when the last
+  // phase's lanes 0..hot-1 can hold store slots 0..hot-1 (a warp then writes
+  // whole 128 B lines): the lane order of a phase is free (instructions name
+  // tile locations, not thread bits), so move those locations to the front
+  // when none of them is a register bit of the last phase.
+  bool direct = false;
+  {
+    const int hot = dtype == HS_C128 ? 3 : 4;
+    if ((options & HS_PLAN_JIT) && cluster_log == 0 && T - RB >= hot) {
+      std::vector<int> want(hot, -1);
+      for (int loc = 0; loc < T; ++loc)
+        if (rho[bit_at[loc]] < hot) want[rho[bit_at[loc]]] = loc;
+      bool ok = true;
+      uint32_t residues = 0;  // the lanes' swizzle residues must differ (conflict-free loads)
+      for (int r = 0; r < hot; ++r) {
+        ok &= want[r] >= 0;
+        for (int k = 0; ok && k < RB; ++k) ok &= last->rpos[k] != want[r];
+        if (ok) residues |= 1u << (want[r] % hot);
+      }
+      ok &= residues == (1u << hot) - 1;
+      if (ok) {
+        std::vector<int> order(want.begin(), want.end());
+        for (int m = 0; m < T - RB; ++m)
+          if (std::find(want.begin(), want.end(), (int)last->npos[m]) == want.end()) order.push_back(last->npos[m]);
+        for (int m = 0; m < T - RB; ++m) last->npos[m] = (uint8_t)order[m];
+        direct = true;
+      }
+    }
+  }
   PartLaunch& L = P.launch;
   std::memset(&L, 0, sizeof(L));
+  L.direct_store = direct ? 1 : 0;
   L.nprog = (int32_t)P.prog.size();
   L.T = T;
   L.RB = RB;

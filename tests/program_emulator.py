@@ -21,7 +21,7 @@ K_NONE = 0xFF
 LAUNCH = np.dtype([("prog_offset", "<i8"), ("nprog", "<i4"), ("T", "<i4"), ("RB", "<i4"), ("fin_sync", "<i4"),
                    ("tpos", "u1", 16), ("fin_rpos", "u1", 4), ("fin_npos", "u1", 12),
                    ("oop", "<i4"), ("in_buf", "<i4"), ("out_buf", "<i4"), ("cluster_log", "<i4"),
-                   ("opos", "u1", 16), ("fpos", "u1", 56)])
+                   ("opos", "u1", 16), ("fpos", "u1", 52), ("direct_store", "<i4")])
 INSTR = np.dtype([("op", "<u2"), ("k", "u1"), ("flags", "u1"), ("creg", "<u4"), ("ctid", "<u4"), ("qtid", "<u4"),
                   ("rpos", "u1", 4), ("npos", "u1", 12), ("m", "<f8", 8)])
 assert LAUNCH.itemsize == 144 and INSTR.itemsize == 96

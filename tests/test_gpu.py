@@ -292,7 +292,7 @@ def test_initial_layout_for_basis_starts(name):
 
 
 @pytest.mark.parametrize("name,limit,dtype", [("c2@22", 14, "complex128"), ("c2@24", 13, "complex128"),
-                                              ("c2@17", 14, "complex128"), ("c2@22", 15, "complex64")])
+                                              ("c2@17", 14, "complex128"), ("c2@22", 14, "complex64")])
 def test_wide_parts_match_c_oracle(name, limit, dtype):
     """c5's k = 14 parts (256 KB of complex128 per tile, more than one SM
     holds): by default sub-passes that fit the tile; with HS_PLAN_CLUSTER

@@ -270,7 +270,7 @@ def test_structured_2x2_factorisation():
         assert s0 == 1 and cost0 <= 16 and np.max(np.abs(mm0 - m)) < 1e-15
 
 
-@pytest.mark.parametrize("name,limit,dtype", [("c2@16", 14, 0), ("c2@15", 13, 0), ("c2@17", 15, 1)])
+@pytest.mark.parametrize("name,limit,dtype", [("c2@16", 14, 0), ("c2@15", 13, 0), ("c2@17", 14, 1)])
 def test_cluster_tile_parts(tmp_path, name, limit, dtype):
     """Parts wider than one CTA's tile (c5's k = 14: 256 KB of complex128)
     are planned as cluster tiles for compiled kernels: the emulated program
@@ -283,7 +283,7 @@ def test_cluster_tile_parts(tmp_path, name, limit, dtype):
     part = partition_dfs(build_dag(c), limit)
     assert max(len(p.qubits) for p in part.parts) == limit
     exes = [remap_part(c, p) for p in part.parts]
-    tile = 12 if dtype == 0 else 13
+    tile = 12  # compiled programs use 12-bit tiles for both dtypes
     want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
     for opts in (0x95, 0x95 | 8 | 0x40):  # cluster tiles (HS_PLAN_CLUSTER)
         launches = emu.plan_program(_native, c.num_qubits, dtype, tile, exes, options=opts)
