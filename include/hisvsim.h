@@ -205,6 +205,13 @@ int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options,
 int hs_jit_source(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
                   const hs_gate* gates, int num_gates, char* buf, size_t buf_bytes, size_t* bytes);
 
+/* dagP merge phase (hisim partition.py:396-478, partition_dagp's greedy pair
+ * contraction) on the host: groups with qubit masks and group-level DAG
+ * edges in, the surviving group of every group out; identical merges to
+ * the reference. Host-only; circuits of at most 64 qubits. */
+int hs_dagp_merge(int num_groups, const uint64_t* qmask, int num_edges, const int32_t* edge_src,
+                  const int32_t* edge_dst, int limit, int32_t* merged_into);
+
 /* the structured form compiled kernels use for a 2x2 gate matrix m
  * (row-major complex, 8 doubles): m = s * m_out with m_out's entries
  * snapped to 0 / +-1 within a few ulps; returns the FP64 instructions per

@@ -33,7 +33,7 @@ EXPORTS = (
     "hs_program_bind_scratch",
     "hs_program_jit_error",
     "hs_program_dump",
-    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_jit_source", "hs_structure_2x2", "hs_part_apply",
+    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_jit_source", "hs_structure_2x2", "hs_dagp_merge", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
     "hs_pack_segments", "hs_unpack_segments", "hs_pack_segments_range", "hs_unpack_segments_range",
 )
@@ -114,6 +114,8 @@ def _declare(lib) -> None:
         "hs_jit_source": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int32), I, ctypes.POINTER(HsGate), I,
                               ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
         "hs_structure_2x2": (I, [ctypes.POINTER(D), I, ctypes.POINTER(D), ctypes.POINTER(D)]),
+        "hs_dagp_merge": (I, [I, ctypes.POINTER(ctypes.c_uint64), I, ctypes.POINTER(ctypes.c_int32),
+                              ctypes.POINTER(ctypes.c_int32), I, ctypes.POINTER(ctypes.c_int32)]),
         "hs_part_apply": (I, [P, P, I64, I, I, ctypes.POINTER(ctypes.c_int32), I,
                               ctypes.POINTER(HsGate), I, P]),
         "hs_state_init_basis": (I, [P, I64, I, I64, P]),

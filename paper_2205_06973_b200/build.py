@@ -10,7 +10,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 SRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libhisvsim.so"
-SOURCES = ("hs_api.cu", "hs_kernels.cu", "hs_planner.cpp", "hs_jit.cpp")
+SOURCES = ("hs_api.cu", "hs_kernels.cu", "hs_planner.cpp", "hs_jit.cpp", "hs_dagp.cpp")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -403,6 +403,52 @@ class _PartGraph:
 
 
 def _merge_groups(groups, qubits_of, succ, limit):
+    """The merge phase: the host C++ restatement (hs_dagp_merge) when the
+    circuit fits 64-qubit masks and the library loads, else Python."""
+    if _NATIVE_MERGE:
+        merged = _merge_groups_native(groups, qubits_of, succ, limit)
+        if merged is not None:
+            return merged
+    return _merge_groups_py(groups, qubits_of, succ, limit)
+
+
+#: use hs_dagp_merge (tests flip this to compare with the Python merge)
+_NATIVE_MERGE = True
+
+
+def _merge_groups_native(groups, qubits_of, succ, limit):
+    import ctypes
+
+    try:
+        from . import _native
+
+        lib = _native.load()
+    except Exception:  # no library on this host: the Python merge
+        return None
+    G = len(groups)
+    masks = (ctypes.c_uint64 * max(1, G))()
+    where = {}
+    for i, gs in enumerate(groups):
+        m = 0
+        for g in gs:
+            where[g] = i
+            for q in qubits_of[g]:
+                if q >= 64:
+                    return None
+                m |= 1 << q
+        masks[i] = m
+    edges = sorted({(where[g], where[s]) for g, ss in enumerate(succ) for s in ss if where[g] != where[s]})
+    src = (ctypes.c_int32 * max(1, len(edges)))(*[a for a, _ in edges])
+    dst = (ctypes.c_int32 * max(1, len(edges)))(*[b for _, b in edges])
+    into = (ctypes.c_int32 * max(1, G))()
+    _native.check(lib.hs_dagp_merge(G, masks, len(edges), src, dst, limit, into))
+    alive = {}
+    for i in range(G):
+        alive.setdefault(int(into[i]), set()).update(groups[i])
+    return [sorted(alive[p]) for p in sorted(alive)]
+
+
+def _merge_groups_py(groups, qubits_of, succ, limit):
     """Greedy pair contraction (reference: partition.py:396-478): pop pairs by
     (-shared qubits, -union size, u, v); a popped key is recomputed and
     requeued if stale; a valid pair merges when contraction stays acyclic,

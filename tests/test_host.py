@@ -218,3 +218,37 @@ def test_closed_form_scales_to_36_qubits():
     part = partition_dfs(build_dag(c), 14)
     _, layouts, switches = plan_layouts(c, part, 3)
     assert switches and all(s.bytes_remote + s.bytes_resident == 16 << 36 for *_, s in switches)
+
+
+@pytest.mark.parametrize("name,limit", [("c1", 10), ("c2@16", 8), ("c3@18", 6), ("c3", 12), ("c2", 12)])
+def test_native_dagp_merge_matches_python(name, limit):
+    """hs_dagp_merge (C++ restatement of the dagP merge phase) gives the same
+    partition as the Python merge, which the corpus goldens pin to the
+    reference."""
+    import paper_2205_06973_b200.partition as P
+    from paper_2205_06973_b200 import build_dag, configs, partition_dagp
+
+    d = build_dag(configs.build(name))
+    try:
+        P._NATIVE_MERGE = True
+        a = partition_dagp(d, limit)
+        P._NATIVE_MERGE = False
+        b = partition_dagp(d, limit)
+    finally:
+        P._NATIVE_MERGE = True
+    assert [(p.gate_indices, p.qubits) for p in a.parts] == [(p.gate_indices, p.qubits) for p in b.parts]
+
+
+def test_native_dagp_merge_on_tfim_chain():
+    import paper_2205_06973_b200.partition as P
+    from paper_2205_06973_b200 import build_dag, partition_dagp
+    from paper_2205_06973_b200.configs import ising_config
+
+    d = build_dag(ising_config(20, 6))
+    try:
+        P._NATIVE_MERGE = False
+        b = partition_dagp(d, 8)
+    finally:
+        P._NATIVE_MERGE = True
+    a = partition_dagp(d, 8)
+    assert [(p.gate_indices, p.qubits) for p in a.parts] == [(p.gate_indices, p.qubits) for p in b.parts]
