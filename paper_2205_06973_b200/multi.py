@@ -211,8 +211,9 @@ class ShardedRun:
             where[q] = pa[i]
         return tuple(where[q] for q in new.local)
 
-    def _exchange(self, packed, recv, out_segs, incoming, seg):
-        """Batched P2P: my segment k -> peer; slot j of recv <- source."""
+    def _post(self, packed, recv, out_segs, incoming, seg):
+        """Batched P2P: my segment k -> peer; slot j of recv <- source.
+        Returns the pending works (the self-segment is copied right away)."""
         import torch.distributed as dist
 
         reqs = []
@@ -226,9 +227,11 @@ class ShardedRun:
         for src, slot in incoming.items():
             if src != self.rank:
                 reqs.append(dist.P2POp(dist.irecv, _wire(recv[slot * seg:(slot + 1) * seg]), src, self.group))
-        if reqs:
-            for w in dist.batch_isend_irecv(reqs):
-                w.wait()
+        return dist.batch_isend_irecv(reqs) if reqs else []
+
+    def _exchange(self, packed, recv, out_segs, incoming, seg):
+        for w in self._post(packed, recv, out_segs, incoming, seg):
+            w.wait()
 
     def switch(self, shard, old: RankLayout, new: RankLayout):
         """In-place, chunked layout switch of this rank's shard (dist.py:520-526).
@@ -237,21 +240,35 @@ class ShardedRun:
         data arriving from the source whose B qubits spell j lands in the
         positions of segment j, which were just sent. Chunk by chunk of inner
         offsets: pack every segment's chunk into staging, one batched
-        send/recv, unpack into the same offsets. Returns the shard (same
-        buffer) in ``arrival_layout(old, new)``."""
+        send/recv, unpack into the same offsets. Two staging pairs alternate
+        so chunk m + 1 is packed (and chunk m - 1 unpacked) while chunk m is
+        on the wire. Returns the shard (same buffer) in
+        ``arrival_layout(old, new)``."""
         _, out_segs, incoming, _, c = switch_schedule(old, new, self.rank)
         A, B, pa = self.switch_plan(old, new)
         l = self.n_local
         inner = 1 << (l - c)
         amp = shard.element_size()
-        chunk = max(1, min(inner, self.chunk_bytes // (amp << c)))
-        send = self.ops.empty(chunk << c, shard)
-        recv = self.ops.empty(chunk << c, shard)
-        for begin in range(0, inner, chunk):
-            cnt = min(chunk, inner - begin)
-            self.ops.pack_range(shard, send, l, pa, begin, cnt)
-            self._exchange(send, recv, out_segs, incoming, cnt)
+        chunk = max(1, min(inner, self.chunk_bytes // (2 * (amp << c))))
+        bufs = [(self.ops.empty(chunk << c, shard), self.ops.empty(chunk << c, shard)) for _ in range(2)]
+        pending = None
+
+        def finish(p):
+            works, recv, begin, cnt = p
+            for w in works:
+                w.wait()  # the device stream waits for the transfer
             self.ops.unpack_range(recv, shard, l, pa, begin, cnt)
+
+        for m, begin in enumerate(range(0, inner, chunk)):
+            cnt = min(chunk, inner - begin)
+            send, recv = bufs[m % 2]
+            self.ops.pack_range(shard, send, l, pa, begin, cnt)
+            works = self._post(send, recv, out_segs, incoming, cnt)
+            if pending is not None:
+                finish(pending)
+            pending = (works, recv, begin, cnt)
+        if pending is not None:
+            finish(pending)
         return shard
 
     def run(self, shard, events=None, run_part=None):
