@@ -129,7 +129,7 @@ struct Gen {
     if (fr == 1.0 && fi == 0.0) return;
     if (fi == 0.0) {
       if (fr == -1.0) {
-        o << "      " << re(i) << " = -" << re(i) << "; " << im(i) << " = -" << im(i) << ";\n";
+        o << "      " << re(i) << " = NEG(" << re(i) << "); " << im(i) << " = NEG(" << im(i) << ");\n";
         return;
       }
       o << "      " << re(i) << " *= " << lit(fr, c128) << "; " << im(i) << " *= " << lit(fr, c128) << ";\n";
@@ -139,8 +139,8 @@ struct Gen {
     if (fr == 0.0) {  // (x + iy) * (i b) = -b y + i b x
       const std::string b = lit(fi, c128);
       o << "      { const " << R() << " x = " << re(i) << ", y = " << im(i) << "; ";
-      if (fi == 1.0) o << re(i) << " = -y; " << im(i) << " = x; }\n";
-      else if (fi == -1.0) o << re(i) << " = y; " << im(i) << " = -x; }\n";
+      if (fi == 1.0) o << re(i) << " = NEG(y); " << im(i) << " = x; }\n";
+      else if (fi == -1.0) o << re(i) << " = y; " << im(i) << " = NEG(x); }\n";
       else {
         o << re(i) << " = -" << b << " * y; " << im(i) << " = " << b << " * x; }\n";
         ops += 2 * wgt;
@@ -186,6 +186,7 @@ struct Gen {
       else e = "fma(" + lit(coef[t], c128) + ", " + src[t] + ", " + e + ")";
       ops += wgt;
     }
+    if (start >= 0 && e == "-" + src[start]) return "NEG(" + src[start] + ")";  // a lone negation: sign bit
     return e.empty() ? std::string(c128 ? "0.0" : "0.0f") : e;
   }
 
@@ -353,7 +354,7 @@ struct Gen {
       if (!tbits) {
         const bool one = rp;
         if (one) {
-          if (sign) o << "      " << re(i) << " = -" << re(i) << "; " << im(i) << " = -" << im(i) << ";\n";
+          if (sign) o << "      " << re(i) << " = NEG(" << re(i) << "); " << im(i) << " = NEG(" << im(i) << ");\n";
           else if (!d1one) cmul_const(i, in.m[2], in.m[3]);
         } else if (!d0one) {
           cmul_const(i, in.m[0], in.m[1]);
@@ -362,7 +363,9 @@ struct Gen {
       }
       const std::string one = rp ? "!tp" : "tp";
       if (sign) {
-        o << "      if (" << one << ") { " << re(i) << " = -" << re(i) << "; " << im(i) << " = -" << im(i) << "; }\n";
+        // sign flip on the integer pipe: XOR the sign bit under a per-thread mask
+        o << "      { const SM m_ = (" << one << ") ? SIGN_BIT : SM(0); " << re(i) << " = XSGN(" << re(i) << ", m_); "
+          << im(i) << " = XSGN(" << im(i) << ", m_); }\n";
       } else {
         o << "      { const " << R() << " dr = " << one << " ? " << d1r << " : " << d0r << ", di = " << one << " ? "
           << d1i << " : " << d0i << ";\n  ";
@@ -466,6 +469,19 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   const int amp = g.c128 ? 16 : 8;
   std::ostringstream& o = g.o;
   o << "typedef " << C << " C;\n";
+  if (g.c128)
+    o << "typedef unsigned long long SM;\n#define SIGN_BIT 0x8000000000000000ull\n"
+      << "__device__ __forceinline__ double XSGN(double x, SM m) { return __longlong_as_double(__double_as_longlong(x) ^ (long long)m); }\n";
+  else
+    o << "typedef unsigned SM;\n#define SIGN_BIT 0x80000000u\n"
+      << "__device__ __forceinline__ float XSGN(float x, SM m) { return __uint_as_float(__float_as_uint(x) ^ m); }\n";
+  // a sign flip the compiler cannot turn back into an FP64 negation
+  if (g.c128)
+    o << "__device__ __forceinline__ double NEG(double x) { double r; asm(\"{ .reg .b32 lo_, hi_; mov.b64 {lo_, hi_}, %1; "
+         "xor.b32 hi_, hi_, 0x80000000; mov.b64 %0, {lo_, hi_}; }\" : \"=d\"(r) : \"d\"(x)); return r; }\n";
+  else
+    o << "__device__ __forceinline__ float NEG(float x) { float r; asm(\"xor.b32 %0, %1, 0x80000000;\" : \"=f\"(r) : \"f\"(x)); "
+         "return r; }\n";
   o << "__device__ __forceinline__ unsigned swz(unsigned s) { return s ^ "
     << (g.c128 ? "(((s >> 3) ^ (s >> 6) ^ (s >> 9) ^ (s >> 12)) & 7u)" : "(((s >> 4) ^ (s >> 8) ^ (s >> 12)) & 15u)")
     << "; }\n";
