@@ -420,3 +420,34 @@ def test_run_stream_many_initial_states():
     torch.cuda.synchronize()
     for o, r in zip(outs, refs):
         assert float(np.max(np.abs(o.numpy() - r))) < 1e-10
+
+
+@pytest.mark.parametrize("extra", ["layout", "pingpong", "pingpong_init", "cluster"])
+def test_corpus_through_every_compiled_path(golden, extra):
+    """Every corpus circuit and partition (all gate kinds, controls on thread
+    and register bits, SWAPs, tiny states where a team is a few threads)
+    through the compiled kernels with the layout machinery switched on."""
+    from paper_2205_06973_b200.hier import PartProgram
+
+    base = _native.default_options() | _native.HS_PLAN_JIT
+    opts = {"layout": base | _native.HS_PLAN_LAYOUT,
+            "pingpong": base | _native.HS_PLAN_LAYOUT | _native.HS_PLAN_PINGPONG,
+            "pingpong_init": base | _native.HS_PLAN_LAYOUT | _native.HS_PLAN_PINGPONG | _native.HS_PLAN_INIT_LAYOUT,
+            "cluster": base | _native.HS_PLAN_CLUSTER}[extra]
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    checked = 0
+    for i, doc in enumerate(docs):
+        if i % 4:  # every fourth circuit, all its partitions (NVRTC compiles every part)
+            continue
+        c = parse_qasm(doc["qasm"])
+        for key, parts in doc["partitions"].items():
+            part = partition_of(parts)
+            exes = [remap_part(c, p) for p in part.parts]
+            prog = PartProgram(c.num_qubits, exes, options=opts)
+            assert prog.jit_error == ""
+            st = torch.zeros(1 << c.num_qubits, dtype=torch.complex128, device="cuda")
+            prog.init_basis(st, 0)
+            prog.run(st)
+            assert float(np.max(np.abs(st.cpu().numpy() - states[f"c{i}"]))) < 1e-10, (i, key, extra)
+            checked += 1
+    assert checked >= 15
