@@ -25,6 +25,52 @@ struct PartGraph {
   std::vector<int> pot;   // topological potential: pot[a] < pot[b] on every edge a -> b
   std::vector<int> mark;  // visit stamps for searches
   int stamp = 0;
+  // transitive closure (graphs up to kClosureMax groups): bit y of row x =
+  // y reachable from x by a path of >= 1 edge; queries become bit tests
+  static constexpr int kClosureMax = 16384;
+  int W = 0;
+  std::vector<uint64_t> R;
+  bool has(int x, int y) const { return R[size_t(x) * W + (y >> 6)] >> (y & 63) & 1; }
+
+  void build_closure(int G) {
+    W = (G + 63) / 64;
+    R.assign(size_t(G) * W, 0);
+    std::vector<int> order(G);
+    for (int i = 0; i < G; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return pot[a] > pot[b]; });  // sinks first
+    for (int x : order) {
+      uint64_t* rx = &R[size_t(x) * W];
+      for (int y : out[x]) {
+        rx[y >> 6] |= 1ull << (y & 63);
+        const uint64_t* ry = &R[size_t(y) * W];
+        for (int w = 0; w < W; ++w) rx[w] |= ry[w];
+      }
+    }
+  }
+  // after contracting v into u: u reaches what either reached; whoever
+  // reached u or v reaches u and all of it; v is gone
+  void merge_closure(int u, int v, const std::vector<char>& alive) {
+    uint64_t* ru = &R[size_t(u) * W];
+    const uint64_t* rv = &R[size_t(v) * W];
+    for (int w = 0; w < W; ++w) ru[w] |= rv[w];
+    ru[u >> 6] &= ~(1ull << (u & 63));
+    ru[v >> 6] &= ~(1ull << (v & 63));
+    const int G = (int)alive.size();
+    for (int x = 0; x < G; ++x) {
+      if (!alive[x] || x == u) continue;
+      uint64_t* rx = &R[size_t(x) * W];
+      const bool bu = rx[u >> 6] >> (u & 63) & 1, bv = rx[v >> 6] >> (v & 63) & 1;
+      if (!bu && !bv) continue;
+      for (int w = 0; w < W; ++w) rx[w] |= ru[w];
+      rx[u >> 6] |= 1ull << (u & 63);
+      rx[v >> 6] &= ~(1ull << (v & 63));
+    }
+  }
+  bool reaches_indirectly_closure(int src, int dst) const {
+    for (int m : out[src])
+      if (m != dst && has(m, dst)) return true;
+    return false;
+  }
 
   static void add_unique(std::vector<int>& v, int x) {
     if (std::find(v.begin(), v.end(), x) == v.end()) v.push_back(x);
@@ -112,6 +158,8 @@ extern "C" int hs_dagp_merge(int num_groups, const uint64_t* qmask, int num_edge
       }
     }
   }
+  const bool closure = G <= PartGraph::kClosureMax;
+  if (closure) g.build_closure(G);
   std::vector<uint64_t> q(qmask, qmask + G);
   std::vector<char> alive(G, 1);
   for (int i = 0; i < G; ++i) merged_into[i] = i;
@@ -124,15 +172,44 @@ extern "C" int hs_dagp_merge(int num_groups, const uint64_t* qmask, int num_edge
     k = (uint64_t(64 - shared) << 54) | (uint64_t(64 - uni) << 47) | (uint64_t(u) << 20) | uint64_t(v);
     return true;
   };
+  // Pairs sharing no qubit have keys after every sharing pair, so they are
+  // only needed once the heap's minimum gets there: insert them then (for the
+  // groups still alive, with current keys). Until that moment the reference
+  // could only pop sharing pairs, so the pop sequence is the same, and the
+  // heap starts with the sharing pairs only (found per qubit).
+  const uint64_t kShared0 = uint64_t(64) << 54;  // keys >= this share no qubit
   std::vector<uint64_t> init;
-  for (int u = 0; u < G; ++u)
-    for (int v = u + 1; v < G; ++v) {
-      uint64_t k;
-      if (key(u, v, k)) init.push_back(k);
-    }
+  {
+    std::vector<std::vector<int>> by_qubit(64);
+    for (int u = 0; u < G; ++u)
+      for (int b = 0; b < 64; ++b)
+        if (q[u] >> b & 1) by_qubit[b].push_back(u);
+    for (auto& lst : by_qubit)
+      for (size_t i = 0; i < lst.size(); ++i)
+        for (size_t j = i + 1; j < lst.size(); ++j) {
+          uint64_t k;
+          if (key(lst[i], lst[j], k)) init.push_back(k);
+        }
+    std::sort(init.begin(), init.end());
+    init.erase(std::unique(init.begin(), init.end()), init.end());
+  }
   std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>> heap(std::greater<uint64_t>(),
                                                                                     std::move(init));
-  while (!heap.empty()) {
+  bool disjoint_in = false;
+  for (;;) {
+    if (!disjoint_in && (heap.empty() || heap.top() >= kShared0)) {
+      disjoint_in = true;
+      std::vector<int> live;
+      for (int i = 0; i < G; ++i)
+        if (alive[i]) live.push_back(i);
+      for (size_t i = 0; i < live.size(); ++i)
+        for (size_t j = i + 1; j < live.size(); ++j) {
+          if (q[live[i]] & q[live[j]]) continue;
+          uint64_t k;
+          if (key(live[i], live[j], k)) heap.push(k);
+        }
+    }
+    if (heap.empty()) break;
     const uint64_t entry = heap.top();
     heap.pop();
     const int u = int((entry >> 20) & 0xFFFFF), v = int(entry & 0xFFFFF);
@@ -140,10 +217,13 @@ extern "C" int hs_dagp_merge(int num_groups, const uint64_t* qmask, int num_edge
     uint64_t k;
     if (!key(u, v, k)) continue;
     if (k != entry) { heap.push(k); continue; }
-    if (g.reaches_indirectly(u, v) || g.reaches_indirectly(v, u)) continue;
+    if (closure ? (g.reaches_indirectly_closure(u, v) || g.reaches_indirectly_closure(v, u))
+                : (g.reaches_indirectly(u, v) || g.reaches_indirectly(v, u)))
+      continue;
     alive[v] = 0;
     q[u] |= q[v];
     g.contract(u, v);
+    if (closure) g.merge_closure(u, v, alive);
     for (int i = 0; i < G; ++i) {
       if (!alive[i] || i == u) continue;
       if (key(std::min(u, i), std::max(u, i), k)) heap.push(k);
