@@ -305,6 +305,41 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
 
     # e2e through the public API: host initial state in, host state out
     e2e = None
+    if dist and not args.no_e2e:
+        # every rank uploads its shard of the initial state (natural order of
+        # the first layout) from pinned host memory, runs all parts and
+        # switches, and downloads its final shard; max over ranks
+        run_e2e = ShardedRun(circuit, part, int(math.log2(world)), device=dev, basis_start=False)
+        host_in = torch.zeros(1 << n_local, dtype=torch.complex128).pin_memory()
+        if rank == 0:
+            host_in[0] = 1.0
+        host_out = torch.empty(1 << n_local, dtype=torch.complex128).pin_memory()
+
+        def e2e_step():
+            state.copy_(host_in, non_blocking=True)
+            out = run_e2e.run(state)
+            host_out.copy_(out, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(t.item())
+        e2e = {"value": world * num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
+               "launches_per_step": sum(pr.num_launches for pr in run_e2e.programs if pr is not None),
+               "ms_per_step": e_ms, "h2d_bytes_per_step": world * (1 << n_local) * 16,
+               "d2h_bytes_per_step": world * (1 << n_local) * 16,
+               "path": "public API ShardedRun.run per rank: shard uploaded from pinned host, every part and "
+                       "layout switch, shard downloaded; max over ranks"}
     if not dist and not args.no_e2e:
         # a caller's initial state arrives in natural order: the e2e program
         # is planned without an initial layout of its own
