@@ -422,8 +422,10 @@ def test_run_stream_many_initial_states():
         assert float(np.max(np.abs(o.numpy() - r))) < 1e-10
 
 
-@pytest.mark.parametrize("extra", ["layout", "pingpong", "pingpong_init", "cluster"])
-def test_corpus_through_every_compiled_path(golden, extra):
+@pytest.mark.parametrize("extra,dtype", [("layout", "complex128"), ("pingpong", "complex128"),
+                                         ("pingpong_init", "complex128"), ("cluster", "complex128"),
+                                         ("pingpong_init", "complex64")])
+def test_corpus_through_every_compiled_path(golden, extra, dtype):
     """Every corpus circuit and partition (all gate kinds, controls on thread
     and register bits, SWAPs, tiny states where a team is a few threads)
     through the compiled kernels with the layout machinery switched on."""
@@ -443,11 +445,12 @@ def test_corpus_through_every_compiled_path(golden, extra):
         for key, parts in doc["partitions"].items():
             part = partition_of(parts)
             exes = [remap_part(c, p) for p in part.parts]
-            prog = PartProgram(c.num_qubits, exes, options=opts)
+            prog = PartProgram(c.num_qubits, exes, options=opts, dtype=dtype)
             assert prog.jit_error == ""
-            st = torch.zeros(1 << c.num_qubits, dtype=torch.complex128, device="cuda")
+            st = torch.zeros(1 << c.num_qubits, dtype=prog.dtype, device="cuda")
             prog.init_basis(st, 0)
             prog.run(st)
-            assert float(np.max(np.abs(st.cpu().numpy() - states[f"c{i}"]))) < 1e-10, (i, key, extra)
+            err = float(np.max(np.abs(st.cpu().numpy().astype(np.complex128) - states[f"c{i}"])))
+            assert err < TOL[dtype], (i, key, extra)
             checked += 1
     assert checked >= 15
