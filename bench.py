@@ -46,7 +46,9 @@ def _peaks():
 def _traffic_from_profiles(config: str, strategy: str):
     """Per-launch DRAM bytes of the part kernel from the committed ncu
     summary of this workload (profiles/*_ncu_summary.json), else None."""
-    for f in sorted((ROOT / "profiles").glob("*ncu_summary.json"), reverse=True):
+    files = sorted((ROOT / "profiles").glob("*ncu_summary.json"), reverse=True)
+    files.sort(key=lambda f: "final" not in f.name)  # the latest capture of this round first
+    for f in files:
         try:
             d = json.loads(f.read_text())
         except Exception:
