@@ -14,6 +14,7 @@
 // relabels where two qubits live and the final store writes the tile back in
 // natural order.
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstring>
 
@@ -665,6 +666,32 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
           if (std::find(want.begin(), want.end(), (int)last->npos[m]) == want.end()) order.push_back(last->npos[m]);
         for (int m = 0; m < T - RB; ++m) last->npos[m] = (uint8_t)order[m];
         direct = true;
+      }
+    }
+    // Otherwise the registers go to shared memory in the store order first:
+    // pick the last phase's lanes 0..hot-1 so that both their tile locations
+    // (the phase's loads) and their store slots (that write) cover every
+    // swizzle residue - both bank-conflict free.
+    if (!direct && T - RB >= hot) {
+      std::vector<int> cand(last->npos, last->npos + (T - RB));
+      auto slot = [&](int loc) { return rho[bit_at[loc]]; };
+      std::vector<int> pick;
+      std::function<bool(size_t, uint32_t, uint32_t)> dfs = [&](size_t from, uint32_t rl, uint32_t rs) -> bool {
+        if ((int)pick.size() == hot) return true;
+        for (size_t i = from; i < cand.size(); ++i) {
+          const uint32_t a = 1u << (cand[i] % hot), b = 1u << (slot(cand[i]) % hot);
+          if ((rl & a) || (rs & b)) continue;
+          pick.push_back(cand[i]);
+          if (dfs(i + 1, rl | a, rs | b)) return true;
+          pick.pop_back();
+        }
+        return false;
+      };
+      if (dfs(0, 0, 0)) {
+        std::vector<int> order(pick);
+        for (int c : cand)
+          if (std::find(pick.begin(), pick.end(), c) == pick.end()) order.push_back(c);
+        for (int m = 0; m < T - RB; ++m) last->npos[m] = (uint8_t)order[m];
       }
     }
   }
