@@ -140,9 +140,11 @@ class ShardedRun:
 
     def __init__(self, circuit, partition, num_rank_bits: int, group=None, device=None, ops=None,
                  dtype="complex128", program=True, chunk_bytes: int = SWITCH_CHUNK_BYTES, basis_start: bool = True,
-                 loopback: bool = False):
+                 loopback: bool = False, policy: str = "lookahead"):
         """``loopback``: all ranks live in this process on one device
-        (``run_loopback``); no process group is used."""
+        (``run_loopback``); no process group is used. ``policy``: layout
+        schedule (``dist.plan_layouts``): "lookahead" (default: fewest remap
+        bytes) or "reference" (the reference's layouts and CommStats)."""
         import torch.distributed as dist
 
         self.circuit = circuit
@@ -159,7 +161,8 @@ class ShardedRun:
         self.n = circuit.num_qubits
         self.n_local = self.n - num_rank_bits
         self.chunk_bytes = int(chunk_bytes)
-        self.first, self.layouts, switches = plan_layouts(circuit, partition, num_rank_bits)
+        self.policy = policy
+        self.first, self.layouts, switches = plan_layouts(circuit, partition, num_rank_bits, policy)
         self.switch_at = {i: (old, new, st) for i, old, new, st in switches}
         self.exes, self.bounds = [], []
         for i, lay in enumerate(self.layouts):
@@ -354,14 +357,14 @@ class ShardedState:
 
 
 def simulate_distributed_group(circuit, partition, num_rank_bits, *, group=None, initial=None, dtype="complex128",
-                               device=None) -> DistributedRun:
+                               device=None, policy: str = "reference") -> DistributedRun:
     """``simulate_distributed`` over a process group: every rank returns its
     own shard (``DistributedRun.state`` is a ``ShardedState``)."""
     import torch
 
     from .statevec import allocate, init_basis
 
-    run = ShardedRun(circuit, partition, num_rank_bits, group=group, device=device, dtype=dtype)
+    run = ShardedRun(circuit, partition, num_rank_bits, group=group, device=device, dtype=dtype, policy=policy)
     shard = allocate(run.n_local, dtype, device)
     if initial is None:
         if run.rank == 0:

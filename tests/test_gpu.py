@@ -372,7 +372,8 @@ def test_program_from_a_given_layout():
     assert float(np.max(np.abs(st.cpu().numpy() - ref))) < 1e-10
 
 
-def test_sharded_run_loopback_on_one_gpu(golden):
+@pytest.mark.parametrize("policy", ["reference", "lookahead"])
+def test_sharded_run_loopback_on_one_gpu(golden, policy):
     """The distributed path's device pieces - in-place chunked switches
     (pack/unpack kernels) and segment programs starting from the arrival
     layout - for all ranks on one GPU (transfers as copies), against the
@@ -386,7 +387,9 @@ def test_sharded_run_loopback_on_one_gpu(golden):
         for d in doc["dist"]:
             if not d["switches"] or c.num_qubits < 8:
                 continue
-            run = ShardedRun(c, partition_of(d["parts"]), d["p"], loopback=True, chunk_bytes=256)
+            run = ShardedRun(c, partition_of(d["parts"]), d["p"], loopback=True, chunk_bytes=256, policy=policy)
+            if policy == "reference":
+                assert [[list(x.local), list(x.process)] for x in run.layouts] == d["layouts"]
             R = 1 << d["p"]
             shards = [torch.zeros(1 << run.n_local, dtype=torch.complex128, device="cuda") for _ in range(R)]
             shards[0][0] = 1.0
@@ -454,3 +457,15 @@ def test_corpus_through_every_compiled_path(golden, extra, dtype):
             assert err < TOL[dtype], (i, key, extra)
             checked += 1
     assert checked >= 15
+
+
+def test_emulated_ranks_lookahead_policy(golden):
+    """simulate_distributed(policy="lookahead"): the same amplitudes as the
+    reference with no more remote bytes than its schedule."""
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    for i, doc in enumerate(docs[:20]):
+        c = parse_qasm(doc["qasm"])
+        for d in doc["dist"]:
+            run = simulate_distributed(c, partition_of(d["parts"]), d["p"], policy="lookahead")
+            assert _dev_err(run.state, states[f"c{i}"]) < 1e-10
+            assert run.stats.total_bytes <= sum(s["bytes_remote"] for s in d["switches"])

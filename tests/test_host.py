@@ -252,3 +252,28 @@ def test_native_dagp_merge_on_tfim_chain():
         P._NATIVE_MERGE = True
     a = partition_dagp(d, 8)
     assert [(p.gate_indices, p.qubits) for p in a.parts] == [(p.gate_indices, p.qubits) for p in b.parts]
+
+
+@pytest.mark.parametrize("name,limit,p", [("c5", 14, 3), ("c3", 12, 3), ("c4@20", 8, 2), ("c2", 12, 1)])
+def test_lookahead_remap_policy(name, limit, p):
+    """plan_layouts(policy="lookahead"): every part's qubits are local in its
+    layout, consecutive layouts differ only where a part needed a rank
+    qubit, and the remote volume never exceeds the reference policy's."""
+    from paper_2205_06973_b200 import build_dag, configs, partition_dfs
+
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), limit)
+    _, ref_layouts, ref_sw = plan_layouts(c, part, p, "reference")
+    first, layouts, sw = plan_layouts(c, part, p, "lookahead")
+    for lay, pt in zip(layouts, part.parts):
+        assert all(lay.is_local(q) for q in pt.qubits)
+    at = {i: (old, new) for i, old, new, _ in sw}
+    prev = first
+    for i, lay in enumerate(layouts):
+        if i in at:
+            assert at[i][0] == prev and at[i][1] == lay and lay != prev
+        else:
+            assert lay == prev
+        prev = lay
+    assert sum(s.bytes_remote for *_, s in sw) <= sum(s.bytes_remote for *_, s in ref_sw)
+    assert len(sw) <= len(ref_sw)
