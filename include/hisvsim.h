@@ -131,6 +131,10 @@ typedef struct {
  * as a short sequence of passes over sub-parts of its gates that fit the tile
  * (the hierarchical idea one level down; same results). */
 #define HS_PLAN_CLUSTER 0x80u
+/* with HS_PLAN_LAYOUT: leave the buffer in the program's final layout
+ * (hs_program_final_layout) instead of restoring natural order, e.g. when a
+ * layout switch that can pack from any layout follows */
+#define HS_PLAN_NO_RESTORE 0x100u
 #define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
 
 typedef struct hs_engine hs_engine;
@@ -169,6 +173,9 @@ int hs_program_part_info(hs_program* prog, int part, hs_part_info* out);
  * (phys[n_local]; identity unless HS_PLAN_INIT_LAYOUT). Basis state |x>
  * lives at index sum_q bit_q(x) << phys[q]. */
 int hs_program_initial_layout(hs_program* prog, int32_t* phys);
+/* physical bit of each logical position after the program's last launch
+ * (identity unless HS_PLAN_NO_RESTORE) */
+int hs_program_final_layout(hs_program* prog, int32_t* phys);
 /* scratch buffer for HS_PLAN_PINGPONG programs: device memory of at least
  * the state's size, owned by the caller, used by every later run */
 int hs_program_bind_scratch(hs_program* prog, void* scratch, size_t bytes);

@@ -30,6 +30,7 @@ EXPORTS = (
     "hs_engine_query", "hs_engine_set_options", "hs_program_create", "hs_program_create_from_layout",
     "hs_program_destroy",
     "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_initial_layout",
+    "hs_program_final_layout",
     "hs_program_bind_scratch",
     "hs_program_jit_error",
     "hs_program_dump",
@@ -101,6 +102,7 @@ def _declare(lib) -> None:
         "hs_program_num_launches": (I, [P]),
         "hs_program_jit_error": (ctypes.c_char_p, [P]),
         "hs_program_initial_layout": (I, [P, ctypes.POINTER(ctypes.c_int32)]),
+        "hs_program_final_layout": (I, [P, ctypes.POINTER(ctypes.c_int32)]),
         "hs_program_bind_scratch": (I, [P, P, ctypes.c_size_t]),
         "hs_program_part_info": (I, [P, I, ctypes.POINTER(HsPartInfo)]),
         "hs_program_dump": (I, [P, I, P, ctypes.c_size_t, ctypes.POINTER(I),
@@ -193,7 +195,7 @@ def engine_query(device: int) -> dict:
 
 
 HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY, HS_PLAN_LAYOUT, HS_PLAN_JIT = 0x1, 0x2, 0x4, 0x8, 0x10
-HS_PLAN_INIT_LAYOUT, HS_PLAN_PINGPONG, HS_PLAN_CLUSTER = 0x20, 0x40, 0x80
+HS_PLAN_INIT_LAYOUT, HS_PLAN_PINGPONG, HS_PLAN_CLUSTER, HS_PLAN_NO_RESTORE = 0x20, 0x40, 0x80, 0x100
 HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY
 
 

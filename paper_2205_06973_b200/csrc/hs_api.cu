@@ -45,6 +45,7 @@ struct hs_program {
   int dtype = 0;
   int user_parts = 0;            // plans beyond this are layout-restore launches
   std::vector<int32_t> init_phys; // layout the program expects its input in
+  std::vector<int32_t> final_phys; // layout the program leaves the buffer in
   void* scratch = nullptr;        // HS_PLAN_PINGPONG partner buffer (caller-owned)
   size_t scratch_bytes = 0;
   std::string jit_error;         // why HS_PLAN_JIT fell back to the interpreter
@@ -170,7 +171,7 @@ static int program_create(hs_engine* eng, int n_local, int dtype, const hs_part*
     // thread, so complex64 tiles are 12 bits there too
     const int tile = (eng->options & HS_PLAN_JIT) ? std::min(tile_for(eng, dtype), 12) : tile_for(eng, dtype);
     int s = plan_program(n_local, dtype, tile, eng->options, parts, num_parts, gates, num_gates,
-                         prog->plans, err, &prog->init_phys, init_phys);
+                         prog->plans, err, &prog->init_phys, init_phys, &prog->final_phys);
     if (s != HS_OK) return fail(s, err);
   }
   prog->user_parts = num_parts;
@@ -292,6 +293,13 @@ int hs_program_bind_scratch(hs_program* prog, void* scratch, size_t bytes) {
   if (!prog) return fail(HS_ERR_INVALID, "program is NULL");
   prog->scratch = scratch;
   prog->scratch_bytes = scratch ? bytes : 0;
+  return HS_OK;
+}
+
+int hs_program_final_layout(hs_program* prog, int32_t* phys) {
+  if (!prog || !phys) return fail(HS_ERR_INVALID, "program/phys is NULL");
+  for (int q = 0; q < prog->n_local; ++q)
+    phys[q] = q < (int)prog->final_phys.size() ? prog->final_phys[q] : q;
   return HS_OK;
 }
 

@@ -103,7 +103,8 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
 // restore launches that bring every qubit home at the end).
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                  const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
-                 std::vector<int32_t>* init_phys = nullptr, const int32_t* given_init = nullptr);
+                 std::vector<int32_t>* init_phys = nullptr, const int32_t* given_init = nullptr,
+                 std::vector<int32_t>* final_phys = nullptr);
 
 // 2x2 base matrix of a gate kind (controls handled by masking), row-major
 // complex: m[0..7] = m00 re/im, m01, m10, m11. Mirrors statevec.py:33-98.

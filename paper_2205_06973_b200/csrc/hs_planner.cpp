@@ -883,7 +883,7 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
 
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                  const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
-                 std::vector<int32_t>* init_phys, const int32_t* given_init) {
+                 std::vector<int32_t>* init_phys, const int32_t* given_init, std::vector<int32_t>* final_phys) {
   bool wide = false;
   for (int i = 0; i < num_parts; ++i) wide |= parts[i].num_staged > tile_max;
   if (wide && !((options & HS_PLAN_CLUSTER) && (options & HS_PLAN_JIT))) {
@@ -893,7 +893,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, xp, xg, owner, err);
     if (s != HS_OK) return s;
     s = plan_program(n_local, dtype, tile_max, options, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
-                     err, init_phys, given_init);
+                     err, init_phys, given_init, final_phys);
     if (s != HS_OK) return s;
     for (auto& pl : plans)
       if (pl.info.user_part >= 0) pl.info.user_part = owner[pl.info.user_part];
@@ -949,8 +949,9 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
   // the last part writes natural order directly only if qubits 0..hot-1 are
   // among its own (coalesced stores); otherwise it writes a coalesced layout
   // and one gate-free out-of-place launch permutes into natural order
+  const bool no_restore = (options & HS_PLAN_NO_RESTORE) != 0;
   bool need_restore = false;
-  if (pp) {
+  if (pp && !no_restore) {
     const hs_part& pl = parts[num_parts - 1];
     for (int q = 0; q < hot; ++q) {
       bool in = false;
@@ -975,7 +976,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       lay.inv_in = inv.data();
       lay.phys_out = next.data();
       lay.mode = LAYOUT_OOP;
-      if (i + 1 == num_parts && !need_restore) {
+      if (i + 1 == num_parts && !need_restore && !no_restore) {
         for (int q = 0; q < n_local; ++q) tgt[q] = q;  // the last part writes natural order
       } else {
         // the next layout: this tile's qubits that the next part stages go
@@ -1021,7 +1022,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       lay.target = home.data();
       // in place: the last part sends its qubits home, restore launches
       // fix the rest (ping-pong part 0 only prepares the next layout)
-      lay.mode = (!pp && i + 1 == num_parts) ? LAYOUT_TARGET : LAYOUT_PRIORITY;
+      lay.mode = (!pp && !no_restore && i + 1 == num_parts) ? LAYOUT_TARGET : LAYOUT_PRIORITY;
     }
     std::string e;
     int s = plan_part(n_local, dtype, tile_max, options, p.staged, p.num_staged, gates + p.gate_offset, p.num_gates,
@@ -1064,8 +1065,11 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     pl.launch.out_buf = cur_buf ^ 1;
     plans.push_back(pl);
   }
-  if (pp) return HS_OK;  // natural order, in the state
-  if (layout) return plan_restore(n_local, dtype, tile_max, options, phys, plans, err);
+  if (layout && !pp && !no_restore) {
+    int s = plan_restore(n_local, dtype, tile_max, options, phys, plans, err);
+    if (s != HS_OK) return s;
+  }
+  if (final_phys) final_phys->assign(phys.begin(), phys.begin() + n_local);  // identity once restored
   return HS_OK;
 }
 

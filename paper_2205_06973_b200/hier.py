@@ -216,7 +216,8 @@ class PartProgram:
     once; ``run`` only launches."""
 
     def __init__(self, n_local: int, exes: Sequence[ExecutablePart], dtype="complex128", device=None,
-                 options: int | None = None, basis_start: bool = False, init_layout: Sequence[int] | None = None):
+                 options: int | None = None, basis_start: bool = False, init_layout: Sequence[int] | None = None,
+                 final_natural: bool = True):
         """``options``: planner bits (``_native.HS_PLAN_*``); default: the
         engine default plus ``HS_PLAN_JIT`` / ``HS_PLAN_LAYOUT`` by state
         size. ``basis_start``: the program will only be run on basis states
@@ -224,7 +225,9 @@ class PartProgram:
         (``HS_PLAN_INIT_LAYOUT``; ``run`` then expects that layout).
         ``init_layout``: the buffer arrives with logical position q on
         physical bit ``init_layout[q]`` (after an in-place layout switch);
-        the program ends in natural order."""
+        the program ends in natural order unless ``final_natural`` is False
+        (then the buffer stays in ``final_layout``; a layout switch packs
+        from it)."""
         import torch
 
         self.n_local = n_local
@@ -260,6 +263,8 @@ class PartProgram:
             options &= ~_native.HS_PLAN_INIT_LAYOUT
         else:
             init_layout = None
+        if not final_natural and options & _native.HS_PLAN_LAYOUT:
+            options |= _native.HS_PLAN_NO_RESTORE
         self.options = options
         parts, gates, total = _pack(exes)
         out = ctypes.c_void_p()
@@ -285,6 +290,9 @@ class PartProgram:
         _native.check(lib.hs_program_initial_layout(self._h, phys))
         #: physical bit of each qubit in the state ``run`` expects
         self.initial_layout = tuple(int(phys[q]) for q in range(n_local))
+        _native.check(lib.hs_program_final_layout(self._h, phys))
+        #: ... and the layout ``run`` leaves it in (natural unless final_natural=False)
+        self.final_layout = tuple(int(phys[q]) for q in range(n_local))
 
     def basis_index(self, index: int) -> int:
         """Where basis state |index> lives in the program's initial layout."""

@@ -42,11 +42,14 @@ class Segment:
     peer: int      # destination rank
 
 
-def switch_schedule(old: RankLayout, new: RankLayout, rank: int):
+def switch_schedule(old: RankLayout, new: RankLayout, rank: int, A=None):
     """For ``rank``: the packed storage order, the outgoing segments, the
     incoming segments (source rank -> slot in the receive buffer) and the
-    receive-buffer storage order (low: kept locals, high: B qubits)."""
-    A = [q for q in old.local if q in new.process]
+    receive-buffer storage order (low: kept locals, high: B qubits).
+    ``A``: order of the outgoing qubits = the bits of a segment index
+    (default ascending; the in-place switch orders them by physical bit)."""
+    if A is None:
+        A = [q for q in old.local if q in new.process]
     B = [q for q in old.process if q in new.local]
     kept = [q for q in old.local if q not in A]
     c = len(A)
@@ -175,15 +178,32 @@ class ShardedRun:
         self.segments = list(zip(starts, ends))
         self.ops = ops or DeviceOps()
         self.programs = []
+        self.seg_phys_in, self.seg_phys_out = [], []  # per segment: layout in / out (None = natural)
         if program:
+            # a segment followed by a switch leaves the shard in its final
+            # layout (no restore passes): the switch packs from it, and the
+            # next segment starts from the layout the switch leaves
+            phys = None
             for si, (a, b) in enumerate(self.segments):
+                init = None
+                if si > 0:
+                    old, new, _ = self.switch_at[a]
+                    init = self.arrival_layout(old, new, phys)
+                self.seg_phys_in.append(init)
                 ex = self.exes[self.bounds[a][0]:self.bounds[b - 1][0] + self.bounds[b - 1][1]] if b > a else []
+                last = si + 1 == len(self.segments)
                 if not ex:
                     self.programs.append(None)
+                    phys = None if init is None else tuple(init)
+                    if last and phys is not None:
+                        raise NotImplementedError("a switch with no parts after it")
+                    self.seg_phys_out.append(phys)
                     continue
-                init = None if si == 0 else self.arrival_layout(*self.switch_at[a][:2])
-                self.programs.append(PartProgram(self.n_local, ex, dtype=dtype, device=device, init_layout=init,
-                                                 basis_start=basis_start and si == 0))
+                pr = PartProgram(self.n_local, ex, dtype=dtype, device=device, init_layout=init,
+                                 basis_start=basis_start and si == 0, final_natural=last)
+                self.programs.append(pr)
+                phys = None if pr.final_layout == tuple(range(self.n_local)) else pr.final_layout
+                self.seg_phys_out.append(phys)
         self.program = self.programs[0] if self.programs else None
         self.stats = CommStats(self.n, num_rank_bits, len(self.layouts),
                                [st for _, _, st in self.switch_at.values()])
@@ -196,20 +216,25 @@ class ShardedRun:
                 "remote_fraction_of_state": self.stats.total_bytes / float((1 << self.n) * 16)}
 
     @staticmethod
-    def switch_plan(old: RankLayout, new: RankLayout):
-        """Offset positions of the outgoing qubits A (ascending) and the
-        incoming qubits B, bit i of a segment / slot index = A[i] / B[i]."""
+    def switch_plan(old: RankLayout, new: RankLayout, phys=None):
+        """Physical bits of the outgoing qubits A (ascending: A is ordered by
+        them) and the incoming qubits B; bit i of a segment / slot index is
+        A[i] / B[i]. ``phys``: physical bit of each offset position of
+        ``old`` in the shard (the previous segment's final layout; None =
+        natural)."""
+        at = (lambda j: j) if phys is None else (lambda j: phys[j])
         A = [q for q in old.local if q in new.process]
+        A.sort(key=lambda q: at(old.local.index(q)))
         B = [q for q in old.process if q in new.local]
-        pa = [old.local.index(q) for q in A]
+        pa = [at(old.local.index(q)) for q in A]
         return A, B, pa
 
     @classmethod
-    def arrival_layout(cls, old: RankLayout, new: RankLayout):
+    def arrival_layout(cls, old: RankLayout, new: RankLayout, phys=None):
         """Physical offset bit of each of ``new.local``'s qubits after the
-        in-place switch: kept qubits stay, B[i] lands on A[i]'s position."""
-        A, B, pa = cls.switch_plan(old, new)
-        where = {q: j for j, q in enumerate(old.local)}
+        in-place switch: kept qubits stay, B[i] lands on A[i]'s bit."""
+        A, B, pa = cls.switch_plan(old, new, phys)
+        where = {q: (j if phys is None else phys[j]) for j, q in enumerate(old.local)}
         for i, q in enumerate(B):
             where[q] = pa[i]
         return tuple(where[q] for q in new.local)
@@ -236,7 +261,7 @@ class ShardedRun:
         for w in self._post(packed, recv, out_segs, incoming, seg):
             w.wait()
 
-    def switch(self, shard, old: RankLayout, new: RankLayout):
+    def switch(self, shard, old: RankLayout, new: RankLayout, phys=None):
         """In-place, chunked layout switch of this rank's shard (dist.py:520-526).
 
         Segment k of the shard (the A qubits spell k) goes to one peer; the
@@ -247,8 +272,8 @@ class ShardedRun:
         so chunk m + 1 is packed (and chunk m - 1 unpacked) while chunk m is
         on the wire. Returns the shard (same buffer) in
         ``arrival_layout(old, new)``."""
-        _, out_segs, incoming, _, c = switch_schedule(old, new, self.rank)
-        A, B, pa = self.switch_plan(old, new)
+        A, B, pa = self.switch_plan(old, new, phys)
+        _, out_segs, incoming, _, c = switch_schedule(old, new, self.rank, A)
         l = self.n_local
         inner = 1 << (l - c)
         amp = shard.element_size()
@@ -289,7 +314,8 @@ class ShardedRun:
         for si, (a, b) in enumerate(self.segments):
             if a in self.switch_at:
                 old, new, _ = self.switch_at[a]
-                shard = self.switch(shard, old, new)
+                phys = self.seg_phys_out[si - 1] if run_part is None and self.programs else None
+                shard = self.switch(shard, old, new, phys)
                 mark("switch")
                 if run_part is not None:  # host stand-ins run parts in natural order
                     shard = self.ops.to_natural(shard, self.arrival_layout(old, new))
@@ -315,9 +341,9 @@ def run_loopback(run: ShardedRun, shards):
     for si, (a, b) in enumerate(run.segments):
         if a in run.switch_at:
             old, new, _ = run.switch_at[a]
-            sched = [switch_schedule(old, new, r) for r in range(R)]
+            A, _, pa = run.switch_plan(old, new, run.seg_phys_out[si - 1])
+            sched = [switch_schedule(old, new, r, A) for r in range(R)]
             c = sched[0][4]
-            _, _, pa = run.switch_plan(old, new)
             inner = 1 << (l - c)
             amp = shards[0].element_size()
             chunk = max(1, min(inner, run.chunk_bytes // (amp << c)))

@@ -381,7 +381,7 @@ def test_sharded_run_loopback_on_one_gpu(golden, policy):
     from paper_2205_06973_b200.multi import ShardedRun, run_loopback, shard_positions
 
     docs, states = golden.json("corpus"), golden.npz("corpus")
-    checked = 0
+    checked = handed = 0
     for i, doc in enumerate(docs):
         c = parse_qasm(doc["qasm"])
         for d in doc["dist"]:
@@ -399,7 +399,9 @@ def test_sharded_run_loopback_on_one_gpu(golden, policy):
                 full[shard_positions(run.layouts[-1], r)] = shards[r].cpu().numpy()
             assert np.max(np.abs(full - states[f"c{i}"])) < 1e-10, (i, d["p"])
             checked += 1
+            handed += sum(1 for ph in run.seg_phys_out[:-1] if ph is not None)
     assert checked >= 5
+    assert handed >= 1  # some switch packed straight from a segment's final (non-natural) layout
 
 
 def test_run_stream_many_initial_states():
@@ -469,3 +471,25 @@ def test_emulated_ranks_lookahead_policy(golden):
             run = simulate_distributed(c, partition_of(d["parts"]), d["p"], policy="lookahead")
             assert _dev_err(run.state, states[f"c{i}"]) < 1e-10
             assert run.stats.total_bytes <= sum(s["bytes_remote"] for s in d["switches"])
+
+
+@pytest.mark.parametrize("policy", ["reference", "lookahead"])
+def test_sharded_run_loopback_large_shards(policy):
+    """24 qubits over 2 ranks (23 local: compiled, layout-planned segments):
+    segments before a switch end in their own layout and the switch packs
+    from it; the assembled state equals the C oracle's."""
+    from paper_2205_06973_b200.multi import ShardedRun, run_loopback, shard_positions
+
+    c = configs.build("c3@24")
+    part = partition_dfs(build_dag(c), 12)
+    run = ShardedRun(c, part, 1, loopback=True, policy=policy)
+    assert run.switch_at
+    shards = [torch.zeros(1 << run.n_local, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    shards[0][0] = 1.0
+    shards = run_loopback(run, shards)
+    full = np.zeros(1 << c.num_qubits, dtype=np.complex128)
+    for r in range(2):
+        full[shard_positions(run.layouts[-1], r)] = shards[r].cpu().numpy()
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert float(np.max(np.abs(full - ref))) < 1e-10
+    assert any(ph is not None for ph in run.seg_phys_out[:-1])
