@@ -365,6 +365,15 @@ class PartProgram:
         self._bind_scratch(data)
         _native.check(self._lib.hs_program_run(self._h, data.data_ptr(), rows, first, count, s))
 
+    @property
+    def needs_scratch(self) -> bool:
+        return bool(self.options & _native.HS_PLAN_PINGPONG)
+
+    def share_scratch(self, scratch) -> None:
+        """Use ``scratch`` (a device tensor at least the state's size) as the
+        ping-pong partner, e.g. one buffer for several programs."""
+        self._scratch = scratch
+
     def _bind_scratch(self, data) -> None:
         """HS_PLAN_PINGPONG: a device buffer like ``data`` the parts alternate
         with (allocated once per shape, kept by the program)."""

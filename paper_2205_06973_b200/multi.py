@@ -208,6 +208,20 @@ class ShardedRun:
         self.stats = CommStats(self.n, num_rank_bits, len(self.layouts),
                                [st for _, _, st in self.switch_at.values()])
 
+    def _share_scratch(self, shard) -> None:
+        """One ping-pong scratch buffer for all segment programs (each would
+        otherwise keep its own shard-sized buffer)."""
+        sc = getattr(self, "_scratch", None)
+        if not any(pr is not None and pr.needs_scratch for pr in self.programs):
+            return
+        if sc is None or sc.numel() < shard.numel() or sc.dtype != shard.dtype or sc.device != shard.device:
+            import torch
+
+            self._scratch = sc = torch.empty(shard.numel(), dtype=shard.dtype, device=shard.device)
+        for pr in self.programs:
+            if pr is not None:
+                pr.share_scratch(sc)
+
     def part_infos(self):
         return [pr.info(i) for pr in self.programs if pr is not None for i in range(pr.num_parts)]
 
@@ -325,6 +339,7 @@ class ShardedRun:
                     for j in range(start, start + count):
                         run_part(shard, self.exes[j])
             elif self.programs[si] is not None:
+                self._share_scratch(shard)
                 self.programs[si].run(shard)
             mark("parts")
         return shard
@@ -360,6 +375,7 @@ def run_loopback(run: ShardedRun, shards):
                 for r in range(R):
                     run.ops.unpack_range(recv[r], shards[r], l, pa, begin, cnt)
         if run.programs[si] is not None:
+            run._share_scratch(shards[0])
             for r in range(R):
                 run.programs[si].run(shards[r])
     return shards

@@ -493,3 +493,6 @@ def test_sharded_run_loopback_large_shards(policy):
     ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
     assert float(np.max(np.abs(full - ref))) < 1e-10
     assert any(ph is not None for ph in run.seg_phys_out[:-1])
+    # the segment programs share one ping-pong scratch buffer
+    scratch = {id(pr._scratch) for pr in run.programs if pr is not None and pr.needs_scratch}
+    assert len(scratch) <= 1
