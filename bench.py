@@ -312,6 +312,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         # the first layout) from pinned host memory, runs all parts and
         # switches, and downloads its final shard; max over ranks
         run_e2e = ShardedRun(circuit, part, int(math.log2(world)), device=dev, basis_start=False)
+        run_e2e._scratch = getattr(run, "_scratch", None)  # one ping-pong scratch per rank, not two
         host_in = torch.zeros(1 << n_local, dtype=torch.complex128).pin_memory()
         if rank == 0:
             host_in[0] = 1.0
