@@ -559,22 +559,39 @@ struct SegRangeParams {
   int32_t nseg;
   int32_t nbits;
   int64_t begin, count;
+  int32_t kfast;       // segment index varies fastest across threads (segment bits among the low bits)
+  int32_t count_log;   // log2(count) when count is a power of two, else -1
 };
 
 template <typename C, bool PACK>
 __global__ void seg_range_kernel(const C* __restrict__ in, C* __restrict__ out, SegRangeParams p) {
   const uint64_t total = uint64_t(p.count) << p.nseg;
+  const uint64_t kmask = (uint64_t(1) << p.nseg) - 1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = i / uint64_t(p.count), m = i - k * uint64_t(p.count);
+    // thread order: (m, k) with k fastest when segment bits sit among the
+    // lowest bits (then neighbouring threads touch neighbouring amplitudes
+    // of the shard), else (k, m) with m fastest
+    uint64_t k, m;
+    if (p.kfast) {
+      k = i & kmask;
+      m = i >> p.nseg;
+    } else if (p.count_log >= 0) {
+      k = i >> p.count_log;
+      m = i & ((uint64_t(1) << p.count_log) - 1);
+    } else {
+      k = i / uint64_t(p.count);
+      m = i - k * uint64_t(p.count);
+    }
+    const uint64_t slot = k * uint64_t(p.count) + m;
     uint64_t idx = uint64_t(p.begin) + m;
     for (int b = 0; b < p.nseg; ++b) {  // insert segment bit b at seg_pos[b] (ascending)
       const int q = p.seg_pos[b];
       const uint64_t lo = idx & ((1ull << q) - 1);
       idx = ((idx ^ lo) << 1) | lo | (((k >> b) & 1ull) << q);
     }
-    if (PACK) out[i] = in[idx];
-    else out[idx] = in[i];
+    if (PACK) out[slot] = in[idx];
+    else out[idx] = in[slot];
   }
 }
 
@@ -586,6 +603,12 @@ cudaError_t launch_segments_range(bool pack, const void* in, void* out, int nbit
   p.begin = begin;
   p.count = count;
   for (int k = 0; k < nseg; ++k) p.seg_pos[k] = (int8_t)seg_pos[k];
+  p.kfast = (nseg > 0 && seg_pos[0] < (dtype == HS_C128 ? 3 : 4)) ? 1 : 0;
+  p.count_log = -1;
+  if (count > 0 && (count & (count - 1)) == 0) {
+    p.count_log = 0;
+    while ((int64_t(1) << p.count_log) < count) ++p.count_log;
+  }
   const uint64_t n = uint64_t(count) << nseg;
   uint64_t blocks = (n + 255) / 256;
   if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
