@@ -496,3 +496,24 @@ def test_sharded_run_loopback_large_shards(policy):
     # the segment programs share one ping-pong scratch buffer
     scratch = {id(pr._scratch) for pr in run.programs if pr is not None and pr.needs_scratch}
     assert len(scratch) <= 1
+
+
+def test_edge_case_circuits():
+    """Empty circuits, one qubit, SWAP-only circuits (no arithmetic: pure
+    relabels) and a single wide CCX, through the compiled path (n >= 20) and
+    the interpreter, against the oracle."""
+    from paper_2205_06973_b200.qasm import Circuit
+
+    def check(c, limit):
+        part = partition_dfs(build_dag(c), limit)
+        st = execute_hierarchical(c, part)
+        ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+        assert float(np.max(np.abs(st.to_numpy() - ref))) < 1e-12
+        return part.num_parts
+
+    assert check(Circuit(21, ()), 12) == 0
+    check(Circuit(1, (GateOp(GateKind.H, (0,)),)), 1)
+    swaps = tuple(GateOp(GateKind.SWAP, (a, b)) for a, b in [(0, 20), (3, 17), (20, 5), (1, 2), (19, 0)])
+    check(Circuit(21, (GateOp(GateKind.X, (0,)), GateOp(GateKind.H, (3,))) + swaps), 12)
+    check(Circuit(22, (GateOp(GateKind.X, (0,)), GateOp(GateKind.X, (21,)),
+                       GateOp(GateKind.CCX, (0, 21, 11)), GateOp(GateKind.SWAP, (11, 1)))), 3)
