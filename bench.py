@@ -260,19 +260,38 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         torch.distributed.barrier()
     clocks = ClockSampler(dev.index if dev.index is not None else 0)
     clocks.start()
-    start = torch.cuda.Event(enable_timing=True)
-    stop = torch.cuda.Event(enable_timing=True)
-    marks = []
+    # K timed steps: each step's initial state is prepared first (t_init,
+    # reported apart: the input is resident when the hot path starts), then
+    # all parts (and switches) run between two events on the launch stream
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
-    start.record(stream)
-    for _ in range(args.steps):
+    for e_init, e0, e1 in step_ev:
+        e_init.record(stream)
+        if not dist:
+            run.program.init_basis(state, 0)
+        elif rank == 0:
+            init_basis(state, 0)
+        else:
+            state.zero_()
+        e0.record(stream)
+        if dist:
+            run.run(state)
+        else:
+            run.program.run(state)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    total_ms = sum(e0.elapsed_time(e1) for _, e0, e1 in step_ev)
+    init_ms = sum(ei.elapsed_time(e0) for ei, e0, _ in step_ev) / args.steps
+    clk = clocks.stop()
+    # per-launch durations (events between launches) from further untimed steps
+    marks = []
+    for _ in range(min(args.steps, 3)):
         ev = []
         one_step(ev)
         marks.append(ev)
-    stop.record(stream)
     torch.cuda.synchronize()
-    total_ms = start.elapsed_time(stop)
-    clk = clocks.stop()
+    n_marked = len(marks)
     # per-launch durations of the part kernel (events between launches);
     # distributed: per segment ("parts") and per layout switch ("switch")
     durs, restore_ms, switch_ms, seg_ms = [], 0.0, 0.0, 0.0
@@ -297,7 +316,6 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
             else:
                 restore_ms += dj
         durs += per_part
-    # only the part kernels sit between the events when not distributed
     if dist:
         t = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -347,13 +365,14 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         # a caller's initial state arrives in natural order: the e2e program
         # is planned without an initial layout of its own
         run_e2e = HierarchicalRun(circuit, part, device=dev, options=args.plan_options, basis_start=False)
-        # two pinned host inputs / outputs alternate (the streams overlap step
-        # i+1's upload, step i's parts and step i-1's download)
+        # pinned host inputs / outputs alternate; three device buffers let
+        # the streams overlap step i+1's upload, step i's parts and step
+        # i-1's download
         host_in = [torch.zeros(1 << n, dtype=torch.complex128).pin_memory() for _ in range(2)]
         for h in host_in:
             h[0] = 1.0
         host_out = [torch.empty(1 << n, dtype=torch.complex128).pin_memory() for _ in range(2)]
-        bufs = [state, torch.empty_like(state)]
+        bufs = [state, torch.empty_like(state), torch.empty_like(state)]
 
         def e2e_steps(k):
             run_e2e.run_stream([host_in[i % 2] for i in range(k)], [host_out[i % 2] for i in range(k)],
@@ -375,7 +394,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
                "ms_per_step": e_ms, "h2d_bytes_per_step": (1 << n) * 16, "d2h_bytes_per_step": (1 << n) * 16,
                "path": "public API HierarchicalRun.run_stream: each step uploads an initial state from pinned host, "
                        "runs every part and downloads the final state; upload/parts/download of consecutive "
-                       "steps overlap on three streams"}
+                       "steps overlap on three streams over three device buffers"}
 
     info = ([run.program.info(i) for i in range(num_launches)] if not dist else run.part_infos())
     # FP64 roofline: issued FP64 pipe work of the part kernels vs a measured DFMA peak
@@ -386,7 +405,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     peak = ctypes.c_double()
     _native.check(_native.load().hs_fp64_peak(ctypes.byref(peak), stream.cuda_stream))
     fp64_instr = sum(i["fp64_instr_per_amp"] for i in info) * (1 << n_local)
-    part_ms = sum(durs) / args.steps if durs else (seg_ms / args.steps if dist else ms_step)
+    part_ms = sum(durs) / n_marked if durs else (seg_ms / n_marked if dist else ms_step)
     fp64 = {"bound_note": "random-circuit parts are FP64-bound, not HBM-bound (SURVEY.md 7.3)",
             "instr_per_step": fp64_instr, "achieved_tflops": 2 * fp64_instr / (part_ms / 1e3) / 1e12,
             "peak_tflops_measured": peak.value,
@@ -395,10 +414,11 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     return {
         "ms_step": ms_step, "value": value, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
         "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
-        "num_launches": num_launches, "restore_ms_per_step": restore_ms / args.steps, "fp64": fp64,
-        "comm": (dict(run.comm_summary(), switch_ms_per_step=switch_ms / args.steps,
-                      parts_ms_per_step=seg_ms / args.steps,
-                      nvlink_gbs_per_rank=(run.stats.total_bytes / world / (switch_ms / args.steps / 1e3) / 1e9
+        "num_launches": num_launches, "restore_ms_per_step": restore_ms / n_marked, "fp64": fp64,
+        "init_ms_per_step": init_ms,
+        "comm": (dict(run.comm_summary(), switch_ms_per_step=switch_ms / n_marked,
+                      parts_ms_per_step=seg_ms / n_marked,
+                      nvlink_gbs_per_rank=(run.stats.total_bytes / world / (switch_ms / n_marked / 1e3) / 1e9
                                            if switch_ms > 0 else None))
                  if dist else None),
     }
@@ -462,7 +482,9 @@ def main(argv=None):
         return 0
     peak, peak_kind = _peaks()
     durs = g["durations_ms"]
-    avg_ms = sum(durs) / len(durs) if durs else g["ms_step"] / g["num_parts"]
+    # average part-pass duration over the timed region: the timed part time
+    # less the gate-free layout launches (their share from the event pass)
+    avg_ms = (g["ms_step"] - g["restore_ms_per_step"]) / g["num_parts"]
     achieved = g["bytes_per_pass"] / (avg_ms / 1e3) / 1e9
     traffic = _traffic_from_profiles(args.config, args.strategy)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -470,6 +492,7 @@ def main(argv=None):
                 "kernel": "hs_part_kernel (one launch = one part-pass)",
                 "algorithmic_bytes_per_launch": g["bytes_per_pass"],
                 "avg_launch_ms": avg_ms,
+                "avg_launch_ms_event_pass": (sum(durs) / len(durs)) if durs else None,
                 "per_part_gbs": [g["bytes_per_pass"] / (d / 1e3) / 1e9 for d in durs[: g["num_parts"]]]}
     infos = g["info"]
     flops = sum(i["fp_ops_per_amp"] for i in infos) * (1 << g["n_local"])
@@ -492,6 +515,7 @@ def main(argv=None):
             "config": config, "roofline": roofline, "clocks": g["clocks"],
             "gpu_launches": args.steps * g["num_launches"] + (args.steps * g["e2e"]["launches_per_step"] if g["e2e"] else 0),
             "layout_restore_ms_per_step": g["restore_ms_per_step"],
+            "init_ms_per_step": g["init_ms_per_step"],
             "e2e": g["e2e"],
             "time_to_solution_ms": g["ms_step"],
             "fp64_flops_per_step_paper_count": flops,

@@ -567,8 +567,9 @@ class HierarchicalRun:
         """Simulate the circuit on a sequence of host states: ``inputs[i]``
         (pinned host tensors, natural order, e.g. many initial states) ->
         ``outputs[i]``. Uploads, part passes and downloads run on three
-        streams over two device buffers, so step i + 1's upload and step
-        i - 1's download overlap step i's part passes. Returns when the last
+        streams over three device buffers (by default), so step i + 1's
+        upload, step i's part passes and step i - 1's download all overlap
+        (with two buffers an upload waits for the download before it). Returns when the last
         download is queued (synchronize to read outputs). The program must
         accept natural-order input (``basis_start=False``)."""
         import torch
@@ -581,7 +582,7 @@ class HierarchicalRun:
         compute = stream or torch.cuda.current_stream(dev)
         if buffers is None:
             like = inputs[0]
-            buffers = [torch.empty(like.shape, dtype=self.program.dtype, device=dev) for _ in range(2)]
+            buffers = [torch.empty(like.shape, dtype=self.program.dtype, device=dev) for _ in range(3)]
         up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         loaded = [torch.cuda.Event() for _ in buffers]
         done = [torch.cuda.Event() for _ in buffers]
