@@ -482,18 +482,26 @@ def main(argv=None):
         return 0
     peak, peak_kind = _peaks()
     durs = g["durations_ms"]
-    # average part-pass duration over the timed region: the timed part time
-    # less the gate-free layout launches (their share from the event pass)
-    avg_ms = (g["ms_step"] - g["restore_ms_per_step"]) / g["num_parts"]
+    # average duration of a launch that carries gates over the timed region:
+    # the timed part time less the gate-free layout launches (their share
+    # from the event pass). Wide parts take several launches (sub-passes,
+    # regrouped across parts), so a launch is not always a part: the per
+    # part-pass figure (value's unit) is reported beside it.
+    gate_launches = (sum(1 for i in g["info"] if i["user_part"] >= 0) if world == 1 else g["num_parts"])
+    avg_ms = (g["ms_step"] - g["restore_ms_per_step"]) / max(1, gate_launches)
+    part_pass_ms = (g["ms_step"] - g["restore_ms_per_step"]) / g["num_parts"]
     achieved = g["bytes_per_pass"] / (avg_ms / 1e3) / 1e9
     traffic = _traffic_from_profiles(args.config, args.strategy)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "kernel": "hs_part_kernel (one launch = one part-pass)",
+                "kernel": "compiled part kernel (one launch = one pass over the state)",
                 "algorithmic_bytes_per_launch": g["bytes_per_pass"],
-                "avg_launch_ms": avg_ms,
+                "avg_launch_ms": avg_ms, "gate_launches_per_step": gate_launches,
+                "part_passes_per_step": g["num_parts"],
+                "effective_gbs_per_part_pass": g["bytes_per_pass"] / (part_pass_ms / 1e3) / 1e9,
                 "avg_launch_ms_event_pass": (sum(durs) / len(durs)) if durs else None,
-                "per_part_gbs": [g["bytes_per_pass"] / (d / 1e3) / 1e9 for d in durs[: g["num_parts"]]]}
+                "per_part_gbs": [g["bytes_per_pass"] / (d / 1e3) / 1e9 if d > 0 else None
+                                 for d in durs[: g["num_parts"]]]}
     infos = g["info"]
     flops = sum(i["fp_ops_per_amp"] for i in infos) * (1 << g["n_local"])
     # binding roofline per part: max(bytes / HBM peak, FP64
@@ -501,10 +509,9 @@ def main(argv=None):
     # measured part time
     fp_rate = g["fp64"]["peak_tflops_measured"] * 1e12 / 2  # instructions/s (FMA = 2 flops)
     bind_ms = 0.0
-    for p_ in range(g["num_parts"] if world == 1 else 0):
-        ins = sum(i["fp64_instr_per_amp"] for i in infos if i["user_part"] == p_) * (1 << g["n_local"])
+    for i in (infos if world == 1 else []):  # every launch is one pass over the state
+        ins = i["fp64_instr_per_amp"] * (1 << g["n_local"])
         bind_ms += max(g["bytes_per_pass"] / (peak * 1e9), ins / fp_rate if fp_rate else 0.0) * 1e3
-    bind_ms += sum(g["bytes_per_pass"] / (peak * 1e9) for i in infos if i["user_part"] < 0) * 1e3
     if world == 1:
         roofline["binding"] = {"what": "sum over launches of max(HBM bytes / peak, FP64 instructions / measured DFMA rate)",
                              "bound_ms_per_step": bind_ms, "measured_ms_per_step": g["ms_step"],

@@ -135,6 +135,15 @@ typedef struct {
  * (hs_program_final_layout) instead of restoring natural order, e.g. when a
  * layout switch that can pack from any layout follows */
 #define HS_PLAN_NO_RESTORE 0x100u
+/* wide parts (HS_PLAN_CLUSTER off): split each part on its own instead of
+ * regrouping the whole program's gate stream into tile-sized passes (the
+ * default when that takes fewer passes; a pass may then carry the end of
+ * one part and the start of the next) */
+#define HS_PLAN_PART_LOCAL 0x200u
+/* regroup the gate stream into tile-sized passes even when every part fits
+ * the tile (fewer launches than parts when consecutive parts together fit
+ * one tile; same results, launches report the part they mostly carry) */
+#define HS_PLAN_MERGE 0x400u
 #define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
 
 typedef struct hs_engine hs_engine;

@@ -814,16 +814,91 @@ namespace {
 // that shares a qubit with it); each round is one pass. The product of the
 // sub-parts' gates is the part's (gates only move past gates on disjoint
 // qubits). owner[j] = the caller's part of expanded part j.
+//
+// With `across` the same greedy runs over the whole program's gate stream
+// (every part's gates in part order, on storage positions): a pass may then
+// finish one part's gates and start the next part's, which the per-part
+// split cannot (c5_33, dfs k = 14: 25 -> 16 passes). A pass belongs to the
+// caller's part that contributes most of its gates (ties: the earlier one).
 int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
-                     std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates, std::vector<int>& owner,
-                     std::string& err) {
+                     bool across, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
+                     std::vector<int>& owner, std::string& err) {
+  struct Ref {
+    int part;
+    const hs_gate* g;
+    uint64_t mask;  // storage positions the gate touches
+  };
+  // one run of the greedy over `stream`; emits passes
+  auto greedy = [&](const std::vector<Ref>& stream) -> int {
+    std::vector<int> rem(stream.size());
+    for (size_t g = 0; g < stream.size(); ++g) rem[g] = (int)g;
+    while (!rem.empty()) {
+      uint64_t in = 0, blocked = 0;
+      std::vector<int> chosen, rest;
+      for (int g : rem) {
+        const Ref& r = stream[g];
+        const uint64_t u = in | r.mask;
+        if (!(r.mask & blocked) && r.mask && __builtin_popcountll(u) <= tile_max) {
+          in = u;
+          chosen.push_back(g);
+        } else {
+          blocked |= r.mask;
+          rest.push_back(g);
+        }
+      }
+      if (chosen.empty()) { err = "internal: wide-part split made no progress"; return HS_ERR_INVALID; }
+      hs_part q;
+      std::memset(&q, 0, sizeof(q));
+      int slot_of[64];
+      for (int b = 0; b < 64; ++b)  // staged positions stay ascending
+        if (in >> b & 1) { slot_of[b] = q.num_staged; q.staged[q.num_staged++] = b; }
+      q.gate_offset = (int32_t)xgates.size();
+      q.num_gates = (int32_t)chosen.size();
+      std::vector<int> votes(num_parts, 0);
+      for (int g : chosen) {
+        const Ref& r = stream[g];
+        hs_gate G = *r.g;
+        const hs_part& p = parts[r.part];
+        for (int a = 0; a < G.num_slots; ++a) G.slots[a] = slot_of[p.staged[G.slots[a]]];
+        xgates.push_back(G);
+        ++votes[r.part];
+      }
+      int best = stream[chosen[0]].part;
+      for (int i = 0; i < num_parts; ++i)
+        if (votes[i] > votes[best] || (votes[i] == votes[best] && i < best)) best = i;
+      xparts.push_back(q);
+      owner.push_back(best);
+      rem.swap(rest);
+    }
+    return HS_OK;
+  };
+  std::vector<Ref> all;
   for (int i = 0; i < num_parts; ++i) {
     const hs_part& p = parts[i];
     if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates) {
       err = "part " + std::to_string(i) + ": gate window outside the gate array";
       return HS_ERR_INVALID;
     }
+    if (p.num_staged < 0 || p.num_staged > HS_MAX_STAGED) { err = "part " + std::to_string(i) + ": bad width"; return HS_ERR_INVALID; }
+    for (int j = 0; j < p.num_staged; ++j)
+      if (p.staged[j] < 0 || p.staged[j] >= 64) { err = "staged position outside 0..63"; return HS_ERR_INVALID; }
     const hs_gate* pg = gates + p.gate_offset;
+    std::vector<Ref> own;
+    for (int g = 0; g < p.num_gates; ++g) {
+      const hs_gate& G = pg[g];
+      uint64_t m = 0;
+      if (G.num_slots < 1 || G.num_slots > 3) { err = "gate arity outside 1..3"; return HS_ERR_INVALID; }
+      for (int a = 0; a < G.num_slots; ++a) {
+        const int sl = G.slots[a];
+        if (sl < 0 || sl >= p.num_staged) { err = "gate slot outside the part"; return HS_ERR_INVALID; }
+        m |= 1ull << p.staged[sl];
+      }
+      own.push_back(Ref{i, &G, m});
+    }
+    if (across) {
+      all.insert(all.end(), own.begin(), own.end());
+      continue;
+    }
     if (p.num_staged <= tile_max) {
       hs_part q = p;
       q.gate_offset = (int32_t)xgates.size();
@@ -832,50 +907,9 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
       owner.push_back(i);
       continue;
     }
-    std::vector<int> rem(p.num_gates);
-    for (int g = 0; g < p.num_gates; ++g) rem[g] = g;
-    while (!rem.empty()) {
-      std::vector<char> in(p.num_staged, 0), blocked(p.num_staged, 0);
-      int used = 0;
-      std::vector<int> chosen, rest;
-      for (int g : rem) {
-        const hs_gate& G = pg[g];
-        bool ok = G.num_slots >= 1 && G.num_slots <= 3;
-        int extra = 0;
-        for (int a = 0; ok && a < G.num_slots; ++a) {
-          const int sl = G.slots[a];
-          if (sl < 0 || sl >= p.num_staged) { err = "gate slot outside the part"; return HS_ERR_INVALID; }
-          if (blocked[sl]) ok = false;
-          else if (!in[sl]) ++extra;
-        }
-        if (ok && used + extra <= tile_max) {
-          for (int a = 0; a < G.num_slots; ++a)
-            if (!in[G.slots[a]]) { in[G.slots[a]] = 1; ++used; }
-          chosen.push_back(g);
-        } else {
-          for (int a = 0; a < G.num_slots; ++a)
-            if (G.slots[a] >= 0 && G.slots[a] < p.num_staged) blocked[G.slots[a]] = 1;
-          rest.push_back(g);
-        }
-      }
-      if (chosen.empty()) { err = "internal: wide-part split made no progress"; return HS_ERR_INVALID; }
-      hs_part q;
-      std::memset(&q, 0, sizeof(q));
-      std::vector<int> slot_of(p.num_staged, -1);
-      for (int sl = 0; sl < p.num_staged; ++sl)  // staged positions stay ascending
-        if (in[sl]) { slot_of[sl] = q.num_staged; q.staged[q.num_staged++] = p.staged[sl]; }
-      q.gate_offset = (int32_t)xgates.size();
-      q.num_gates = (int32_t)chosen.size();
-      for (int g : chosen) {
-        hs_gate G = pg[g];
-        for (int a = 0; a < G.num_slots; ++a) G.slots[a] = slot_of[G.slots[a]];
-        xgates.push_back(G);
-      }
-      xparts.push_back(q);
-      owner.push_back(i);
-      rem.swap(rest);
-    }
+    if (int s = greedy(own)) return s;
   }
+  if (across) return greedy(all);
   return HS_OK;
 }
 
@@ -886,13 +920,22 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
                  std::vector<int32_t>* init_phys, const int32_t* given_init, std::vector<int32_t>* final_phys) {
   bool wide = false;
   for (int i = 0; i < num_parts; ++i) wide |= parts[i].num_staged > tile_max;
-  if (wide && !((options & HS_PLAN_CLUSTER) && (options & HS_PLAN_JIT))) {
+  if ((wide && !((options & HS_PLAN_CLUSTER) && (options & HS_PLAN_JIT))) || ((options & HS_PLAN_MERGE) && num_parts > 1)) {
     std::vector<hs_part> xp;
     std::vector<hs_gate> xg;
     std::vector<int> owner;
-    int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, xp, xg, owner, err);
+    int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, false, xp, xg, owner, err);
     if (s != HS_OK) return s;
-    s = plan_program(n_local, dtype, tile_max, options, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
+    if (!(options & HS_PLAN_PART_LOCAL)) {
+      // regroup the whole gate stream when that takes fewer passes
+      std::vector<hs_part> ap;
+      std::vector<hs_gate> ag;
+      std::vector<int> ao;
+      s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, true, ap, ag, ao, err);
+      if (s != HS_OK) return s;
+      if (ap.size() < xp.size()) { xp.swap(ap); xg.swap(ag); owner.swap(ao); }
+    }
+    s = plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
                      err, init_phys, given_init, final_phys);
     if (s != HS_OK) return s;
     for (auto& pl : plans)

@@ -313,3 +313,28 @@ def test_cluster_tile_parts(tmp_path, name, limit, dtype):
     assert res.returncode == 0, res.stderr[-3000:]
     spill = int(re.search(r"(\d+) bytes spill stores", res.stderr).group(1))
     assert spill <= 160, res.stderr  # per-tile addresses, outside the gate code
+
+
+@pytest.mark.parametrize("name,limit,tile", [("c2@16", 14, 12), ("c2@15", 13, 12), ("c4@14", 8, 10), ("c1@13", 6, 10)])
+def test_regrouped_passes_match_oracle(name, limit, tile):
+    """Wide parts regroup the whole gate stream into tile-sized passes (a pass
+    may end one part and start the next; default) unless HS_PLAN_PART_LOCAL;
+    HS_PLAN_MERGE regroups even parts that fit. Fewer or equal launches than
+    the per-part split, same amplitudes, in place and ping-pong."""
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), limit)
+    exes = [remap_part(c, p) for p in part.parts]
+    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    extra = 0x400 if limit <= tile else 0  # HS_PLAN_MERGE for parts that fit
+    for layout in (0, 8, 8 | 0x40):
+        local = emu.plan_program(_native, c.num_qubits, 0, tile, exes, options=5 | layout | 0x200)
+        merged = emu.plan_program(_native, c.num_qubits, 0, tile, exes, options=5 | layout | extra)
+        if layout == 0:  # no restore launches: one launch per pass
+            assert len(merged) <= len(local)
+            if limit <= tile:
+                assert len(local) == len(exes) and len(merged) < len(exes)
+        for launches in (local, merged):
+            psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
+            psi[0, 0] = 1
+            emu.run_program(psi, c.num_qubits, launches)
+            assert np.max(np.abs(psi[0] - want)) < 1e-12, (layout, len(launches))
