@@ -436,10 +436,16 @@ def main(argv=None):
     ap.add_argument("--cpu-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--plan-options", type=int, default=None,
+    ap.add_argument("--plan-add", type=lambda x: int(x, 0), default=0,
+                    help="HS_PLAN_* bits added to the engine defaults (e.g. 0x400 = HS_PLAN_MERGE)")
+    ap.add_argument("--plan-options", type=lambda x: int(x, 0), default=None,
                     help="planner option bits (HS_PLAN_*) of the single-GPU program (default: the engine "
                          "default + JIT + LAYOUT, chosen by state size)")
     args = ap.parse_args(argv)
+    if args.plan_add:
+        from paper_2205_06973_b200 import _native
+
+        _native._default_options |= args.plan_add
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
 
@@ -462,7 +468,7 @@ def main(argv=None):
               "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
               "state_bytes_per_gpu": (1 << (n - extra)) * 16,
               "l2_policy": "inputs larger than L2: the state (>= 1 GiB) exceeds the 126 MB L2",
-              "partition_seconds_host": round(t_part, 4), "parallelism": f"qubit-sharded x{world}" if world > 1 else "single GPU"}
+              "partition_seconds_host": round(t_part, 4), "plan_add": hex(args.plan_add), "parallelism": f"qubit-sharded x{world}" if world > 1 else "single GPU"}
 
     if args.impl == "reference":
         r = cpu_arm(args, cfg, circuit, part, t_part, args.steps, args.warmup)

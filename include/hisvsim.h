@@ -144,7 +144,7 @@ typedef struct {
  * the tile (fewer launches than parts when consecutive parts together fit
  * one tile; same results, launches report the part they mostly carry) */
 #define HS_PLAN_MERGE 0x400u
-#define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY)
+#define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY | HS_PLAN_MERGE)
 
 typedef struct hs_engine hs_engine;
 typedef struct hs_program hs_program;

@@ -91,6 +91,8 @@ struct LayoutIO {
   int32_t* phys_out = nullptr;        // updated for the tile's qubits
   const int32_t* next_use = nullptr;  // PRIORITY: parts until q is staged again
   const int32_t* target = nullptr;    // TARGET: wanted physical position of q
+  const int32_t* extra_first = nullptr;  // physical positions that fill the tile before the lowest free ones
+  int num_extra_first = 0;
   int mode = LAYOUT_KEEP;
 };
 

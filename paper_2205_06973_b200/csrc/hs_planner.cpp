@@ -352,8 +352,12 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   for (int j = 0; j < w; ++j) phy[j] = lay && lay->phys_in ? lay->phys_in[staged[j]] : staged[j];
   // tile = staged physical positions + lowest free physical positions
   std::vector<int> tile(phy);
+  for (int e = 0; lay && e < lay->num_extra_first && (int)tile.size() < T; ++e) {
+    const int p = lay->extra_first[e];
+    if (p >= 0 && p < n_local && std::find(tile.begin(), tile.end(), p) == tile.end()) tile.push_back(p);
+  }
   for (int p = 0; (int)tile.size() < T && p < n_local; ++p)
-    if (std::find(phy.begin(), phy.end(), p) == phy.end()) tile.push_back(p);
+    if (std::find(tile.begin(), tile.end(), p) == tile.end()) tile.push_back(p);
   std::sort(tile.begin(), tile.end());
   std::vector<int> tl(w);
   for (int j = 0; j < w; ++j) tl[j] = int(std::find(tile.begin(), tile.end(), phy[j]) - tile.begin());
@@ -997,14 +1001,26 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
   // among its own (coalesced stores); otherwise it writes a coalesced layout
   // and one gate-free out-of-place launch permutes into natural order
   const bool no_restore = (options & HS_PLAN_NO_RESTORE) != 0;
+  // The last part's tile takes the lowest logical qubits it does not stage
+  // as its extra bits; it writes natural order itself when those and its
+  // own cover qubits 0..hot-1 (stores in 2^hot-amplitude runs), else the
+  // gate-free launch follows.
   bool need_restore = false;
+  std::vector<int32_t> last_extra;  // logical qubits
   if (pp && !no_restore) {
     const hs_part& pl = parts[num_parts - 1];
-    for (int q = 0; q < hot; ++q) {
-      bool in = false;
-      for (int j = 0; j < pl.num_staged; ++j) in |= pl.staged[j] == q;
-      need_restore |= !in;
-    }
+    const int w = std::max(0, std::min(pl.num_staged, HS_MAX_STAGED));
+    const int T = std::min(std::max(tile_max, w), n_local);
+    std::vector<char> cov(n_local + 1, 0);
+    for (int j = 0; j < w; ++j)
+      if (pl.staged[j] >= 0 && pl.staged[j] < n_local) cov[pl.staged[j]] = 1;
+    for (int q = 0; q < n_local && w + (int)last_extra.size() < T; ++q)
+      if (!cov[q]) { last_extra.push_back(q); cov[q] = 1; }
+    int run = 0;
+    while (run < n_local && cov[run]) ++run;
+    // (measured: 64 B runs, final_run = 2, lose to the extra coalesced
+    // launch: c2 6.51 vs 5.74 ms, c3 119.1 vs 116.1 ms)
+    need_restore = run < std::min(hot, n_local);
   }
   const bool first_inplace = pp && ((num_parts + (need_restore ? 1 : 0)) % 2 == 1);
   int cur_buf = 0;
@@ -1023,8 +1039,12 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       lay.inv_in = inv.data();
       lay.phys_out = next.data();
       lay.mode = LAYOUT_OOP;
+      std::vector<int32_t> extra_phys;
       if (i + 1 == num_parts && !need_restore && !no_restore) {
         for (int q = 0; q < n_local; ++q) tgt[q] = q;  // the last part writes natural order
+        for (int32_t q : last_extra) extra_phys.push_back(phys[q]);
+        lay.extra_first = extra_phys.data();
+        lay.num_extra_first = (int)extra_phys.size();
       } else {
         // the next layout: this tile's qubits that the next part stages go
         // to the lowest positions (coalesced stores now, coalesced loads

@@ -223,7 +223,9 @@ class ShardedRun:
                 pr.share_scratch(sc)
 
     def part_infos(self):
-        return [pr.info(i) for pr in self.programs if pr is not None for i in range(pr.num_parts)]
+        """hs_part_info of every launch of every segment program (wide parts
+        take several launches; gate-free layout launches report user_part -1)."""
+        return [pr.info(i) for pr in self.programs if pr is not None for i in range(pr.num_launches)]
 
     def comm_summary(self) -> dict:
         return {"switches": self.stats.num_switches, "bytes_remote_total": self.stats.total_bytes,

@@ -36,8 +36,13 @@ def _dev_err(state, ref):
     return float(np.max(np.abs(state.to_numpy() - ref)))
 
 
-@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
-def test_corpus_every_partition_matches_reference(golden, dtype):
+@pytest.mark.parametrize("dtype,merge", [("complex128", True), ("complex64", True), ("complex128", False)])
+def test_corpus_every_partition_matches_reference(golden, dtype, merge, monkeypatch):
+    """Every corpus circuit under every reference partition; with the
+    default HS_PLAN_MERGE (consecutive parts that fit one tile share a pass)
+    and without it (one pass per part)."""
+    if not merge:
+        monkeypatch.setattr(_native, "_default_options", _native.default_options() & ~_native.HS_PLAN_MERGE)
     docs, states = golden.json("corpus"), golden.npz("corpus")
     worst = 0.0
     for i, doc in enumerate(docs):
@@ -241,7 +246,7 @@ def test_compiled_parts_match_reference(golden, dtype):
         part = partition_of(doc["partitions"][key])
         exes = [remap_part(c, p) for p in part.parts]
         prog = PartProgram(c.num_qubits, exes, dtype=dtype, options=opts)
-        assert prog.jit_error == "" and all(prog.info(j)["compiled"] for j in range(prog.num_parts))
+        assert prog.jit_error == "" and all(prog.info(j)["compiled"] for j in range(prog.num_launches))
         st = from_numpy(np.eye(1, 1 << c.num_qubits, 0).ravel().astype(np.complex128), dtype=dtype)
         prog.run(st.data)
         assert _dev_err(st, states[f"c{i}"]) < TOL[dtype]
@@ -256,7 +261,7 @@ def test_compiled_full_size_c2_matches_c_oracle():
     c = configs.build("c2")
     part = partition_dfs(build_dag(c), 12)
     run = HierarchicalRun(c, part)
-    assert all(run.program.info(j)["compiled"] for j in range(run.program.num_parts))
+    assert all(run.program.info(j)["compiled"] for j in range(run.program.num_launches))
     from paper_2205_06973_b200.statevec import zero_state
 
     st = zero_state(26)
@@ -434,15 +439,16 @@ def test_run_stream_many_initial_states():
 
 @pytest.mark.parametrize("extra,dtype", [("layout", "complex128"), ("pingpong", "complex128"),
                                          ("pingpong_init", "complex128"), ("cluster", "complex128"),
-                                         ("pingpong_init", "complex64")])
+                                         ("pingpong_init", "complex64"), ("merged", "complex128")])
 def test_corpus_through_every_compiled_path(golden, extra, dtype):
     """Every corpus circuit and partition (all gate kinds, controls on thread
     and register bits, SWAPs, tiny states where a team is a few threads)
     through the compiled kernels with the layout machinery switched on."""
     from paper_2205_06973_b200.hier import PartProgram
 
-    base = _native.default_options() | _native.HS_PLAN_JIT
-    opts = {"layout": base | _native.HS_PLAN_LAYOUT,
+    base = (_native.default_options() & ~_native.HS_PLAN_MERGE) | _native.HS_PLAN_JIT  # one pass per part
+    opts = {"merged": base | _native.HS_PLAN_MERGE | _native.HS_PLAN_LAYOUT | _native.HS_PLAN_PINGPONG,
+            "layout": base | _native.HS_PLAN_LAYOUT,
             "pingpong": base | _native.HS_PLAN_LAYOUT | _native.HS_PLAN_PINGPONG,
             "pingpong_init": base | _native.HS_PLAN_LAYOUT | _native.HS_PLAN_PINGPONG | _native.HS_PLAN_INIT_LAYOUT,
             "cluster": base | _native.HS_PLAN_CLUSTER}[extra]
