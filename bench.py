@@ -46,16 +46,17 @@ def _peaks():
 def _traffic_from_profiles(config: str, strategy: str):
     """Per-launch DRAM bytes of the part kernel from the committed ncu
     summary of this workload (profiles/*_ncu_summary.json), else None."""
-    files = sorted((ROOT / "profiles").glob("*ncu_summary.json"), reverse=True)
-    files.sort(key=lambda f: "final" not in f.name)  # the latest capture of this round first
-    for f in files:
+    best = None  # the latest capture: highest capture_seq, else a "final" one
+    for f in sorted((ROOT / "profiles").glob("*ncu_summary.json")):
         try:
             d = json.loads(f.read_text())
         except Exception:
             continue
         if d.get("workload") == f"{config}/{strategy}" and d.get("dram_bytes_per_launch"):
-            return float(d["dram_bytes_per_launch"])
-    return None
+            key = (int(d.get("capture_seq", 1 if "final" in f.name else 0)), f.name)
+            if best is None or key > best[0]:
+                best = (key, float(d["dram_bytes_per_launch"]))
+    return best[1] if best else None
 
 
 class ClockSampler:

@@ -312,7 +312,7 @@ def test_cluster_tile_parts(tmp_path, name, limit, dtype):
         launches = emu.plan_program(_native, c.num_qubits, dtype, tile, exes, options=opts)
         assert max(int(l["cluster_log"]) for l, _ in launches) == 0
         assert max(int(l["T"]) for l, _ in launches) <= tile
-        assert sum(1 for l, _ in launches) > len(exes)
+        assert sum(1 for l, _ in launches) >= len(exes)  # sub-passes (regrouped across parts)
         psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
         psi[0, 0] = 1
         emu.run_program(psi, c.num_qubits, launches)
