@@ -979,7 +979,9 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
                  std::vector<int32_t>* init_phys, const int32_t* given_init, std::vector<int32_t>* final_phys) {
   bool wide = false;
   for (int i = 0; i < num_parts; ++i) wide |= parts[i].num_staged > tile_max;
-  if ((wide && !((options & HS_PLAN_CLUSTER) && (options & HS_PLAN_JIT))) || ((options & HS_PLAN_MERGE) && num_parts > 1)) {
+  // (cluster tiles run wide parts as one pass each: no regrouping then)
+  const bool cluster = (options & HS_PLAN_CLUSTER) && (options & HS_PLAN_JIT);
+  if (wide ? !cluster : ((options & HS_PLAN_MERGE) && num_parts > 1)) {
     std::vector<hs_part> xp;
     std::vector<hs_gate> xg;
     std::vector<int> owner;
