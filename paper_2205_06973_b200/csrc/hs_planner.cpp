@@ -407,13 +407,31 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   std::vector<int> R;
   double flops = 0, fp64 = 0;
   int phases = 0;
+  // A diagonal gate is "mixed" in a phase when its locations (target,
+  // parity partner, controls) are partly register and partly thread bits:
+  // compiled kernels fold register-only runs into constants and thread-only
+  // runs into one scalar per thread, but apply a mixed one as its own complex
+  // multiply per amplitude (QAOA / TFIM parity diagonals: up to half a part's
+  // FP64 work).
+  auto diag_mixed = [&](const Gate& G, const std::vector<int>& lo, uint32_t regs) {
+    int in = 0, all = 0;
+    auto see = [&](int b) { ++all; in += (regs >> lo[b]) & 1; };
+    see(G.tgt);
+    if (G.par >= 0) see(G.par);
+    for (int a = 0; a < G.nctl; ++a) see(G.ctl[a]);
+    return in > 0 && in < all;
+  };
   // How many non-diagonal gates a phase would take with register locations
-  // restricted to `allow` (a mask; ~0u = first come, up to RB of them).
-  auto phase_yield = [&](uint32_t allow) {
+  // restricted to `allow` (a mask; ~0u = first come, up to RB of them), and
+  // how many mixed diagonals it would apply. With `defer` (allow an exact
+  // register set) mixed diagonals are left for a later phase.
+  struct Yield { int taken, mixed; };
+  auto phase_yield = [&](uint32_t allow, bool defer) {
     std::vector<char> dn(done);
     std::vector<int> lo(loc_of);
-    int taken = 0, nR = 0;
+    int taken = 0, nR = 0, mixed = 0;
     uint32_t Rm = 0;
+    const bool exact = __builtin_popcount(allow) == RB;
     for (;;) {
       bool progress = false;
       uint32_t blk_nd = 0, blk_d = 0;
@@ -422,7 +440,11 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         const Gate& G = gs[g];
         if ((G.nd & (blk_nd | blk_d)) || (G.d & blk_nd)) { blk_nd |= G.nd; blk_d |= G.d; continue; }
         bool ok = G.cls == C_DIAG || G.cls == C_SWAP;
-        if (!ok) {
+        if (G.cls == C_DIAG && exact && diag_mixed(G, lo, allow)) {
+          if (defer) ok = false;
+          else ++mixed;
+        }
+        if (!ok && G.cls != C_DIAG) {
           const int L = lo[G.tgt];
           if (Rm >> L & 1) ok = true;
           else if (nR < RB && (allow >> L & 1)) { Rm |= 1u << L; ++nR; ok = true; }
@@ -435,20 +457,33 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       }
       if (!progress) break;
     }
-    return taken;
+    return Yield{taken, mixed};
   };
   while (remaining > 0) {
     R.clear();
     // compiled parts pay a shared-memory exchange per phase: pick the
     // register locations that let the most gates into this phase (all
-    // RB-subsets of the tile), not just the first targets met
+    // RB-subsets of the tile), not just the first targets met; among equals
+    // the one applying the fewest mixed diagonals, deferring them to a later
+    // phase when that costs this phase no gate
     uint32_t allow = ~0u;
+    bool defer = false;
     if ((options & HS_PLAN_JIT) && T <= 16) {
-      int best = phase_yield(~0u);
+      Yield best = phase_yield(~0u, false);
+      best.mixed = 1 << 30;  // first come: mixed count unknown, any exact set with as many gates wins
       for (uint32_t m = 0; m < (1u << T); ++m) {
         if (__builtin_popcount(m) != RB) continue;
-        const int y = phase_yield(m);
-        if (y > best) { best = y; allow = m; }
+        Yield y = phase_yield(m, false);
+        bool d = false;
+        if (y.mixed > 0 && y.taken > 0) {
+          const Yield yd = phase_yield(m, true);
+          if (yd.taken == y.taken) { y = yd; d = true; }
+        }
+        if (y.taken > best.taken || (y.taken == best.taken && y.mixed < best.mixed)) {
+          best = y;
+          allow = m;
+          defer = d;
+        }
       }
     }
     std::vector<Rec> recs;
@@ -460,7 +495,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         Gate& G = gs[g];
         if ((G.nd & (blk_nd | blk_d)) || (G.d & blk_nd)) { blk_nd |= G.nd; blk_d |= G.d; continue; }
         bool ok = false;
-        if (G.cls == C_DIAG || G.cls == C_SWAP) ok = true;
+        if (G.cls == C_DIAG || G.cls == C_SWAP) ok = !(G.cls == C_DIAG && defer && diag_mixed(G, loc_of, allow));
         else {
           int L = loc_of[G.tgt];
           if (std::find(R.begin(), R.end(), L) != R.end()) ok = true;
@@ -485,6 +520,10 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       if (!progress) break;
     }
     if (recs.empty()) continue;  // only relabels
+    // the rest of the chosen register set first (the mixed-diagonal choice
+    // above assumed it), then the lowest locations
+    for (int L = 0; allow != ~0u && L < T && (int)R.size() < RB; ++L)
+      if ((allow >> L & 1) && std::find(R.begin(), R.end(), L) == R.end()) R.push_back(L);
     for (int L = 0; (int)R.size() < RB; ++L)
       if (std::find(R.begin(), R.end(), L) == R.end()) R.push_back(L);
     Instr ph;
@@ -832,9 +871,19 @@ namespace {
 // contributes most of its gates (ties: the earlier one).
 enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER };
 
+// Cost of a pass sequence in units of one coalesced pass: a full-width pass
+// that shares fewer than 3 qubits with the pass before it cannot find its
+// qubits on the lowest storage positions (the previous pass could only move
+// its own tile's qubits there), so its reads run in short pieces - measured
+// ~2x the time of a coalesced pass (c3: 12.7 vs 5.8 ms, ncu r01s3).
+double pass_cost(uint64_t used, uint64_t prev, int tile_max) {
+  const bool full = __builtin_popcountll(used) > tile_max - 3;
+  return (prev && full && __builtin_popcountll(used & prev) < 3) ? 2.0 : 1.0;
+}
+
 int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
                      Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
-                     std::vector<int>& owner, std::string& err) {
+                     std::vector<int>& owner, double* cost, std::string& err) {
   struct Ref {
     int part;
     const hs_gate* g;
@@ -856,6 +905,29 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
       }
     }
     return n;
+  };
+  // frontier growth from `in`: add the qubits of the frontier gate that make
+  // the most gates runnable per added qubit, until full or nothing gains
+  auto grow = [&](const std::vector<Ref>& stream, const std::vector<int>& rem, uint64_t in) -> uint64_t {
+    for (;;) {
+      const int base = runnable(stream, rem, in, nullptr);
+      uint64_t blocked = 0, best_add = 0;
+      double best_gain = 0.0;
+      std::vector<uint64_t> seen;
+      for (int g : rem) {
+        const uint64_t m = stream[g].mask;
+        if (m & blocked) continue;
+        blocked |= m;
+        const uint64_t add = m & ~in;
+        if (!add || __builtin_popcountll(in | add) > tile_max) continue;
+        if (std::find(seen.begin(), seen.end(), add) != seen.end()) continue;
+        seen.push_back(add);
+        const double gain = double(runnable(stream, rem, in | add, nullptr) - base) / __builtin_popcountll(add);
+        if (gain > best_gain) { best_gain = gain; best_add = add; }
+      }
+      if (!best_add) return in;
+      in |= best_add;
+    }
   };
   auto emit = [&](const std::vector<Ref>& stream, const std::vector<int>& chosen, uint64_t in) {
     hs_part q;
@@ -880,45 +952,51 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
     xparts.push_back(q);
     owner.push_back(best);
   };
+  uint64_t prev = 0;  // storage positions of the previous pass
+  double total = 0.0;
   // group `stream` into passes and emit them
   auto group = [&](const std::vector<Ref>& stream, bool frontier) -> int {
     std::vector<int> rem(stream.size());
     for (size_t g = 0; g < stream.size(); ++g) rem[g] = (int)g;
     while (!rem.empty()) {
-      uint64_t in = 0;
+      std::vector<int> chosen;
+      uint64_t used = 0;
       if (!frontier) {
-        uint64_t blocked = 0;
+        uint64_t in = 0, blocked = 0;
         for (int g : rem) {
           const uint64_t m = stream[g].mask, u = in | m;
           if (!(m & blocked) && __builtin_popcountll(u) <= tile_max) in = u;
           else blocked |= m;
         }
+        runnable(stream, rem, in, &chosen);
+        for (int g : chosen) used |= stream[g].mask;
       } else {
-        for (;;) {
-          const int base = runnable(stream, rem, in, nullptr);
-          uint64_t blocked = 0, best_add = 0;
-          double best_gain = 0.0;
-          std::vector<uint64_t> seen;
-          for (int g : rem) {
-            const uint64_t m = stream[g].mask;
-            if (m & blocked) continue;
-            blocked |= m;
-            const uint64_t add = m & ~in;
-            if (!add || __builtin_popcountll(in | add) > tile_max) continue;
-            if (std::find(seen.begin(), seen.end(), add) != seen.end()) continue;
-            seen.push_back(add);
-            const double gain = double(runnable(stream, rem, in | add, nullptr) - base) / __builtin_popcountll(add);
-            if (gain > best_gain) { best_gain = gain; best_add = add; }
-          }
-          if (!best_add) break;
-          in |= best_add;
+        // candidates: plain growth, and growth seeded with the 1-3 previous
+        // pass qubits that run the most gates on their own (they stay in
+        // the pass, so its reads find them on the low positions); keep the
+        // most gates per unit of pass_cost
+        std::vector<std::pair<int, uint64_t>> solo;
+        for (int b = 0; b < 64; ++b)
+          if (prev >> b & 1) solo.push_back({runnable(stream, rem, 1ull << b, nullptr), b});
+        std::stable_sort(solo.begin(), solo.end(), [](const std::pair<int, uint64_t>& x,
+                                                      const std::pair<int, uint64_t>& y) { return x.first > y.first; });
+        double best = -1.0;
+        for (int seeds = 0; seeds <= 3 && seeds <= (int)solo.size(); ++seeds) {
+          uint64_t seed = 0;
+          for (int k = 0; k < seeds; ++k) seed |= 1ull << solo[k].second;
+          const uint64_t in = grow(stream, rem, seed);
+          std::vector<int> took;
+          runnable(stream, rem, in, &took);
+          if (took.empty()) continue;
+          uint64_t u = seed;
+          for (int g : took) u |= stream[g].mask;
+          const double score = double(took.size()) / pass_cost(u, prev, tile_max);
+          if (score > best) { best = score; chosen.swap(took); used = u; }
         }
       }
-      std::vector<int> chosen;
-      runnable(stream, rem, in, &chosen);
       if (chosen.empty()) { err = "internal: pass grouping made no progress"; return HS_ERR_INVALID; }
-      uint64_t used = 0;  // the pass stages only the qubits its gates touch
-      for (int g : chosen) used |= stream[g].mask;
+      total += pass_cost(used, prev, tile_max);
+      prev = used;
       emit(stream, chosen, used);
       std::vector<int> rest;
       rest.reserve(rem.size() - chosen.size());
@@ -964,11 +1042,18 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
       xgates.insert(xgates.end(), pg, pg + p.num_gates);
       xparts.push_back(q);
       owner.push_back(i);
+      uint64_t u = 0;
+      for (int j = 0; j < p.num_staged; ++j) u |= 1ull << p.staged[j];
+      total += pass_cost(u, prev, tile_max);
+      prev = u;
       continue;
     }
     if (int s = group(own, false)) return s;
   }
-  if (mode != GROUP_PER_PART) return group(all, mode == GROUP_FRONTIER);
+  if (mode != GROUP_PER_PART) {
+    if (int s = group(all, mode == GROUP_FRONTIER)) return s;
+  }
+  if (cost) *cost = total;
   return HS_OK;
 }
 
@@ -985,17 +1070,19 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     std::vector<hs_part> xp;
     std::vector<hs_gate> xg;
     std::vector<int> owner;
-    int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, err);
+    double cost = 0.0;
+    int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
     if (s != HS_OK) return s;
     if (!(options & HS_PLAN_PART_LOCAL)) {
-      // regroup the whole gate stream when that takes fewer passes
+      // regroup the whole gate stream when that costs fewer coalesced passes
       for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER}) {
         std::vector<hs_part> ap;
         std::vector<hs_gate> ag;
         std::vector<int> ao;
-        s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, err);
+        double c = 0.0;
+        s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
-        if (ap.size() < xp.size()) { xp.swap(ap); xg.swap(ag); owner.swap(ao); }
+        if (c < cost) { xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c; }
       }
     }
     s = plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
