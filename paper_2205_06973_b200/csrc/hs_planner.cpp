@@ -869,7 +869,7 @@ namespace {
 // the set and that no gate left behind precedes (c4, dfs k = 12: 137 parts
 // -> 44 passes; c3 17 -> 14). A pass belongs to the caller's part that
 // contributes most of its gates (ties: the earlier one).
-enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER };
+enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED };
 
 // Cost of a pass sequence in units of one coalesced pass: a full-width pass
 // that shares fewer than 3 qubits with the pass before it cannot find its
@@ -955,7 +955,7 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
   uint64_t prev = 0;  // storage positions of the previous pass
   double total = 0.0;
   // group `stream` into passes and emit them
-  auto group = [&](const std::vector<Ref>& stream, bool frontier) -> int {
+  auto group = [&](const std::vector<Ref>& stream, bool frontier, bool seeded) -> int {
     std::vector<int> rem(stream.size());
     for (size_t g = 0; g < stream.size(); ++g) rem[g] = (int)g;
     while (!rem.empty()) {
@@ -981,7 +981,7 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
         std::stable_sort(solo.begin(), solo.end(), [](const std::pair<int, uint64_t>& x,
                                                       const std::pair<int, uint64_t>& y) { return x.first > y.first; });
         double best = -1.0;
-        for (int seeds = 0; seeds <= 3 && seeds <= (int)solo.size(); ++seeds) {
+        for (int seeds = 0; seeds <= (seeded ? 3 : 0) && seeds <= (int)solo.size(); ++seeds) {
           uint64_t seed = 0;
           for (int k = 0; k < seeds; ++k) seed |= 1ull << solo[k].second;
           const uint64_t in = grow(stream, rem, seed);
@@ -1048,10 +1048,10 @@ int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs
       prev = u;
       continue;
     }
-    if (int s = group(own, false)) return s;
+    if (int s = group(own, false, false)) return s;
   }
   if (mode != GROUP_PER_PART) {
-    if (int s = group(all, mode == GROUP_FRONTIER)) return s;
+    if (int s = group(all, mode != GROUP_ACROSS, mode == GROUP_FRONTIER_SEEDED)) return s;
   }
   if (cost) *cost = total;
   return HS_OK;
@@ -1074,15 +1074,23 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
     if (s != HS_OK) return s;
     if (!(options & HS_PLAN_PART_LOCAL)) {
-      // regroup the whole gate stream when that costs fewer coalesced passes
-      for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER}) {
+      // regroup the whole gate stream when that takes fewer passes; among
+      // regroupings with as few passes, the lowest pass_cost. (Measured on
+      // one B200: c2 keeps its 9 parts - a 9-pass regrouping with better
+      // coalescing ran 6.00 vs 5.71 ms; c3's seeded frontier 105 vs 110 ms;
+      // c5_33's unseeded frontier, 15 passes, 1224 vs 1273 ms for 16.)
+      bool regrouped = false;
+      for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED}) {
         std::vector<hs_part> ap;
         std::vector<hs_gate> ag;
         std::vector<int> ao;
         double c = 0.0;
         s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
-        if (c < cost) { xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c; }
+        if (ap.size() < xp.size() || (regrouped && ap.size() == xp.size() && c < cost)) {
+          xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c;
+          regrouped = true;
+        }
       }
     }
     s = plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
