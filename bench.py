@@ -458,10 +458,13 @@ def main(argv=None):
         if args.impl == "reference":
             if rank != 0:
                 return 0
-            world = 1
         else:
             tdist.init_process_group("nccl")
+    # weak scaling: n + log2 N qubits (the reference arm times the same
+    # workload on rank 0's host cores)
     extra = int(math.log2(world)) if world > 1 else 0
+    if args.impl == "reference":
+        world = 1
     cfg, circuit, part, t_part = build_workload(args.config, args.strategy, extra, args.limit)
     n = circuit.num_qubits
     config = {"workload": f"{args.config}: {cfg.description}" + (f", scaled to {n} qubits" if extra else ""),
@@ -469,7 +472,8 @@ def main(argv=None):
               "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
               "state_bytes_per_gpu": (1 << (n - extra)) * 16,
               "l2_policy": "inputs larger than L2: the state (>= 1 GiB) exceeds the 126 MB L2",
-              "partition_seconds_host": round(t_part, 4), "plan_add": hex(args.plan_add), "parallelism": f"qubit-sharded x{world}" if world > 1 else "single GPU"}
+              "partition_seconds_host": round(t_part, 4), "plan_add": hex(args.plan_add), "parallelism": (f"qubit-sharded x{world}" if world > 1 else "single GPU") if args.impl != "reference"
+              else f"host CPU threads (rank 0 of {args.gpus})"}
 
     if args.impl == "reference":
         r = cpu_arm(args, cfg, circuit, part, t_part, args.steps, args.warmup)
