@@ -296,6 +296,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     # per-launch durations of the part kernel (events between launches);
     # distributed: per segment ("parts") and per layout switch ("switch")
     durs, restore_ms, switch_ms, seg_ms = [], 0.0, 0.0, 0.0
+    launch_ms = []  # per launch, per marked step
     for ev in marks:
         if dist:
             for i in range(1, len(ev)):
@@ -307,6 +308,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
                     seg_ms += prev.elapsed_time(e)
             continue
         d = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)]
+        launch_ms.append(d)
         # a launch belongs to a caller's part (wide parts may take several
         # sub-pass launches) or is a gate-free layout launch (user_part -1)
         per_part = [0.0] * num_parts
@@ -414,6 +416,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
             "part_kernel_ms_per_step": part_ms}
     return {
         "ms_step": ms_step, "value": value, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
+        "launch_ms": [sum(c) / len(c) for c in zip(*launch_ms)] if launch_ms else [],
         "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
         "num_launches": num_launches, "restore_ms_per_step": restore_ms / n_marked, "fp64": fp64,
         "init_ms_per_step": init_ms,
@@ -512,7 +515,9 @@ def main(argv=None):
                 "effective_gbs_per_part_pass": g["bytes_per_pass"] / (part_pass_ms / 1e3) / 1e9,
                 "avg_launch_ms_event_pass": (sum(durs) / len(durs)) if durs else None,
                 "per_part_gbs": [g["bytes_per_pass"] / (d / 1e3) / 1e9 if d > 0 else None
-                                 for d in durs[: g["num_parts"]]]}
+                                 for d in durs[: g["num_parts"]]],
+                "per_launch_ms": [round(x, 4) for x in g["launch_ms"]],
+                "per_launch_gbs": [round(g["bytes_per_pass"] / (x / 1e3) / 1e9, 1) for x in g["launch_ms"] if x > 0]}
     infos = g["info"]
     flops = sum(i["fp_ops_per_amp"] for i in infos) * (1 << g["n_local"])
     # binding roofline per part: max(bytes / HBM peak, FP64
