@@ -528,3 +528,73 @@ def test_edge_case_circuits():
     check(Circuit(21, (GateOp(GateKind.X, (0,)), GateOp(GateKind.H, (3,))) + swaps), 12)
     check(Circuit(22, (GateOp(GateKind.X, (0,)), GateOp(GateKind.X, (21,)),
                        GateOp(GateKind.CCX, (0, 21, 11)), GateOp(GateKind.SWAP, (11, 1)))), 3)
+
+
+def _inverse_appended(c):
+    """The circuit followed by its inverse (reversed ops, each inverted within
+    the reference gate set): the product is the identity, so a basis start
+    must come back exactly - a size-independent check at full config sizes."""
+    from paper_2205_06973_b200.qasm import Circuit
+
+    swap = {GateKind.S: GateKind.SDG, GateKind.SDG: GateKind.S, GateKind.T: GateKind.TDG, GateKind.TDG: GateKind.T}
+    angle = {GateKind.RX, GateKind.RY, GateKind.RZ, GateKind.U1, GateKind.CRZ, GateKind.CRY}
+    inv = []
+    for op in reversed(c.ops):
+        if op.kind in swap:
+            inv.append(GateOp(swap[op.kind], op.qubits, ()))
+        elif op.kind in angle:
+            inv.append(GateOp(op.kind, op.qubits, (-op.params[0],)))
+        elif op.kind == GateKind.U3:  # U3(t, p, l)^-1 = U3(-t, -l, -p)
+            t, p, l = op.params
+            inv.append(GateOp(op.kind, op.qubits, (-t, -l, -p)))
+        else:  # H, X, Y, Z, CX, CZ, SWAP, CCX are their own inverses
+            inv.append(op)
+    return Circuit(c.num_qubits, tuple(c.ops) + tuple(inv))
+
+
+def _basis_error(state, index):
+    """max |psi - e_index| over the device state, in chunks (33-qubit states
+    leave no room for a full-size temporary)."""
+    d = state.data
+    worst = abs(complex(d[index].item()) - 1.0)
+    step = 1 << 26
+    for s in range(0, d.numel(), step):
+        a = d[s:s + step].abs()
+        if s <= index < s + step:
+            a[index - s] = 0
+        worst = max(worst, float(a.max()))
+    return worst
+
+
+@pytest.mark.parametrize("name,limit", [("c3", 12), ("c4", 12), ("c5_33", 14)])
+def test_full_size_circuit_then_inverse_returns_to_basis(name, limit):
+    """BASELINE configs at their full size (30 / 33 / 33 qubits: 16 / 128 /
+    128 GiB, the last two in place) run forward and back through the engine's
+    planned passes: the state must return to |0..0> within 1e-10."""
+    c = _inverse_appended(configs.build(name))
+    part = partition_dfs(build_dag(c), limit)
+    st = execute_hierarchical(c, part)
+    torch.cuda.synchronize()
+    assert _basis_error(st, 0) < 1e-10
+
+
+def test_bv30_known_answer():
+    """30-qubit Bernstein-Vazirani (secret on the odd data qubits 1..27,
+    ancilla 29 prepared in |->): the final state is exactly
+    (|s> - |s + 2^29>) / sqrt(2) with s = 0xAAAAAAA, a 16 GiB known answer
+    that needs no CPU oracle."""
+    from paper_2205_06973_b200.qasm import Circuit
+
+    n, anc, s = 30, 29, 0xAAAAAAA
+    ops = [GateOp(GateKind.X, (anc,), ())] + [GateOp(GateKind.H, (q,), ()) for q in range(n)]
+    ops += [GateOp(GateKind.CX, (q, anc), ()) for q in range(anc) if s >> q & 1]
+    ops += [GateOp(GateKind.H, (q,), ()) for q in range(anc)]
+    c = Circuit(n, tuple(ops))
+    for strategy in (partition_dfs, partition_nat):
+        st = execute_hierarchical(c, strategy(build_dag(c), 12))
+        d = st.data
+        r = 2 ** -0.5
+        assert abs(complex(d[s].item()) - r) < 1e-12 and abs(complex(d[s + (1 << anc)].item()) + r) < 1e-12
+        d[s] = 0
+        d[s + (1 << anc)] = 0
+        assert float(d.abs().max()) < 1e-12
