@@ -255,7 +255,9 @@ class PartProgram:
                 # when a scratch copy of the state fits next to it (counted
                 # as if the state were not allocated yet)
                 amp = 16 if self.dtype == torch.complex128 else 8
-                free, _ = torch.cuda.mem_get_info(self.device)
+                from .statevec import free_bytes
+
+                free = free_bytes(self.device)
                 if 2 * (amp << n_local) + PINGPONG_HEADROOM <= free:
                     options |= _native.HS_PLAN_PINGPONG
         if init_layout is not None and tuple(init_layout) != tuple(range(n_local)):

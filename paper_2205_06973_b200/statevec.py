@@ -173,6 +173,14 @@ def max_qubits_cap(max_qubits: int | None = None) -> int:
     return min(max_qubits, HARD_MAX_QUBITS)
 
 
+def free_bytes(device) -> int:
+    """Free HBM on ``device`` as allocations see it: the driver's free memory
+    plus what torch's caching allocator holds reserved but unused."""
+    torch = _torch()
+    free, _ = torch.cuda.mem_get_info(device)
+    return free + torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
+
+
 def allocate(n: int, dtype="complex128", device=None, rows: int = 1):
     """Uninitialized device buffer of rows x 2^n amplitudes; raises
     ``QubitCountOutOfRangeError`` if it does not fit in free HBM."""
@@ -180,7 +188,7 @@ def allocate(n: int, dtype="complex128", device=None, rows: int = 1):
     dt = _dtype_of(dtype)
     device = device or default_device()
     need = rows * (1 << n) * (16 if dt == torch.complex128 else 8)
-    free, _ = torch.cuda.mem_get_info(device)
+    free = free_bytes(device)
     if need > free:
         raise QubitCountOutOfRangeError(
             f"{need} bytes for {rows} x 2^{n} amplitudes exceed {free} free bytes on {device}"
