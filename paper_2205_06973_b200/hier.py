@@ -210,62 +210,6 @@ def _pack(exes: Sequence[ExecutablePart]):
     return parts, gates, total
 
 
-#: tile width (qubits) of compiled part kernels, both dtypes (hs_api.cu)
-TILE_BITS_JIT = 12
-#: gate streams up to this length also try the dagP re-partition (host time)
-REGROUP_MAX_GATES = 4000
-
-
-def _tile_width_regroup(n_local: int, exes: Sequence[ExecutablePart], tile: int):
-    """The program's gate stream (parts in order, on storage positions)
-    re-partitioned by dagP at the tile width, from two gate orders (the
-    stream itself, and its ASAP layers - dagP depends on the order it is
-    given: c5_33's dfs stream 15 parts, its layers 10). Returns a list of
-    (executable parts, owner) where owner[j] is the caller's part that
-    contributes most of part j's gates (ties: the earlier); empty when not
-    applicable."""
-    from collections import Counter
-
-    from .dag import build_dag
-    from .partition import partition_dagp
-
-    ops, src = [], []
-    for j, e in enumerate(exes):
-        pos = e.slot_map.qubits
-        for op, sl in zip(e.ops, e.op_slots):
-            ops.append(GateOp(op.kind, tuple(pos[x] for x in sl), op.params))
-            src.append(j)
-    if not ops or len(ops) > REGROUP_MAX_GATES or max(len(op.qubits) for op in ops) > tile:
-        return []
-    level, depth = [], {}
-    for op in ops:  # ASAP layer of every gate
-        lv = 1 + max(depth.get(q, 0) for q in op.qubits)
-        for q in op.qubits:
-            depth[q] = lv
-        level.append(lv)
-    out = []
-    for order in (list(range(len(ops))), sorted(range(len(ops)), key=lambda i: (level[i], i))):
-        c = Circuit(n_local, tuple(ops[i] for i in order))
-        part = partition_dagp(build_dag(c), tile)
-        new = [remap_part(c, p) for p in part.parts]
-        owner = []
-        for p in part.parts:
-            cnt = Counter(src[order[g]] for g in p.gate_indices)
-            top = max(cnt.values()) if cnt else 0
-            owner.append(min((j for j, v in cnt.items() if v == top), default=0))
-        out.append((new, owner))
-    return out
-
-
-def _planned_launches(n_local: int, code: int, options: int, exes: Sequence[ExecutablePart]) -> int:
-    """Launch count of a program plan (hs_plan_program, host only)."""
-    parts, gates, total = _pack(exes)
-    size, nl = ctypes.c_size_t(), ctypes.c_int()
-    _native.check(_native.load().hs_plan_program(n_local, code, TILE_BITS_JIT, options, parts, len(exes), gates,
-                                                 total, None, 0, ctypes.byref(size), ctypes.byref(nl)))
-    return nl.value
-
-
 class PartProgram:
     """A planned, device-resident sequence of parts for buffers of
     ``rows x 2^n_local`` amplitudes (hs_program_create). Planning happens
@@ -324,21 +268,9 @@ class PartProgram:
         if not final_natural and options & _native.HS_PLAN_LAYOUT:
             options |= _native.HS_PLAN_NO_RESTORE
         self.options = options
-        # compiled programs: also plan the gate stream re-partitioned at the
-        # tile width (dagP, limit 12) and keep it when it takes fewer
-        # launches - e.g. c5_33's k = 14 dfs parts: 15 tile passes regrouped
-        # from the parts vs 10 from dagP at 12 qubits
-        self._owner = None
-        code = 0 if self.dtype == torch.complex128 else 1
-        if (options & _native.HS_PLAN_JIT) and (options & _native.HS_PLAN_MERGE) and not (
-                options & (_native.HS_PLAN_PART_LOCAL | _native.HS_PLAN_CLUSTER)):
-            best = _planned_launches(n_local, code, options, exes)
-            for alt, owner in _tile_width_regroup(n_local, exes, TILE_BITS_JIT):
-                count = _planned_launches(n_local, code, options, alt)
-                if count < best:
-                    best, exes, self._owner = count, alt, owner
         parts, gates, total = _pack(exes)
         out = ctypes.c_void_p()
+        code = 0 if self.dtype == torch.complex128 else 1
         with torch.cuda.device(self.device):
             _native.check(lib.hs_engine_set_options(eng, options))
             try:
@@ -401,8 +333,7 @@ class PartProgram:
             "restore": bool(inf.restore),
             "compiled": bool(inf.compiled),
             "fp64_instr_per_amp": float(inf.fp64_instr_per_amp),
-            "user_part": (int(inf.user_part) if self._owner is None or inf.user_part < 0
-                          else self._owner[inf.user_part]),
+            "user_part": int(inf.user_part),
         }
 
     def dump(self, i: int) -> bytes:

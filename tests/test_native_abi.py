@@ -352,36 +352,3 @@ def test_regrouped_passes_match_oracle(name, limit, tile):
             psi[0, 0] = 1
             emu.run_program(psi, c.num_qubits, launches)
             assert np.max(np.abs(psi[0] - want)) < 1e-12, (layout, len(launches))
-
-
-@pytest.mark.parametrize("name,limit", [("c2@16", 14), ("c3@16", 12), ("c1@14", 8)])
-def test_tile_width_dagp_regroup_matches_oracle(name, limit):
-    """PartProgram's alternative plan: the gate stream re-partitioned by dagP
-    at the tile width (on storage positions). Its emulated launches must give
-    the oracle's state, every gate must land in exactly one new part, and the
-    owner map must name caller parts."""
-    from paper_2205_06973_b200.hier import _planned_launches, _tile_width_regroup
-
-    c = configs.build(name)
-    part = partition_dfs(build_dag(c), limit)
-    exes = [remap_part(c, p) for p in part.parts]
-    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
-    cands = _tile_width_regroup(c.num_qubits, exes, 12)
-    assert len(cands) == 2
-    for alt, owner in cands:
-        _check_regroup(c, exes, alt, owner, want)
-
-
-def _check_regroup(c, exes, alt, owner, want):
-    from paper_2205_06973_b200.hier import _planned_launches
-
-    assert sum(len(e.ops) for e in alt) == sum(len(e.ops) for e in exes)
-    assert len(owner) == len(alt) and set(owner) <= set(range(len(exes)))
-    assert max(e.num_slots for e in alt) <= 12
-    opts = _native.default_options() | 0x10 | 8 | 0x40
-    assert _planned_launches(c.num_qubits, 0, opts, alt) >= 1
-    launches = emu.plan_program(_native, c.num_qubits, 0, 12, alt, options=opts)
-    psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
-    psi[0, 0] = 1
-    emu.run_program(psi, c.num_qubits, launches)
-    assert np.max(np.abs(psi[0] - want)) < 1e-12
