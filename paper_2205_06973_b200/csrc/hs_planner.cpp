@@ -881,7 +881,7 @@ double pass_cost(uint64_t used, uint64_t prev, int tile_max) {
   return (prev && full && __builtin_popcountll(used & prev) < 3) ? 2.0 : 1.0;
 }
 
-int split_wide_parts(int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
+int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
                      Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
                      std::vector<int>& owner, double* cost, std::string& err) {
   struct Ref {
@@ -1071,7 +1071,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     std::vector<hs_gate> xg;
     std::vector<int> owner;
     double cost = 0.0;
-    int s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
+    int s = group_passes(tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
     if (s != HS_OK) return s;
     if (!(options & HS_PLAN_PART_LOCAL)) {
       // regroup the whole gate stream when that takes fewer passes; among
@@ -1085,7 +1085,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
         std::vector<hs_gate> ag;
         std::vector<int> ao;
         double c = 0.0;
-        s = split_wide_parts(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
+        s = group_passes(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
         if (ap.size() < xp.size() || (regrouped && ap.size() == xp.size() && c < cost)) {
           xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c;

@@ -566,16 +566,18 @@ def _basis_error(state, index):
     return worst
 
 
-@pytest.mark.parametrize("name,limit", [("c3", 12), ("c4", 12), ("c5_33", 14)])
-def test_full_size_circuit_then_inverse_returns_to_basis(name, limit):
+@pytest.mark.parametrize("name,limit,dtype", [("c3", 12, "complex128"), ("c4", 12, "complex128"),
+                                              ("c5_33", 14, "complex128"), ("c3", 12, "complex64")])
+def test_full_size_circuit_then_inverse_returns_to_basis(name, limit, dtype):
     """BASELINE configs at their full size (30 / 33 / 33 qubits: 16 / 128 /
     128 GiB, the last two in place) run forward and back through the engine's
-    planned passes: the state must return to |0..0> within 1e-10."""
+    planned passes: the state must return to |0..0> within 1e-10 (complex64:
+    1e-4)."""
     c = _inverse_appended(configs.build(name))
     part = partition_dfs(build_dag(c), limit)
-    st = execute_hierarchical(c, part)
+    st = execute_hierarchical(c, part, dtype=dtype)
     torch.cuda.synchronize()
-    assert _basis_error(st, 0) < 1e-10
+    assert _basis_error(st, 0) < TOL[dtype]
 
 
 def test_bv30_known_answer():
