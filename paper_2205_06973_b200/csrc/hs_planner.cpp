@@ -869,7 +869,12 @@ namespace {
 // the set and that no gate left behind precedes (c4, dfs k = 12: 137 parts
 // -> 44 passes; c3 17 -> 14). A pass belongs to the caller's part that
 // contributes most of its gates (ties: the earlier one).
-enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED };
+// GROUP_REVERSE_LOW3 / LOW6 run the seeded frontier over the reversed
+// stream (the last pass is chosen first: a gate may join it when no later
+// gate left behind shares a qubit), the last pass seeded with storage
+// positions 0..2 / 0..5 so that it can write natural order itself.
+enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
+                GROUP_REVERSE_LOW6 };
 
 // Cost of a pass sequence in units of one coalesced pass: a full-width pass
 // that shares fewer than 3 qubits with the pass before it cannot find its
@@ -955,9 +960,12 @@ int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gat
   uint64_t prev = 0;  // storage positions of the previous pass
   double total = 0.0;
   // group `stream` into passes and emit them
-  auto group = [&](const std::vector<Ref>& stream, bool frontier, bool seeded) -> int {
+  std::vector<std::pair<std::vector<int>, uint64_t>> held;  // reverse: passes in reverse order
+  auto group = [&](const std::vector<Ref>& stream, bool frontier, bool seeded, bool reverse,
+                   uint64_t first_seed) -> int {
     std::vector<int> rem(stream.size());
     for (size_t g = 0; g < stream.size(); ++g) rem[g] = (int)g;
+    bool first = true;
     while (!rem.empty()) {
       std::vector<int> chosen;
       uint64_t used = 0;
@@ -982,7 +990,7 @@ int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gat
                                                       const std::pair<int, uint64_t>& y) { return x.first > y.first; });
         double best = -1.0;
         for (int seeds = 0; seeds <= (seeded ? 3 : 0) && seeds <= (int)solo.size(); ++seeds) {
-          uint64_t seed = 0;
+          uint64_t seed = first ? first_seed : 0;
           for (int k = 0; k < seeds; ++k) seed |= 1ull << solo[k].second;
           const uint64_t in = grow(stream, rem, seed);
           std::vector<int> took;
@@ -997,7 +1005,9 @@ int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gat
       if (chosen.empty()) { err = "internal: pass grouping made no progress"; return HS_ERR_INVALID; }
       total += pass_cost(used, prev, tile_max);
       prev = used;
-      emit(stream, chosen, used);
+      first = false;
+      if (reverse) held.push_back({chosen, used});
+      else emit(stream, chosen, used);
       std::vector<int> rest;
       rest.reserve(rem.size() - chosen.size());
       size_t c = 0;
@@ -1048,13 +1058,49 @@ int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gat
       prev = u;
       continue;
     }
-    if (int s = group(own, false, false)) return s;
+    if (int s = group(own, false, false, false, 0)) return s;
   }
-  if (mode != GROUP_PER_PART) {
-    if (int s = group(all, mode != GROUP_ACROSS, mode == GROUP_FRONTIER_SEEDED)) return s;
+  if (mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6) {
+    const int n = (int)all.size();
+    std::vector<Ref> rev(all.rbegin(), all.rend());
+    const uint64_t low = mode == GROUP_REVERSE_LOW3 ? 0x7ull : 0x3Full;
+    if (int s = group(rev, true, true, true, low)) return s;
+    for (auto it = held.rbegin(); it != held.rend(); ++it) {  // back to program order
+      std::vector<int> fwd;
+      for (int g : it->first) fwd.push_back(n - 1 - g);
+      std::sort(fwd.begin(), fwd.end());
+      emit(all, fwd, it->second);
+    }
+  } else if (mode != GROUP_PER_PART) {
+    if (int s = group(all, mode != GROUP_ACROSS, mode == GROUP_FRONTIER_SEEDED, false, 0)) return s;
   }
   if (cost) *cost = total;
   return HS_OK;
+}
+
+// Storage positions 0..run-1 that a last ping-pong pass writing natural order
+// covers: its own staged positions plus the lowest others as the tile's
+// spare bits (plan_program's need_restore rule).
+int final_run_bits(const hs_part& p, int n_local, int tile_max) {
+  const int w = std::max(0, std::min(p.num_staged, HS_MAX_STAGED));
+  const int T = std::min(std::max(tile_max, w), n_local);
+  std::vector<char> cov(n_local + 1, 0);
+  for (int j = 0; j < w; ++j)
+    if (p.staged[j] >= 0 && p.staged[j] < n_local) cov[p.staged[j]] = 1;
+  int have = w;
+  for (int q = 0; q < n_local && have < T; ++q)
+    if (!cov[q]) { cov[q] = 1; ++have; }
+  int run = 0;
+  while (run < n_local && cov[run]) ++run;
+  return run;
+}
+
+// the run (in storage bits) a last pass must write in natural order to make
+// the gate-free final permutation unnecessary: 3 bits = 128 B of complex128
+// (measured: c2 5.96 ms with a 1 KB-run rule and 9 launches vs 5.56 ms with
+// 128 B runs and 8; c3 96.6 vs 94.9 ms; 64 B runs lose: c2 6.51 vs 5.74 ms)
+int final_hot(int n_local, int tile_max) {
+  return std::min(3, std::max(1, std::min(n_local, tile_max / 2)));
 }
 
 }  // namespace
@@ -1079,15 +1125,26 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       // one B200: c2 keeps its 9 parts - a 9-pass regrouping with better
       // coalescing ran 6.00 vs 5.71 ms; c3's seeded frontier 105 vs 110 ms;
       // c5_33's unseeded frontier, 15 passes, 1224 vs 1273 ms for 16.)
+      // launches = passes + the gate-free final permutation of a ping-pong
+      // program whose last pass cannot write natural order itself
+      auto launches = [&](const std::vector<hs_part>& ps) -> size_t {
+        const bool pp = (options & HS_PLAN_LAYOUT) && (options & HS_PLAN_PINGPONG) && !(options & HS_PLAN_NO_RESTORE);
+        if (!pp || ps.empty()) return ps.size();
+        return ps.size() + (final_run_bits(ps.back(), n_local, tile_max) < final_hot(n_local, tile_max) ? 1 : 0);
+      };
       bool regrouped = false;
-      for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED}) {
+      for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
+                            GROUP_REVERSE_LOW6}) {
         std::vector<hs_part> ap;
         std::vector<hs_gate> ag;
         std::vector<int> ao;
         double c = 0.0;
+        const bool pp = (options & HS_PLAN_LAYOUT) && (options & HS_PLAN_PINGPONG) && !(options & HS_PLAN_NO_RESTORE);
+        if (!pp && (mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6)) continue;  // only for a natural-order final write
         s = group_passes(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
-        if (ap.size() < xp.size() || (regrouped && ap.size() == xp.size() && c < cost)) {
+        const size_t la = launches(ap), lx = launches(xp);
+        if (la < lx || (regrouped && la == lx && c < cost)) {
           xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c;
           regrouped = true;
         }
@@ -1151,14 +1208,12 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
   // (measured: c3 126 -> 121 ms, c2 5.95 -> 5.92 ms); the gate-free final
   // permutation stages at most 2 * hot = 12 qubits
   const int hot = std::min(6, std::max(1, std::min(n_local, tile_max / 2)));
-  // the last part writes natural order directly only if qubits 0..hot-1 are
-  // among its own (coalesced stores); otherwise it writes a coalesced layout
-  // and one gate-free out-of-place launch permutes into natural order
   const bool no_restore = (options & HS_PLAN_NO_RESTORE) != 0;
   // The last part's tile takes the lowest logical qubits it does not stage
   // as its extra bits; it writes natural order itself when those and its
-  // own cover qubits 0..hot-1 (stores in 2^hot-amplitude runs), else the
-  // gate-free launch follows.
+  // own cover qubits 0..final_hot-1 (128 B store runs), else it writes a
+  // coalesced layout and one gate-free out-of-place launch permutes into
+  // natural order.
   bool need_restore = false;
   std::vector<int32_t> last_extra;  // logical qubits
   if (pp && !no_restore) {
@@ -1172,9 +1227,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       if (!cov[q]) { last_extra.push_back(q); cov[q] = 1; }
     int run = 0;
     while (run < n_local && cov[run]) ++run;
-    // (measured: 64 B runs, final_run = 2, lose to the extra coalesced
-    // launch: c2 6.51 vs 5.74 ms, c3 119.1 vs 116.1 ms)
-    need_restore = run < std::min(hot, n_local);
+    need_restore = run < std::min(final_hot(n_local, tile_max), n_local);
   }
   const bool first_inplace = pp && ((num_parts + (need_restore ? 1 : 0)) % 2 == 1);
   int cur_buf = 0;
