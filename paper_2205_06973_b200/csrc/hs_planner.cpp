@@ -874,17 +874,18 @@ namespace {
 // gate left behind shares a qubit), the last pass seeded with storage
 // positions 0..2 / 0..5 so that it can write natural order itself.
 enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
-                GROUP_REVERSE_LOW6 };
+                GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6 };
 
-// Cost of a pass sequence in units of one coalesced pass: a full-width pass
-// that shares fewer than 3 qubits with the pass before it cannot find its
-// qubits on the lowest storage positions (the previous pass could only move
-// its own tile's qubits there), so its reads run in short pieces - measured
-// ~2x the time of a coalesced pass (c3: 12.7 vs 5.8 ms, ncu r01s3).
+// Cost of a pass in units of one coalesced HBM pass: a full-width pass that
+// shares fewer than 3 qubits with the pass before it cannot find its qubits
+// on the lowest storage positions (the previous pass could only move its own
+// tile's qubits there), so its reads run in short pieces - measured ~2x the
+// time of a coalesced pass (c3: 12.7 vs 5.8 ms, ncu r01s3).
 double pass_cost(uint64_t used, uint64_t prev, int tile_max) {
   const bool full = __builtin_popcountll(used) > tile_max - 3;
   return (prev && full && __builtin_popcountll(used & prev) < 3) ? 2.0 : 1.0;
 }
+
 
 int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
                      Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
@@ -1060,11 +1061,12 @@ int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gat
     }
     if (int s = group(own, false, false, false, 0)) return s;
   }
-  if (mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6) {
+  if (mode >= GROUP_REVERSE_LOW3) {
     const int n = (int)all.size();
     std::vector<Ref> rev(all.rbegin(), all.rend());
-    const uint64_t low = mode == GROUP_REVERSE_LOW3 ? 0x7ull : 0x3Full;
-    if (int s = group(rev, true, true, true, low)) return s;
+    const bool low3 = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_PLAIN_LOW3;
+    const bool seeded = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6;
+    if (int s = group(rev, true, seeded, true, low3 ? 0x7ull : 0x3Full)) return s;
     for (auto it = held.rbegin(); it != held.rend(); ++it) {  // back to program order
       std::vector<int> fwd;
       for (int g : it->first) fwd.push_back(n - 1 - g);
@@ -1127,25 +1129,28 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       // c5_33's unseeded frontier, 15 passes, 1224 vs 1273 ms for 16.)
       // launches = passes + the gate-free final permutation of a ping-pong
       // program whose last pass cannot write natural order itself
-      auto launches = [&](const std::vector<hs_part>& ps) -> size_t {
+      auto final_perm = [&](const std::vector<hs_part>& ps) -> double {
         const bool pp = (options & HS_PLAN_LAYOUT) && (options & HS_PLAN_PINGPONG) && !(options & HS_PLAN_NO_RESTORE);
-        if (!pp || ps.empty()) return ps.size();
-        return ps.size() + (final_run_bits(ps.back(), n_local, tile_max) < final_hot(n_local, tile_max) ? 1 : 0);
+        if (!pp || ps.empty()) return 0.0;
+        return final_run_bits(ps.back(), n_local, tile_max) < final_hot(n_local, tile_max) ? 1.0 : 0.0;
       };
+      size_t best_launches = xp.size() + (size_t)final_perm(xp);
       bool regrouped = false;
       for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
-                            GROUP_REVERSE_LOW6}) {
+                            GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6}) {
         std::vector<hs_part> ap;
         std::vector<hs_gate> ag;
         std::vector<int> ao;
         double c = 0.0;
         const bool pp = (options & HS_PLAN_LAYOUT) && (options & HS_PLAN_PINGPONG) && !(options & HS_PLAN_NO_RESTORE);
-        if (!pp && (mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6)) continue;  // only for a natural-order final write
+        if (!pp && mode >= GROUP_REVERSE_LOW3) continue;  // only for a natural-order final write
         s = group_passes(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
-        const size_t la = launches(ap), lx = launches(xp);
-        if (la < lx || (regrouped && la == lx && c < cost)) {
-          xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c;
+        const size_t la = ap.size() + (size_t)final_perm(ap);
+        // (measured c3: 13 launches with one short-read pass 96.3 ms, 14
+        // coalesced launches 96.6-97.4 ms - launches first)
+        if (la < best_launches || (regrouped && la == best_launches && c < cost)) {
+          xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c; best_launches = la;
           regrouped = true;
         }
       }
