@@ -1080,23 +1080,6 @@ int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gat
   return HS_OK;
 }
 
-// Storage positions 0..run-1 that a last ping-pong pass writing natural order
-// covers: its own staged positions plus the lowest others as the tile's
-// spare bits (plan_program's need_restore rule).
-int final_run_bits(const hs_part& p, int n_local, int tile_max) {
-  const int w = std::max(0, std::min(p.num_staged, HS_MAX_STAGED));
-  const int T = std::min(std::max(tile_max, w), n_local);
-  std::vector<char> cov(n_local + 1, 0);
-  for (int j = 0; j < w; ++j)
-    if (p.staged[j] >= 0 && p.staged[j] < n_local) cov[p.staged[j]] = 1;
-  int have = w;
-  for (int q = 0; q < n_local && have < T; ++q)
-    if (!cov[q]) { cov[q] = 1; ++have; }
-  int run = 0;
-  while (run < n_local && cov[run]) ++run;
-  return run;
-}
-
 // the run (in storage bits) a last pass must write in natural order to make
 // the gate-free final permutation unnecessary: 3 bits = 128 B of complex128
 // (measured: c2 5.96 ms with a 1 KB-run rule and 9 launches vs 5.56 ms with
@@ -1127,14 +1110,21 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       // one B200: c2 keeps its 9 parts - a 9-pass regrouping with better
       // coalescing ran 6.00 vs 5.71 ms; c3's seeded frontier 105 vs 110 ms;
       // c5_33's unseeded frontier, 15 passes, 1224 vs 1273 ms for 16.)
-      // launches = passes + the gate-free final permutation of a ping-pong
-      // program whose last pass cannot write natural order itself
-      auto final_perm = [&](const std::vector<hs_part>& ps) -> double {
-        const bool pp = (options & HS_PLAN_LAYOUT) && (options & HS_PLAN_PINGPONG) && !(options & HS_PLAN_NO_RESTORE);
-        if (!pp || ps.empty()) return 0.0;
-        return final_run_bits(ps.back(), n_local, tile_max) < final_hot(n_local, tile_max) ? 1.0 : 0.0;
+      // every candidate is planned in full (host only, ~20 ms each) and
+      // judged by its real launch count: passes plus a ping-pong program's
+      // final permutation or an in-place program's restore launches
+      auto planned = [&](const std::vector<hs_part>& ps, const std::vector<hs_gate>& gs, size_t* out) -> int {
+        std::vector<PartPlan> tmp;
+        std::vector<int32_t> ip, fp;
+        std::string e;
+        const int st = plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, ps.data(), (int)ps.size(),
+                                    gs.data(), (int)gs.size(), tmp, e, &ip, given_init, &fp);
+        if (st != HS_OK) { err = e; return st; }
+        *out = tmp.size();
+        return HS_OK;
       };
-      size_t best_launches = xp.size() + (size_t)final_perm(xp);
+      size_t best_launches = 0;
+      if ((s = planned(xp, xg, &best_launches)) != HS_OK) return s;
       bool regrouped = false;
       for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                             GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6}) {
@@ -1142,13 +1132,12 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
         std::vector<hs_gate> ag;
         std::vector<int> ao;
         double c = 0.0;
-        const bool pp = (options & HS_PLAN_LAYOUT) && (options & HS_PLAN_PINGPONG) && !(options & HS_PLAN_NO_RESTORE);
-        if (!pp && mode >= GROUP_REVERSE_LOW3) continue;  // only for a natural-order final write
         s = group_passes(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
-        const size_t la = ap.size() + (size_t)final_perm(ap);
-        // (measured c3: 13 launches with one short-read pass 96.3 ms, 14
-        // coalesced launches 96.6-97.4 ms - launches first)
+        size_t la = 0;
+        if ((s = planned(ap, ag, &la)) != HS_OK) return s;
+        // fewest launches; among as few, the lowest pass_cost (measured c3:
+        // 13 launches with one short-read pass 96.3 ms, 14 coalesced 96.6-97.4)
         if (la < best_launches || (regrouped && la == best_launches && c < cost)) {
           xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c; best_launches = la;
           regrouped = true;
