@@ -887,7 +887,7 @@ double pass_cost(uint64_t used, uint64_t prev, int tile_max) {
 }
 
 
-int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
+int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
                      Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
                      std::vector<int>& owner, double* cost, std::string& err) {
   struct Ref {
@@ -1066,7 +1066,9 @@ int group_passes(int tile_max, const hs_part* parts, int num_parts, const hs_gat
     std::vector<Ref> rev(all.rbegin(), all.rend());
     const bool low3 = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_PLAIN_LOW3;
     const bool seeded = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6;
-    if (int s = group(rev, true, seeded, true, low3 ? 0x7ull : 0x3Full)) return s;
+    // (the seed never names a position the state does not have)
+    const uint64_t avail = n_local >= 64 ? ~0ull : ((1ull << n_local) - 1);
+    if (int s = group(rev, true, seeded, true, (low3 ? 0x7ull : 0x3Full) & avail)) return s;
     for (auto it = held.rbegin(); it != held.rend(); ++it) {  // back to program order
       std::vector<int> fwd;
       for (int g : it->first) fwd.push_back(n - 1 - g);
@@ -1102,7 +1104,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     std::vector<hs_gate> xg;
     std::vector<int> owner;
     double cost = 0.0;
-    int s = group_passes(tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
+    int s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
     if (s != HS_OK) return s;
     if (!(options & HS_PLAN_PART_LOCAL)) {
       // regroup the whole gate stream when that takes fewer passes; among
@@ -1132,7 +1134,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
         std::vector<hs_gate> ag;
         std::vector<int> ao;
         double c = 0.0;
-        s = group_passes(tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
+        s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
         size_t la = 0;
         if ((s = planned(ap, ag, &la)) != HS_OK) return s;

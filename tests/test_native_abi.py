@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import program_emulator as emu
-from conftest import parts_of
+from conftest import partition_of, parts_of
 from oracle import hisim_oracle as orc
 from paper_2205_06973_b200 import _native, build_dag, configs, partition_dfs
 from paper_2205_06973_b200.errors import PartTooWideForLayoutError
@@ -352,3 +352,28 @@ def test_regrouped_passes_match_oracle(name, limit, tile):
             psi[0, 0] = 1
             emu.run_program(psi, c.num_qubits, launches)
             assert np.max(np.abs(psi[0] - want)) < 1e-12, (layout, len(launches))
+
+
+@pytest.mark.parametrize("options", [0x405, 0x40d, 0x44d, 0x415, 0x45d])
+def test_merged_programs_match_oracle_on_corpus(golden, options):
+    """Whole programs with HS_PLAN_MERGE (every pass grouping candidate is
+    planned and the fewest launches win) on the corpus: tiny states (n < 6,
+    where seeds must stay inside the state), every gate kind, with and
+    without layouts / ping-pong, emulated against the reference states."""
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    checked = 0
+    for i, doc in enumerate(docs[:40]):
+        c = parse_qasm(doc["qasm"])
+        for key, parts in doc["partitions"].items():
+            part = partition_of(parts)
+            exes = [remap_part(c, p) for p in part.parts]
+            tile = 12
+            if max(e.num_slots for e in exes) > tile:
+                continue
+            launches = emu.plan_program(_native, c.num_qubits, 0, tile, exes, options=options)
+            psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
+            psi[0, 0] = 1
+            emu.run_program(psi, c.num_qubits, launches)
+            assert np.max(np.abs(psi[0] - states[f"c{i}"])) < 1e-12, (i, key)
+            checked += 1
+    assert checked >= 40
