@@ -1107,14 +1107,14 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     int s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
     if (s != HS_OK) return s;
     if (!(options & HS_PLAN_PART_LOCAL)) {
-      // regroup the whole gate stream when that takes fewer passes; among
-      // regroupings with as few passes, the lowest pass_cost. (Measured on
-      // one B200: c2 keeps its 9 parts - a 9-pass regrouping with better
-      // coalescing ran 6.00 vs 5.71 ms; c3's seeded frontier 105 vs 110 ms;
-      // c5_33's unseeded frontier, 15 passes, 1224 vs 1273 ms for 16.)
-      // every candidate is planned in full (host only, ~20 ms each) and
-      // judged by its real launch count: passes plus a ping-pong program's
-      // final permutation or an in-place program's restore launches
+      // regroup the whole gate stream when that takes fewer launches; among
+      // regroupings with as few, the lowest pass_cost. Every candidate is
+      // planned in full (host only, ~20 ms each) and judged by its real
+      // launch count: passes plus a ping-pong program's final permutation or
+      // an in-place program's restore launches. (Measured on one B200: a
+      // 9-pass forward regrouping of c2 ran 6.00 vs 5.71 ms for its 9 parts
+      // + permutation, so equal counts keep the parts; c5_33's unseeded
+      // frontier, 15 passes, 1224 vs 1273 ms for the seeded 16.)
       auto planned = [&](const std::vector<hs_part>& ps, const std::vector<hs_gate>& gs, size_t* out) -> int {
         std::vector<PartPlan> tmp;
         std::vector<int32_t> ip, fp;
