@@ -873,11 +873,6 @@ namespace {
 // stream (the last pass is chosen first: a gate may join it when no later
 // gate left behind shares a qubit), the last pass seeded with storage
 // positions 0..2 / 0..5 so that it can write natural order itself.
-// randomised grouping restarts per direction (plan_program), for gate
-// streams of at most this many gates (c5_33: 1044 gates, 15 -> 14 passes)
-constexpr int RANDOM_GROUPINGS = 12;
-constexpr int RANDOM_GROUPING_MAX_GATES = 3000;
-
 enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                 GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6 };
 
@@ -894,16 +889,7 @@ double pass_cost(uint64_t used, uint64_t prev, int tile_max) {
 
 int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
                      Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
-                     std::vector<int>& owner, double* cost, std::string& err, uint64_t rng = 0) {
-  // rng != 0: randomised frontier growth (xorshift; a step takes one of the
-  // three best additions instead of the best with probability ~1/7) - a
-  // cheap restart search over groupings, deterministic per seed
-  auto coin = [&rng](uint32_t n) -> uint32_t {
-    rng ^= rng << 13;
-    rng ^= rng >> 7;
-    rng ^= rng << 17;
-    return (uint32_t)(rng >> 33) % n;
-  };
+                     std::vector<int>& owner, double* cost, std::string& err) {
   struct Ref {
     int part;
     const hs_gate* g;
@@ -931,9 +917,9 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
   auto grow = [&](const std::vector<Ref>& stream, const std::vector<int>& rem, uint64_t in) -> uint64_t {
     for (;;) {
       const int base = runnable(stream, rem, in, nullptr);
-      uint64_t blocked = 0;
+      uint64_t blocked = 0, best_add = 0;
+      double best_gain = 0.0;
       std::vector<uint64_t> seen;
-      std::vector<std::pair<double, uint64_t>> cand;  // (gain, addition), first-seen order
       for (int g : rem) {
         const uint64_t m = stream[g].mask;
         if (m & blocked) continue;
@@ -943,14 +929,10 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
         if (std::find(seen.begin(), seen.end(), add) != seen.end()) continue;
         seen.push_back(add);
         const double gain = double(runnable(stream, rem, in | add, nullptr) - base) / __builtin_popcountll(add);
-        if (gain > 0.0) cand.push_back({gain, add});
+        if (gain > best_gain) { best_gain = gain; best_add = add; }
       }
-      if (cand.empty()) return in;
-      std::stable_sort(cand.begin(), cand.end(), [](const std::pair<double, uint64_t>& x,
-                                                    const std::pair<double, uint64_t>& y) { return x.first > y.first; });
-      size_t pick = 0;
-      if (rng && cand.size() > 1 && coin(7) == 0) pick = coin((uint32_t)std::min<size_t>(3, cand.size()));
-      in |= cand[pick].second;
+      if (!best_add) return in;
+      in |= best_add;
     }
   };
   auto emit = [&](const std::vector<Ref>& stream, const std::vector<int>& chosen, uint64_t in) {
@@ -1146,24 +1128,13 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       size_t best_launches = 0;
       if ((s = planned(xp, xg, &best_launches)) != HS_OK) return s;
       bool regrouped = false;
-      // the deterministic groupings, then randomised frontier restarts
-      // (forward and reverse) for streams short enough to plan many times
-      std::vector<std::pair<Grouping, uint64_t>> runs;
       for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
-                            GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6})
-        runs.push_back({mode, 0});
-      if (num_gates <= RANDOM_GROUPING_MAX_GATES)
-        for (uint64_t r = 1; r <= RANDOM_GROUPINGS; ++r) {
-          runs.push_back({GROUP_FRONTIER, 0x9E3779B97F4A7C15ull * r});
-          runs.push_back({GROUP_REVERSE_PLAIN_LOW3, 0xD1B54A32D192ED03ull * r});
-        }
-      for (const auto& run : runs) {
-        const Grouping mode = run.first;
+                            GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6}) {
         std::vector<hs_part> ap;
         std::vector<hs_gate> ag;
         std::vector<int> ao;
         double c = 0.0;
-        s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err, run.second);
+        s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
         if (s != HS_OK) return s;
         size_t la = 0;
         if ((s = planned(ap, ag, &la)) != HS_OK) return s;
