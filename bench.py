@@ -231,6 +231,15 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     state = allocate(n_local, "complex128", dev)
     stream = torch.cuda.current_stream(dev)
 
+    # the whole program as one CUDA graph launch (PartProgram.run_graph,
+    # captured in the warm-up) unless --no-graph: launch overhead matters for
+    # L2-resident states (c1: 7 launches of ~16 us)
+    def launch(buf):
+        if args.no_graph:
+            run.program.run(buf)
+        else:
+            run.program.run_graph(buf, stream=stream)
+
     def one_step(timed_events=None):
         if not dist:
             run.program.init_basis(state, 0)
@@ -247,7 +256,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
             if timed_events is not None:
                 timed_events += marks_
         elif timed_events is None:
-            run.program.run(state)
+            launch(state)
         else:
             for i in range(num_launches):
                 run.program.run(state, i, 1)
@@ -279,7 +288,7 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         if dist:
             run.run(state)
         else:
-            run.program.run(state)
+            launch(state)
         e1.record(stream)
     torch.cuda.synchronize()
     total_ms = sum(e0.elapsed_time(e1) for _, e0, e1 in step_ev)
@@ -440,6 +449,8 @@ def main(argv=None):
     ap.add_argument("--cpu-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the program's kernels one by one instead of as one CUDA graph")
     ap.add_argument("--plan-add", type=lambda x: int(x, 0), default=0,
                     help="HS_PLAN_* bits added to the engine defaults (e.g. 0x400 = HS_PLAN_MERGE)")
     ap.add_argument("--plan-options", type=lambda x: int(x, 0), default=None,
@@ -475,7 +486,8 @@ def main(argv=None):
               "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
               "state_bytes_per_gpu": (1 << (n - extra)) * 16,
               "l2_policy": "inputs larger than L2: the state (>= 1 GiB) exceeds the 126 MB L2",
-              "partition_seconds_host": round(t_part, 4), "plan_add": hex(args.plan_add), "parallelism": (f"qubit-sharded x{world}" if world > 1 else "single GPU") if args.impl != "reference"
+              "partition_seconds_host": round(t_part, 4), "plan_add": hex(args.plan_add),
+              "launch": "per-kernel" if (args.no_graph or world > 1) else "one CUDA graph per step (PartProgram.run_graph)", "parallelism": (f"qubit-sharded x{world}" if world > 1 else "single GPU") if args.impl != "reference"
               else f"host CPU threads (rank 0 of {args.gpus})"}
 
     if args.impl == "reference":
