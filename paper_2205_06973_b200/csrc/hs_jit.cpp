@@ -16,6 +16,7 @@
 
 #include <cinttypes>
 #include <cmath>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -235,11 +236,86 @@ struct Gen {
   std::vector<double> cre, cim;  // pending constant factor per register
   bool have_const = false, have_u = false;
   int u_id = 0;
+  // pending mixed diagonals (register and thread bits, no controls): their
+  // entry is d[parity(i & kreg) ^ parity(t & qtid)]. Grouped by register
+  // mask, a group's factor for register i is F_g[parity(i & kreg)], where
+  // F_g[0] / F_g[1] are per-thread products of d[tp] / d[!tp] over the
+  // group's gates (no per-amplitude work); register i then costs one complex
+  // multiply per extra group plus one to apply, instead of one per gate.
+  std::vector<Instr> mixed;
+  int m_id = 0;
 
   void reset_pending() {
     cre.assign(nreg, 1.0);
     cim.assign(nreg, 0.0);
     have_const = have_u = false;
+    mixed.clear();
+  }
+  // mixed run: per-thread group factors, then one factor per register
+  void flush_mixed() {
+    std::vector<uint32_t> masks;
+    for (const Instr& in : mixed) {
+      const uint32_t kreg = (in.flags & F_PARITY) ? in.rpos[0] : (1u << in.k);
+      if (std::find(masks.begin(), masks.end(), kreg) == masks.end()) masks.push_back(kreg);
+    }
+    ++m_id;
+    const std::string T = R(), M = "m" + std::to_string(m_id) + "_";
+    o << "    {\n";
+    for (size_t gi = 0; gi < masks.size(); ++gi) {
+      const std::string a = M + std::to_string(gi);
+      o << "      " << T << " " << a << "r0, " << a << "i0, " << a << "r1, " << a << "i1;\n";
+      bool first = true;
+      for (const Instr& in : mixed) {
+        const uint32_t kreg = (in.flags & F_PARITY) ? in.rpos[0] : (1u << in.k);
+        if (kreg != masks[gi]) continue;
+        const std::string d0r = lit(in.m[0], c128), d0i = lit(in.m[1], c128);
+        const std::string d1r = lit(in.m[2], c128), d1i = lit(in.m[3], c128);
+        o << "      { const bool tp = (__popc(t & " << in.qtid << "u) & 1) != 0;\n";
+        o << "        const " << T << " ar = tp ? " << d1r << " : " << d0r << ", ai = tp ? " << d1i << " : " << d0i
+          << ", br = tp ? " << d0r << " : " << d1r << ", bi = tp ? " << d0i << " : " << d1i << ";\n";
+        if (first) {
+          o << "        " << a << "r0 = ar; " << a << "i0 = ai; " << a << "r1 = br; " << a << "i1 = bi; }\n";
+          first = false;
+        } else {
+          ops += 8.0;  // per thread, not per amplitude (ops counts a thread's instructions)
+          o << "        { const " << T << " x = " << a << "r0, y = " << a << "i0; " << a << "r0 = x * ar - y * ai; "
+            << a << "i0 = x * ai + y * ar; }\n";
+          o << "        { const " << T << " x = " << a << "r1, y = " << a << "i1; " << a << "r1 = x * br - y * bi; "
+            << a << "i1 = x * bi + y * br; } }\n";
+        }
+      }
+    }
+    // the thread-uniform scalar joins group 0 (per thread, not per amplitude)
+    if (have_u) {
+      ops += 8.0;
+      const std::string a = M + "0", ur = "ur" + std::to_string(u_id), ui = "ui" + std::to_string(u_id);
+      for (int b = 0; b < 2; ++b) {
+        const std::string r = a + "r" + std::to_string(b), i = a + "i" + std::to_string(b);
+        o << "      { const " << T << " x = " << r << ", y = " << i << "; " << r << " = x * " << ur << " - y * " << ui
+          << "; " << i << " = x * " << ui << " + y * " << ur << "; }\n";
+      }
+    }
+    for (int i = 0; i < nreg; ++i) {
+      std::string fr, fi;
+      o << "      {";
+      for (size_t gi = 0; gi < masks.size(); ++gi) {
+        const int par = __builtin_popcount(uint32_t(i) & masks[gi]) & 1;
+        const std::string r = M + std::to_string(gi) + "r" + std::to_string(par);
+        const std::string im_ = M + std::to_string(gi) + "i" + std::to_string(par);
+        if (gi == 0) {
+          o << " " << T << " fr = " << r << ", fi = " << im_ << ";";
+        } else {
+          o << " { const " << T << " x = fr, y = fi; fr = x * " << r << " - y * " << im_ << "; fi = x * " << im_
+            << " + y * " << r << "; }";
+          ops += 4 * wgt;
+        }
+      }
+      o << "\n  ";
+      cmul_const(i, cre[i], cim[i]);
+      cmul_into(i, "fr", "fi");
+      o << "      }\n";
+    }
+    o << "    }\n";
   }
   // final: fold the part's scalar S into the run and apply it (no
   // normalisation); otherwise the most common factor of the run is pulled
@@ -255,7 +331,7 @@ struct Gen {
       Sr = 1.0;
       Si = 0.0;
     }
-    if (!have_const && !have_u) return;
+    if (!have_const && !have_u && mixed.empty()) return;
     if (have_const && !final) {
       int best = -1, best_n = 0;
       for (int i = 0; i < nreg; ++i) {
@@ -280,6 +356,11 @@ struct Gen {
         }
         push_scale(fr, fi);
       }
+    }
+    if (!mixed.empty()) {
+      flush_mixed();
+      reset_pending();
+      return;
     }
     o << "    {\n";
     for (int i = 0; i < nreg; ++i) {
@@ -322,7 +403,12 @@ struct Gen {
       have_const = true;
       return true;
     }
-    if (rdep) return false;
+    if (rdep) {
+      // controlled ones, and sign flips (integer XORs, no FP64), are applied as they come
+      if (in.creg != 0 || in.ctid != 0 || cluster || (in.flags & F_SIGN)) return false;
+      mixed.push_back(in);
+      return true;
+    }
     // uniform per thread: one scalar factor, selected by this thread's bits
     if (!have_u) {
       ++u_id;
