@@ -295,34 +295,14 @@ struct Gen {
           << "; " << i << " = x * " << ui << " + y * " << ur << "; }\n";
       }
     }
-    // two or more groups: the four products of groups 0 and 1 per thread
-    // (16 instructions) save one complex multiply per register
-    const bool pair = masks.size() >= 2;
-    if (pair) {
-      ops += 16.0;
-      for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b) {
-          const std::string x = M + "0", y = M + "1", c = M + "c" + std::to_string(a) + std::to_string(b);
-          const std::string ar = x + "r" + std::to_string(a), ai = x + "i" + std::to_string(a);
-          const std::string br = y + "r" + std::to_string(b), bi = y + "i" + std::to_string(b);
-          o << "      const " << T << " " << c << "r = " << ar << " * " << br << " - " << ai << " * " << bi << ", " << c
-            << "i = " << ar << " * " << bi << " + " << ai << " * " << br << ";\n";
-        }
-    }
     for (int i = 0; i < nreg; ++i) {
       std::string fr, fi;
       o << "      {";
-      for (size_t gi = pair ? 1 : 0; gi < masks.size(); ++gi) {
+      for (size_t gi = 0; gi < masks.size(); ++gi) {
         const int par = __builtin_popcount(uint32_t(i) & masks[gi]) & 1;
-        std::string r = M + std::to_string(gi) + "r" + std::to_string(par);
-        std::string im_ = M + std::to_string(gi) + "i" + std::to_string(par);
-        if (pair && gi == 1) {  // the precomputed product of groups 0 and 1
-          const int p0 = __builtin_popcount(uint32_t(i) & masks[0]) & 1;
-          const std::string c = M + "c" + std::to_string(p0) + std::to_string(par);
-          r = c + "r";
-          im_ = c + "i";
-        }
-        if (gi == (pair ? 1u : 0u)) {
+        const std::string r = M + std::to_string(gi) + "r" + std::to_string(par);
+        const std::string im_ = M + std::to_string(gi) + "i" + std::to_string(par);
+        if (gi == 0) {
           o << " " << T << " fr = " << r << ", fi = " << im_ << ";";
         } else {
           o << " { const " << T << " x = fr, y = fi; fr = x * " << r << " - y * " << im_ << "; fi = x * " << im_
