@@ -867,12 +867,15 @@ namespace {
 // addition makes the most gates runnable per added qubit, until the tile is
 // full or nothing gains; the pass then runs every gate whose qubits are in
 // the set and that no gate left behind precedes (c4, dfs k = 12: 137 parts
-// -> 44 passes; c3 17 -> 14). A pass belongs to the caller's part that
-// contributes most of its gates (ties: the earlier one).
-// GROUP_REVERSE_LOW3 / LOW6 run the seeded frontier over the reversed
-// stream (the last pass is chosen first: a gate may join it when no later
-// gate left behind shares a qubit), the last pass seeded with storage
-// positions 0..2 / 0..5 so that it can write natural order itself.
+// -> 45 passes; c3 17 -> 15). GROUP_FRONTIER_SEEDED also tries growth
+// started from 1-3 qubits of the previous pass (coalesced reads, see
+// pass_cost). GROUP_REVERSE_* run the frontier (seeded or plain) over the
+// reversed stream - the last pass is chosen first: a gate may join it when
+// no later gate left behind shares a qubit - with the last pass seeded with
+// storage positions 0..2 / 0..5 so that it can write natural order itself
+// (c2: 9 parts + a permutation launch -> 8 passes). A pass belongs to the
+// caller's part that contributes most of its gates (ties: the earlier one).
+// plan_program plans every grouping in full and keeps the fewest launches.
 enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                 GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6 };
 
@@ -886,10 +889,9 @@ double pass_cost(uint64_t used, uint64_t prev, int tile_max) {
   return (prev && full && __builtin_popcountll(used & prev) < 3) ? 2.0 : 1.0;
 }
 
-
-int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
-                     Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
-                     std::vector<int>& owner, double* cost, std::string& err) {
+int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates,
+                 int num_gates, Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
+                 std::vector<int>& owner, double* cost, std::string& err) {
   struct Ref {
     int part;
     const hs_gate* g;
