@@ -1201,11 +1201,12 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
   // ping-pong: out-of-place parts alternate state -> scratch -> state; an
   // odd part count runs part 0 in place so the last part lands in the state
   const bool pp = layout && (options & HS_PLAN_PINGPONG) && num_parts >= 2;
-  // the next part's qubits go to the lowest `hot` positions: 3 would give
-  // 128 B runs; 6 gives 1 KB (c128) runs, fewer DRAM pages per tile
-  // (measured: c3 126 -> 121 ms, c2 5.95 -> 5.92 ms); the gate-free final
-  // permutation stages at most 2 * hot = 12 qubits
-  const int hot = std::min(6, std::max(1, std::min(n_local, tile_max / 2)));
+  // the next part's qubits go to the lowest `hot` positions (3: 128 B runs
+  // of complex128). Measured with the tile-pass planner: hot = 3 vs 6 (1 KB
+  // runs) c2 5.42 vs 5.55 ms, c3 95.0 vs 95.4 ms, c1 equal (an earlier
+  // planner measured the opposite: c3 126 vs 121 ms). The gate-free final
+  // permutation stages at most 2 * hot qubits.
+  const int hot = std::min(3, std::max(1, std::min(n_local, tile_max / 2)));
   const bool no_restore = (options & HS_PLAN_NO_RESTORE) != 0;
   // The last part's tile takes the lowest logical qubits it does not stage
   // as its extra bits; it writes natural order itself when those and its
