@@ -190,6 +190,10 @@ int hs_program_final_layout(hs_program* prog, int32_t* phys);
 int hs_program_bind_scratch(hs_program* prog, void* scratch, size_t bytes);
 /* empty unless HS_PLAN_JIT compilation failed (the interpreter then runs) */
 const char* hs_program_jit_error(hs_program* prog);
+/* process-wide counts of compiled-part kernels loaded from the on-disk cubin
+ * cache ($HISVSIM_CACHE_DIR, default ~/.cache/hisvsim; "off" disables) and
+ * compiled with NVRTC (in-process cache hits count as neither) */
+int hs_jit_cache_stats(int* disk_hits, int* compiles);
 /* device instructions of one launch, copied to host (test/debug); returns the
  * count via *count; buf may be NULL to query the size in bytes */
 int hs_program_dump(hs_program* prog, int part, void* buf, size_t buf_bytes,
@@ -215,6 +219,13 @@ int hs_plan_part(int n_local, int dtype, int tile_bits, uint32_t options, const 
 int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options,
                     const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates,
                     void* buf, size_t buf_bytes, size_t* bytes, int* num_launches);
+
+/* host-only: the layouts a program would run with (what
+ * hs_program_initial_layout / hs_program_final_layout report for the same
+ * plan) and its launch count; either array may be NULL */
+int hs_plan_program_layouts(int n_local, int dtype, int tile_bits, uint32_t options, const hs_part* parts,
+                            int num_parts, const hs_gate* gates, int num_gates, int32_t* init_phys,
+                            int32_t* final_phys, int* num_launches);
 
 /* CUDA C++ source of the compiled (HS_PLAN_JIT) kernel of one part, as
  * generated from its plan (host-only; tests compile it with nvcc) */

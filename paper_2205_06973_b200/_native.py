@@ -32,9 +32,9 @@ EXPORTS = (
     "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_initial_layout",
     "hs_program_final_layout",
     "hs_program_bind_scratch",
-    "hs_program_jit_error",
+    "hs_program_jit_error", "hs_jit_cache_stats",
     "hs_program_dump",
-    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_jit_source", "hs_structure_2x2", "hs_dagp_merge", "hs_part_apply",
+    "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_plan_program_layouts", "hs_jit_source", "hs_structure_2x2", "hs_dagp_merge", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
     "hs_pack_segments", "hs_unpack_segments", "hs_pack_segments_range", "hs_unpack_segments_range",
 )
@@ -101,6 +101,7 @@ def _declare(lib) -> None:
         "hs_program_num_parts": (I, [P]),
         "hs_program_num_launches": (I, [P]),
         "hs_program_jit_error": (ctypes.c_char_p, [P]),
+        "hs_jit_cache_stats": (I, [ctypes.POINTER(I), ctypes.POINTER(I)]),
         "hs_program_initial_layout": (I, [P, ctypes.POINTER(ctypes.c_int32)]),
         "hs_program_final_layout": (I, [P, ctypes.POINTER(ctypes.c_int32)]),
         "hs_program_bind_scratch": (I, [P, P, ctypes.c_size_t]),
@@ -113,6 +114,9 @@ def _declare(lib) -> None:
                              P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(HsPartInfo)]),
         "hs_plan_program": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(HsPart), I, ctypes.POINTER(HsGate), I,
                                 P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I)]),
+        "hs_plan_program_layouts": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(HsPart), I, ctypes.POINTER(HsGate),
+                                        I, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                        ctypes.POINTER(I)]),
         "hs_jit_source": (I, [I, I, I, ctypes.c_uint32, ctypes.POINTER(ctypes.c_int32), I, ctypes.POINTER(HsGate), I,
                               ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
         "hs_structure_2x2": (I, [ctypes.POINTER(D), I, ctypes.POINTER(D), ctypes.POINTER(D)]),
@@ -218,3 +222,11 @@ def default_options() -> int:
 def set_default_options(options: int) -> None:
     global _default_options
     _default_options = int(options)
+
+
+def jit_cache_stats() -> dict:
+    """Compiled-part kernels loaded from the on-disk cubin cache vs compiled
+    with NVRTC so far in this process (hs_jit_cache_stats)."""
+    hits, comp = ctypes.c_int(), ctypes.c_int()
+    check(load().hs_jit_cache_stats(ctypes.byref(hits), ctypes.byref(comp)))
+    return {"disk_hits": hits.value, "compiles": comp.value}

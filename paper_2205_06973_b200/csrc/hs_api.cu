@@ -312,6 +312,11 @@ int hs_program_initial_layout(hs_program* prog, int32_t* phys) {
 
 const char* hs_program_jit_error(hs_program* prog) { return prog ? prog->jit_error.c_str() : ""; }
 
+int hs_jit_cache_stats(int* disk_hits, int* compiles) {
+  jit_cache_stats(disk_hits, compiles);
+  return HS_OK;
+}
+
 int hs_program_run(hs_program* prog, void* state, int64_t batch, int first, int count, void* stream) {
   if (!prog || !state) return fail(HS_ERR_INVALID, "program/state is NULL");
   if (batch < 1) return fail(HS_ERR_INVALID, "batch must be >= 1");
@@ -408,6 +413,26 @@ int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options, con
   return HS_OK;
 }
 
+int hs_plan_program_layouts(int n_local, int dtype, int tile_bits, uint32_t options, const hs_part* parts,
+                            int num_parts, const hs_gate* gates, int num_gates, int32_t* init_phys,
+                            int32_t* final_phys, int* num_launches) {
+  if (int s = check_dtype(dtype)) return s;
+  if (num_parts < 0 || (num_parts > 0 && !parts)) return fail(HS_ERR_INVALID, "bad part array");
+  if (tile_bits < 1 || tile_bits > MAX_TILE) return fail(HS_ERR_INVALID, "tile_bits outside [1, 13]");
+  std::vector<PartPlan> plans;
+  std::vector<int32_t> ip, fp;
+  std::string err;
+  int s = plan_program(n_local, dtype, tile_bits, options, parts, num_parts, gates, num_gates, plans, err, &ip,
+                       nullptr, &fp);
+  if (s != HS_OK) return fail(s, err);
+  for (int q = 0; q < n_local; ++q) {
+    if (init_phys) init_phys[q] = q < (int)ip.size() ? ip[q] : q;
+    if (final_phys) final_phys[q] = q < (int)fp.size() ? fp[q] : q;
+  }
+  if (num_launches) *num_launches = (int)plans.size();
+  return HS_OK;
+}
+
 int hs_jit_source(int n_local, int dtype, int tile_bits, uint32_t options, const int32_t* staged, int w,
                   const hs_gate* gates, int num_gates, char* buf, size_t buf_bytes, size_t* bytes) {
   if (int s = check_dtype(dtype)) return s;
@@ -442,12 +467,30 @@ int hs_part_apply(hs_engine* eng, void* state, int64_t batch, int n_local, int d
   for (int j = 0; j < w; ++j) part.staged[j] = staged[j];
   part.gate_offset = 0;
   part.num_gates = num_gates;
+  // a one-shot part never plans an initial layout of its own: the caller's
+  // buffer is in natural order and must be left in natural order
+  const uint32_t saved = eng->options;
+  eng->options &= ~(uint32_t)(HS_PLAN_INIT_LAYOUT | HS_PLAN_NO_RESTORE);
   hs_program* prog = nullptr;
   int s = hs_program_create(eng, n_local, dtype, &part, 1, gates, num_gates, &prog);
+  eng->options = saved;
   if (s != HS_OK) return s;
-  s = hs_program_run(prog, state, batch, 0, 1, stream);
+  void* scratch = nullptr;
+  bool pingpong = false;
+  for (const PartPlan& pl : prog->plans) pingpong |= pl.launch.in_buf || pl.launch.out_buf;
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (pingpong) {  // out-of-place launches: a scratch copy for the program's lifetime
+    const size_t bytes = (size_t(batch) << n_local) * (dtype == HS_C128 ? 16 : 8);
+    cudaError_t e = cudaMallocAsync(&scratch, bytes, cs);
+    if (e != cudaSuccess) { hs_program_destroy(prog); return cuda_fail(e, "cudaMallocAsync scratch"); }
+    hs_program_bind_scratch(prog, scratch, bytes);
+  }
+  // every launch of the plan: a part can take several (tile-sized
+  // sub-passes of a wide part, layout restores, the deferred scalar)
+  s = hs_program_run(prog, state, batch, 0, (int)prog->plans.size(), stream);
+  if (scratch) cudaFreeAsync(scratch, cs);
   if (s == HS_OK) {
-    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    cudaError_t e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) s = cuda_fail(e, "stream sync");
   }
   hs_program_destroy(prog);

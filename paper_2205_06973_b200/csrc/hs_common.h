@@ -79,6 +79,7 @@ struct PartPlan {
 int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, int device, int smem_optin,
                         std::string& err);
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local);
+void jit_cache_stats(int* disk_hits, int* compiles);
 
 // Program-level qubit layout: logical position q (what parts stage) lives at
 // physical bit phys[q] of the buffer. A part's write-back may permute the

@@ -24,6 +24,10 @@
 #include <sstream>
 #include <string>
 #include <thread>
+#include <atomic>
+#include <cstdlib>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <vector>
 
 #include "hs_common.h"
@@ -771,19 +775,116 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
 std::mutex g_cache_mu;
 std::map<std::string, void*> g_cache;  // source -> kernel handle
 
+// ---- on-disk cubin cache. A one-shot execute_hierarchical plans and
+// compiles its parts in every new process; NVRTC is ~0.5-1 s per circuit
+// (parallel over parts) while the planner takes tens of ms. Cubins are kept
+// under $HISVSIM_CACHE_DIR (default $XDG_CACHE_HOME/hisvsim or
+// ~/.cache/hisvsim; "off" disables), keyed by a 64-bit FNV-1a hash of the
+// generated source, the NVRTC options and the NVRTC version; the entry also
+// stores the full source, compared on load, so a hash collision is a miss.
+const char* kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
+
+std::string cache_dir() {
+  const char* d = std::getenv("HISVSIM_CACHE_DIR");
+  if (d && *d) return std::string(d) == "off" ? std::string() : std::string(d);
+  if (const char* x = std::getenv("XDG_CACHE_HOME"); x && *x) return std::string(x) + "/hisvsim";
+  if (const char* h = std::getenv("HOME"); h && *h) return std::string(h) + "/.cache/hisvsim";
+  return std::string();
+}
+
+std::string cache_key(const std::string& src) {
+  int major = 0, minor = 0;
+  nvrtcVersion(&major, &minor);
+  std::string all = src;
+  for (const char* o : kNvrtcOpts) all += std::string("\n//opt ") + o;
+  all += "\n//nvrtc " + std::to_string(major) + "." + std::to_string(minor);
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char ch : all) { h ^= ch; h *= 1099511628211ull; }
+  char buf[32];
+  std::snprintf(buf, sizeof(buf), "%016" PRIx64, h);
+  return buf;
+}
+
+// entry: uint64 source length, source bytes, cubin bytes
+bool cache_load(const std::string& dir, const std::string& key, const std::string& src, std::vector<char>& cubin) {
+  if (dir.empty()) return false;
+  FILE* f = std::fopen((dir + "/" + key + ".cubin").c_str(), "rb");
+  if (!f) return false;
+  bool ok = false;
+  uint64_t n = 0;
+  if (std::fread(&n, sizeof(n), 1, f) == 1 && n == src.size()) {
+    std::string s(n, '\0');
+    if (std::fread(&s[0], 1, n, f) == n && s == src) {
+      std::vector<char> body;
+      char buf[1 << 16];
+      size_t got;
+      while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) body.insert(body.end(), buf, buf + got);
+      if (!body.empty()) { cubin.swap(body); ok = true; }
+    }
+  }
+  std::fclose(f);
+  return ok;
+}
+
+void cache_store(const std::string& dir, const std::string& key, const std::string& src, const std::vector<char>& cubin) {
+  if (dir.empty()) return;
+  // mkdir -p (one level below an existing parent is the common case)
+  for (size_t i = 1; i <= dir.size(); ++i)
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+  char tmp_name[64];
+  std::snprintf(tmp_name, sizeof(tmp_name), ".tmp.%d.%zx", (int)getpid(),
+                std::hash<std::thread::id>()(std::this_thread::get_id()));
+  const std::string tmp = dir + "/" + key + tmp_name, dst = dir + "/" + key + ".cubin";
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  const uint64_t n = src.size();
+  bool ok = std::fwrite(&n, sizeof(n), 1, f) == 1 && std::fwrite(src.data(), 1, n, f) == n &&
+            std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+  ok = (std::fclose(f) == 0) && ok;
+  if (ok) std::rename(tmp.c_str(), dst.c_str());  // atomic: readers see whole entries only
+  else std::remove(tmp.c_str());
+}
+
+std::atomic<int> g_disk_hits{0}, g_compiles{0};
+
+int nvrtc_compile(const std::string& src, std::vector<char>& cubin, std::string& err);
+
 int compile_one(const std::string& src, void** kernel, std::string& err) {
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(src);
     if (it != g_cache.end()) { *kernel = it->second; return HS_OK; }
   }
+  const std::string dir = cache_dir();
+  const std::string key = dir.empty() ? std::string() : cache_key(src);
+  std::vector<char> cubin;
+  if (cache_load(dir, key, src, cubin)) {
+    ++g_disk_hits;
+  } else {
+    int s = nvrtc_compile(src, cubin, err);
+    if (s != HS_OK) return s;
+    ++g_compiles;
+    cache_store(dir, key, src, cubin);
+  }
+  cudaLibrary_t lib;
+  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) { err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e); return HS_ERR_CUDA; }
+  cudaKernel_t k;
+  e = cudaLibraryGetKernel(&k, lib, "hs_jit_part");
+  if (e != cudaSuccess) { err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e); return HS_ERR_CUDA; }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache[src] = (void*)k;
+  *kernel = (void*)k;
+  return HS_OK;
+}
+
+int nvrtc_compile(const std::string& src, std::vector<char>& cubin, std::string& err) {
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "hs_part.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     err = "nvrtcCreateProgram failed";
     return HS_ERR_UNSUPPORTED;
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 3, opts);
+  nvrtcResult r = nvrtcCompileProgram(prog, 3, kNvrtcOpts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
@@ -795,18 +896,9 @@ int compile_one(const std::string& src, void** kernel, std::string& err) {
   }
   size_t sz = 0;
   nvrtcGetCUBINSize(prog, &sz);
-  std::vector<char> cubin(sz);
+  cubin.resize(sz);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
-  cudaLibrary_t lib;
-  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  if (e != cudaSuccess) { err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e); return HS_ERR_CUDA; }
-  cudaKernel_t k;
-  e = cudaLibraryGetKernel(&k, lib, "hs_jit_part");
-  if (e != cudaSuccess) { err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e); return HS_ERR_CUDA; }
-  std::lock_guard<std::mutex> lk(g_cache_mu);
-  g_cache[src] = (void*)k;
-  *kernel = (void*)k;
   return HS_OK;
 }
 
@@ -845,5 +937,10 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
 }
 
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local) { return jit_source(pl, dtype, n_local); }
+
+void jit_cache_stats(int* disk_hits, int* compiles) {
+  if (disk_hits) *disk_hits = g_disk_hits.load();
+  if (compiles) *compiles = g_compiles.load();
+}
 
 }  // namespace hs

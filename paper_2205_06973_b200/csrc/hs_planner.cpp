@@ -1337,6 +1337,9 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     pl.launch.in_buf = cur_buf;
     pl.launch.out_buf = cur_buf ^ 1;
     plans.push_back(pl);
+    // the gate-free launch wrote natural order
+    phys = next;
+    for (int q = 0; q < n_local; ++q) inv[phys[q]] = q;
   }
   if (layout && !pp && !no_restore) {
     int s = plan_restore(n_local, dtype, tile_max, options, phys, plans, err);

@@ -671,16 +671,32 @@ def execute_multilevel(
     return state
 
 
-def execute_parts_as_gates(circuit: Circuit, max_qubits=None, dtype="complex128", device=None) -> StateVector:
-    """Every gate as its own part (``simulate_flat`` on the device)."""
+#: planner options of the independent gate-by-gate run behind
+#: ``simulate_flat`` / ``verify_against_flat``: no single-qubit fusion, no
+#: parity diagonals, no pass merging, no compiled kernels, no layouts - the
+#: interpreter kernel runs each gate as its own pass in natural order, so a
+#: planner or code-generator bug in the hierarchical run cannot verify itself
+FLAT_OPTIONS = 0
+
+
+def flat_program(circuit: Circuit, dtype="complex128", device=None) -> PartProgram:
+    """The gate-by-gate device program: one part, and one launch, per gate."""
     exes = []
     for i, op in enumerate(circuit.ops):
         staged = tuple(sorted(op.qubits))
         exes.append(ExecutablePart(i, (i,), QubitSlotMap(staged), (op,),
                                    (tuple(staged.index(q) for q in op.qubits),)))
+    return PartProgram(circuit.num_qubits, exes, dtype=dtype, device=device, options=FLAT_OPTIONS)
+
+
+def execute_parts_as_gates(circuit: Circuit, max_qubits=None, dtype="complex128", device=None) -> StateVector:
+    """Every gate as its own pass (``simulate_flat`` on the device,
+    statevec.py:269-277): ``FLAT_OPTIONS``, one interpreter launch per gate."""
     state = zero_state(circuit.num_qubits, max_qubits, dtype=dtype, device=device)
-    if exes:
-        PartProgram(circuit.num_qubits, exes, dtype=dtype, device=device).run(state.data)
+    if circuit.ops:
+        prog = flat_program(circuit, dtype=dtype, device=device)
+        assert prog.num_launches == circuit.num_ops
+        prog.run(state.data)
     return state
 
 
@@ -705,11 +721,13 @@ def max_abs_diff(state: StateVector, expect) -> float:
 
 
 def verify_against_flat(circuit: Circuit, state: StateVector, atol: float = 1e-10) -> float:
-    """Compare with a gate-by-gate device run (hier.py:422-436); raises
+    """Compare with the independent gate-by-gate device run (hier.py:422-436;
+    ``FLAT_OPTIONS``: one interpreter pass per gate, none of the planner's
+    merging, fusion, layouts or compiled kernels); raises
     ``VerificationError`` above ``atol``."""
     ref = execute_parts_as_gates(circuit, max_qubits=state.num_qubits, dtype=state.data.dtype,
                                  device=state.data.device)
     err = max_abs_diff(state, ref.data.to(dtype=__import__("torch").complex128))
-    if err > atol:
+    if not err <= atol:
         raise VerificationError(f"max amplitude deviation {err:.3e} exceeds {atol:.1e}")
     return err

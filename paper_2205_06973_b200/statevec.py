@@ -252,9 +252,11 @@ def apply_gate(state: StateVector, op: GateOp) -> None:
 
 
 def simulate_flat(circuit: Circuit, max_qubits: int | None = None, dtype="complex128") -> StateVector:
-    """Gate-by-gate simulation on the device: every gate is its own pass
-    (statevec.py:269-277). The parity oracle is the CPU restatement under
-    ``oracle/``, not this function."""
+    """Gate-by-gate simulation on the device (statevec.py:269-277): every
+    gate is its own interpreter pass with the planner's merging, fusion,
+    layouts and code generation off (``hier.FLAT_OPTIONS``), so it is
+    independent of the hierarchical path it verifies. The parity oracle of
+    the test suite is the CPU restatement under ``oracle/``, not this."""
     from .hier import execute_parts_as_gates
 
     return execute_parts_as_gates(circuit, max_qubits=max_qubits, dtype=dtype)

@@ -157,6 +157,20 @@ def plan_program(native, n_local, dtype, tile_bits, exes, options):
     return out
 
 
+def program_layouts(native, n_local, dtype, tile_bits, exes, options):
+    """hs_plan_program_layouts: (initial layout, final layout, launches)."""
+    from paper_2205_06973_b200.hier import _pack
+
+    parts, gates, total = _pack(exes)
+    lib = native.load()
+    ip = (ctypes.c_int32 * max(1, n_local))()
+    fp = (ctypes.c_int32 * max(1, n_local))()
+    nl = ctypes.c_int()
+    native.check(lib.hs_plan_program_layouts(n_local, dtype, tile_bits, options, parts, len(exes), gates, total, ip,
+                                             fp, ctypes.byref(nl)))
+    return tuple(ip[:n_local]), tuple(fp[:n_local]), nl.value
+
+
 def run_program(psi: np.ndarray, n_local: int, launches) -> np.ndarray:
     """Run a planned program (ping-pong aware) on ``psi``; returns the state
     buffer (``psi`` itself, written in place)."""

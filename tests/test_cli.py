@@ -45,3 +45,41 @@ def test_run_hierarchical_report_trace_state(tmp_path, golden):
     assert cli.main(["run", "c1@12", "--mode", "distributed", "--p", "2", "--limit", "6", "--verify"]) == 0
     assert cli.main(["run", "c1@12", "--mode", "multilevel", "--l1", "8", "--l2", "4", "--verify"]) == 0
     assert cli.main(["run", "c1@12", "--mode", "flat", "--trace", str(tr)]) == 1  # usage
+
+
+@pytest.mark.gpu
+def test_verification_failure_is_exit_three(capsys, monkeypatch):
+    """The reference's fault injection (tests/test_cli.py:62-79): a
+    corrupted executor must fail --verify with exit code 3, which only
+    holds because verify compares against the independent gate-by-gate run."""
+    from paper_2205_06973_b200 import hier
+
+    real = hier.execute_hierarchical
+
+    def corrupted(circuit, partition, **kwargs):
+        out = real(circuit, partition, **kwargs)
+        state = out[0] if isinstance(out, tuple) else out
+        state.data[0] += 0.5
+        return out
+
+    monkeypatch.setattr(hier, "execute_hierarchical", corrupted)
+    code = cli.main(["run", "c1@12", "--mode", "hierarchical", "--limit", "6", "--verify"])
+    assert code == 3
+    assert "delta" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_verify_runs_one_interpreter_launch_per_gate():
+    """verify_against_flat's reference run is the literal gate-by-gate
+    program: as many launches as gates, none compiled, natural order."""
+    from paper_2205_06973_b200 import build_dag, configs, partition_dfs
+    from paper_2205_06973_b200.hier import execute_hierarchical, flat_program, verify_against_flat
+
+    for name in ("c2@20", "c3@20"):
+        c = configs.build(name)
+        prog = flat_program(c)
+        assert prog.num_launches == c.num_ops
+        assert prog.initial_layout == prog.final_layout == tuple(range(c.num_qubits))
+        assert not any(prog.info(i)["compiled"] for i in range(prog.num_launches))
+        st = execute_hierarchical(c, partition_dfs(build_dag(c), 12))
+        assert verify_against_flat(c, st) < 1e-10

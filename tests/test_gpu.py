@@ -600,3 +600,41 @@ def test_bv30_known_answer():
         d[s] = 0
         d[s + (1 << anc)] = 0
         assert float(d.abs().max()) < 1e-12
+
+
+@pytest.mark.parametrize("w", [9, 13, 14])
+def test_part_apply_c_abi_runs_every_launch(w):
+    """hs_part_apply (the C ABI's run_part) on parts whose plan takes
+    several launches (w = 13 / 14: tile-sized sub-passes; LAYOUT adds
+    restore launches, PINGPONG out-of-place launches, JIT defers the part's
+    scalar to the last launch), compared with the oracle's run_part on a
+    random batched state."""
+    import ctypes
+
+    from paper_2205_06973_b200.hier import _pack
+
+    n, rows = 17, 2
+    c = configs.build("c2@17")
+    part = partition_dfs(build_dag(c), w).parts[0]
+    exe = remap_part(c, part)
+    assert exe.num_slots == w
+    rng = np.random.default_rng(w)
+    data = rng.normal(size=(rows, 1 << n)) + 1j * rng.normal(size=(rows, 1 << n))
+    want = data.copy()
+    orc.run_part(want, exe.slot_map.qubits, exe.ops, exe.op_slots)
+    lib = _native.load()
+    eng = _native.engine(0)
+    _, gates, total = _pack([exe])
+    st = (ctypes.c_int32 * w)(*exe.slot_map.qubits)
+    base = _native.HS_PLAN_DEFAULT
+    J, L = _native.HS_PLAN_JIT, _native.HS_PLAN_LAYOUT
+    for opts in (base, base | L, base | J, base | J | L, base | J | L | _native.HS_PLAN_PINGPONG,
+                 base | J | L | _native.HS_PLAN_INIT_LAYOUT | _native.HS_PLAN_NO_RESTORE):
+        dev = torch.from_numpy(data.copy()).cuda()
+        s = torch.cuda.current_stream().cuda_stream
+        _native.check(lib.hs_engine_set_options(eng, opts))
+        try:
+            _native.check(lib.hs_part_apply(eng, dev.data_ptr(), rows, n, 0, st, w, gates, total, s))
+        finally:
+            lib.hs_engine_set_options(eng, _native.default_options())
+        assert float(np.max(np.abs(dev.cpu().numpy() - want))) < 1e-10, hex(opts)

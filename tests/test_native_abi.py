@@ -377,3 +377,41 @@ def test_merged_programs_match_oracle_on_corpus(golden, options):
             assert np.max(np.abs(psi[0] - states[f"c{i}"])) < 1e-12, (i, key)
             checked += 1
     assert checked >= 40
+
+
+@pytest.mark.parametrize("name,limit", [("c2@20", 12), ("c3@16", 9), ("c1@14", 6), ("c4@13", 6)])
+def test_final_layout_is_natural_unless_no_restore(name, limit):
+    """hs_program_final_layout's contract: the identity whenever
+    HS_PLAN_NO_RESTORE is off, for in-place and ping-pong programs alike
+    (including a ping-pong program that ends in a gate-free permutation
+    launch); with it on, the layout the emulated program actually left."""
+    c = configs.build(name)
+    n = c.num_qubits
+    exes = [remap_part(c, p) for p in partition_dfs(build_dag(c), limit).parts]
+    base = 5 | 0x8  # FUSE_1Q | PARITY | LAYOUT
+    for extra in (0, 0x40, 0x40 | 0x400, 0x20, 0x20 | 0x40):
+        ip, fp, nl = emu.program_layouts(_native, n, 0, 12, exes, base | extra)
+        assert fp == tuple(range(n)), (extra, fp)
+        assert nl == len(emu.plan_program(_native, n, 0, 12, exes, base | extra))
+    # a 2-part ping-pong program whose last part misses the low positions:
+    # the restore launch writes natural order, and the final layout says so
+    from paper_2205_06973_b200.partition import Part
+
+    ops = [GateOp(GateKind.H, (q,), ()) for q in range(20)]
+    cc = Circuit(20, tuple(ops))
+    two = [remap_part(cc, Part(0, tuple(range(0, 12)), tuple(range(0, 12)))),
+           remap_part(cc, Part(1, tuple(range(12, 20)), tuple(range(8, 20))))]
+    ip, fp, nl = emu.program_layouts(_native, 20, 0, 12, two, base | 0x40)
+    assert nl == 3 and fp == tuple(range(20))
+    # NO_RESTORE: the reported layout is where the emulated amplitudes are
+    ip, fp, nl = emu.program_layouts(_native, n, 0, 12, exes, base | 0x100)
+    launches = emu.plan_program(_native, n, 0, 12, exes, base | 0x100)
+    psi = np.zeros((1, 1 << n), dtype=np.complex128)
+    psi[0, 0] = 1
+    emu.run_program(psi, n, launches)
+    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in partition_dfs(build_dag(c), limit).parts])
+    idx = np.arange(1 << n, dtype=np.int64)
+    where = np.zeros_like(idx)
+    for q in range(n):
+        where |= ((idx >> q) & 1) << fp[q]
+    assert np.max(np.abs(psi[0][where] - want)) < 1e-12
