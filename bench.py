@@ -1,19 +1,28 @@
 """Benchmark: circuit time-to-solution and effective HBM GB/s per part-pass.
 
-One step = one full simulation of the BASELINE config circuit (every part
-of its partition, one kernel pass each) on a state already resident in HBM.
-``value`` = algorithmic part-pass bytes of all ranks / step time, where a
-part-pass moves 2 x 2^l x 16 B (read + write of a rank's shard, SURVEY.md
-§8(d)); ``ms_per_step`` is the circuit time-to-solution (partitioning, done
-once on the host, is reported separately). ``e2e`` is the same metric
-through the public API with the initial state in pinned host memory and the
-final state read back every step.
+One step = one full simulation of the BASELINE config circuit on a state
+already resident in HBM: every tile pass the planner made of the
+partition's parts (csrc/hs_planner.cpp group_passes), plus any gate-free
+layout launch. ``value`` = HBM bytes the step's launches move (each launch
+reads and writes every amplitude of a rank's shard: 2 x 2^l x 16 B) / step
+time, summed over ranks, so it can never exceed the HBM peak; the metric's
+per-part-pass figure (parts x 2 x 2^l x 16 B / time, a time-to-solution in
+bandwidth units, comparable with the reference arm) is reported beside it
+as ``part_pass_equivalent_gbs``. ``ms_per_step`` is the circuit
+time-to-solution; partitioning and planning (host) are reported
+separately. ``e2e`` is the same metric through the public API with the
+initial state in pinned host memory and the final state read back every
+step. ``one_pass_per_part`` times the literal reference granularity (one
+pass per part, HS_PLAN_PART_LOCAL, no merging) beside the default.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--strategy dfs]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--strategy dfs]
     python bench.py --impl reference ...   # the CPU port of the reference path
 
-Under torchrun (N > 1) the state is sharded over the N ranks (n + log2 N
-qubits, weak scaling) and layout switches run over NCCL.
+Workloads per N (paper_2205_06973_b200.configs.bench_workload): c1 / c2 /
+c3 weak-scale to n + log2 N qubits, c4 is 33 qubits at every N (strong),
+c5 is 33 / 34 / 35 / 36 qubits at 1 / 2 / 4 / 8 GPUs. Under torchrun
+(N > 1) the state is sharded over the ranks and layout switches run over
+NCCL.
 """
 
 from __future__ import annotations
@@ -117,13 +126,12 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def build_workload(config: str, strategy: str, extra_bits: int = 0, limit: int | None = None):
+def build_workload(name: str, strategy: str, limit: int | None = None):
+    """Circuit + partition of a bench workload (``configs.bench_workload``'s
+    circuit name) and the host partitioning time."""
     from paper_2205_06973_b200 import build_dag, configs, partition_dagp, partition_dfs, partition_nat
 
-    cfg = configs.CONFIGS[config.split("@")[0]]
-    name = config
-    if extra_bits:
-        name = f"{config.split('@')[0]}@{cfg.num_qubits + extra_bits}"
+    cfg = configs.CONFIGS[name.split("@")[0]]
     circuit = configs.build(name)
     t0 = time.perf_counter()
     fn = {"nat": partition_nat, "dfs": partition_dfs, "dagp": partition_dagp}[strategy]
@@ -134,7 +142,7 @@ def build_workload(config: str, strategy: str, extra_bits: int = 0, limit: int |
 
 # --------------------------------------------------------------------------- CPU reference arm
 
-def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup, quiet=False):
+def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup):
     """The reference path's CPU restatement (oracle/sv_oracle.c, all host
     threads) on a bounded sample of fixings of every part."""
     import numpy as np
@@ -197,23 +205,94 @@ def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup, quiet=False):
     }
 
 
+def numpy_port_c1_seconds():
+    """The reference's own numpy algorithm (oracle/hisim_oracle.py, a
+    restatement of hisim.hier.execute_hierarchical: per part one batched
+    fancy-index gather, numpy ufunc gates, scatter) on c1 (20 qubits, dfs,
+    k = 10), one core: the reference CPU path's speed at the one BASELINE
+    config it runs in seconds (the C port above is the stronger baseline)."""
+    from oracle import hisim_oracle as orc
+    from paper_2205_06973_b200 import build_dag, configs, partition_dfs
+
+    c = configs.build("c1")
+    parts = [(p.gate_indices, p.qubits) for p in partition_dfs(build_dag(c), 10).parts]
+    t0 = time.perf_counter()
+    orc.execute_hierarchical(c, parts)
+    return time.perf_counter() - t0
+
+
 def config_label(args):
-    return f"{args.config}/{args.strategy}"
+    return f"{args.workload}/{args.strategy}"
 
 
 # --------------------------------------------------------------------------- GPU arm
 
-def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
-    import numpy as np
+def plan_probe(args) -> int:
+    """--plan-probe: plan + compile the workload's program in this (fresh)
+    process and print the host seconds it took (the disk cubin cache is
+    whatever HISVSIM_CACHE_DIR holds)."""
     import torch
 
-    from paper_2205_06973_b200.hier import HierarchicalRun, execute_hierarchical
+    from paper_2205_06973_b200 import _native
+    from paper_2205_06973_b200.hier import HierarchicalRun
+
+    _, circuit, part, _ = build_workload(args.workload, args.strategy, args.limit)
+    torch.cuda.init()
+    _native.engine(0)
+    t0 = time.perf_counter()
+    HierarchicalRun(circuit, part, device="cuda:0", options=args.plan_options, basis_start=True)
+    dt = time.perf_counter() - t0
+    print(json.dumps({"plan_seconds": dt, "jit": _native.jit_cache_stats()}), flush=True)
+    return 0
+
+
+def _warm_plan_seconds(args):
+    """Plan time of the same program in a second process that finds the
+    cubins this process compiled in the on-disk cache."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--plan-probe", "--config", args.config, "--strategy",
+           args.strategy]
+    if args.limit:
+        cmd += ["--limit", str(args.limit)]
+    if args.plan_options is not None:
+        cmd += ["--plan-options", hex(args.plan_options)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ))
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # reported, never fatal for the bench line
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
+def _time_program(run, state, steps, launch, stream):
+    """Device ms per step of ``launch`` over ``steps`` steps, each step's
+    basis state prepared outside the timed window (events on the launch
+    stream)."""
+    import torch
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in ev:
+        run.program.init_basis(state, 0)
+        e0.record(stream)
+        launch(state)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return sum(e0.elapsed_time(e1) for e0, e1 in ev) / steps
+
+
+def gpu_arm(args, circuit, part, rank, world):
+    import torch
+
+    from paper_2205_06973_b200 import _native
+    from paper_2205_06973_b200.hier import HierarchicalRun
     from paper_2205_06973_b200.statevec import allocate, init_basis
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
+    _native.engine(dev.index or 0)
     n = circuit.num_qubits
     dist = world > 1
+    # host planning: the planner + NVRTC code generation of every pass
+    # (cold: this process's own cubin cache directory starts empty)
+    t0 = time.perf_counter()
     if dist:
         from paper_2205_06973_b200.multi import ShardedRun
 
@@ -223,9 +302,11 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         # the timed runs start from |0..0>, prepared in the program's layout
         run = HierarchicalRun(circuit, part, device=dev, options=args.plan_options, basis_start=True)
         n_local = n
+    plan_s = time.perf_counter() - t0
+    jit_stats = _native.jit_cache_stats()
     num_parts = part.num_parts
-    num_launches = (run.program.num_launches if not dist
-                    else sum(pr.num_launches for pr in run.programs if pr is not None))
+    programs = [run.program] if not dist else [pr for pr in run.programs if pr is not None]
+    num_launches = sum(pr.num_launches for pr in programs)
     bytes_per_pass = 2 * (1 << n_local) * 16
     launch_owner = [run.program.info(j)["user_part"] for j in range(num_launches)] if not dist else []
     state = allocate(n_local, "complex128", dev)
@@ -234,19 +315,22 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     # the whole program as one CUDA graph launch (PartProgram.run_graph,
     # captured in the warm-up) unless --no-graph: launch overhead matters for
     # L2-resident states (c1: 7 launches of ~16 us)
-    def launch(buf):
+    def launch(buf, r=run):
         if args.no_graph:
-            run.program.run(buf)
+            r.program.run(buf)
         else:
-            run.program.run_graph(buf, stream=stream)
+            r.program.run_graph(buf, stream=stream)
 
-    def one_step(timed_events=None):
+    def prepare():
         if not dist:
             run.program.init_basis(state, 0)
         elif rank == 0:
             init_basis(state, 0)
         else:
             state.zero_()
+
+    def one_step(timed_events=None):
+        prepare()
         if timed_events is not None:
             timed_events.append(torch.cuda.Event(enable_timing=True))
             timed_events[-1].record(stream)
@@ -272,18 +356,13 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
     clocks.start()
     # K timed steps: each step's initial state is prepared first (t_init,
     # reported apart: the input is resident when the hot path starts), then
-    # all parts (and switches) run between two events on the launch stream
+    # all launches (and switches) run between two events on the launch stream
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
                 torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
     for e_init, e0, e1 in step_ev:
         e_init.record(stream)
-        if not dist:
-            run.program.init_basis(state, 0)
-        elif rank == 0:
-            init_basis(state, 0)
-        else:
-            state.zero_()
+        prepare()
         e0.record(stream)
         if dist:
             run.run(state)
@@ -302,19 +381,22 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         marks.append(ev)
     torch.cuda.synchronize()
     n_marked = len(marks)
-    # per-launch durations of the part kernel (events between launches);
-    # distributed: per segment ("parts") and per layout switch ("switch")
-    durs, restore_ms, switch_ms, seg_ms = [], 0.0, 0.0, 0.0
+    # per launch of the part kernel (events between launches); distributed:
+    # per segment ("parts") and per layout switch ("switch")
+    durs, restore_ms, seg_ms = [], 0.0, 0.0
+    switch_list = []  # ms of each switch, per marked step
     launch_ms = []  # per launch, per marked step
     for ev in marks:
         if dist:
+            sw = []
             for i in range(1, len(ev)):
                 kind, e = ev[i]
                 prev = ev[i - 1][1] if isinstance(ev[i - 1], tuple) else ev[i - 1]
                 if kind == "switch":
-                    switch_ms += prev.elapsed_time(e)
+                    sw.append(prev.elapsed_time(e))
                 else:
                     seg_ms += prev.elapsed_time(e)
+            switch_list.append(sw)
             continue
         d = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)]
         launch_ms.append(d)
@@ -333,7 +415,29 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_step = total_ms / args.steps
-    value = world * num_parts * bytes_per_pass / (ms_step / 1e3) / 1e9
+    moved = world * num_launches * bytes_per_pass  # HBM bytes of all ranks' launches per step
+    value = moved / (ms_step / 1e3) / 1e9
+
+    # the literal reference granularity: one pass per part (no merging or
+    # regrouping of parts into tile passes), same layouts / JIT / graph
+    literal = None
+    if not dist and not args.no_literal:
+        opts = (run.program.options & ~_native.HS_PLAN_MERGE) | _native.HS_PLAN_PART_LOCAL
+        lit = HierarchicalRun(circuit, part, device=dev, options=opts, basis_start=True)
+        if lit.program.needs_scratch and run.program.needs_scratch:
+            lit.program.share_scratch(run.program._scratch)
+        for _ in range(max(1, args.warmup)):
+            lit.program.init_basis(state, 0)
+            launch(state, lit)
+        lit_ms = _time_program(lit, state, args.steps, lambda b: launch(b, lit), stream)
+        nl = lit.program.num_launches
+        literal = {"ms_per_step": lit_ms, "launches_per_step": nl, "parts": num_parts,
+                   "value": nl * bytes_per_pass / (lit_ms / 1e3) / 1e9, "unit": UNIT,
+                   "part_pass_equivalent_gbs": num_parts * bytes_per_pass / (lit_ms / 1e3) / 1e9,
+                   "options": hex(opts),
+                   "note": "HS_PLAN_PART_LOCAL without HS_PLAN_MERGE: every launch carries one part's gates "
+                           "(plus gate-free layout launches); the default regroups parts into tile passes"}
+        del lit
 
     # e2e through the public API: host initial state in, host state out
     e2e = None
@@ -367,74 +471,91 @@ def gpu_arm(args, cfg, circuit, part, t_part, rank, world):
         t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e_ms = float(t.item())
-        e2e = {"value": world * num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
-               "launches_per_step": sum(pr.num_launches for pr in run_e2e.programs if pr is not None),
-               "ms_per_step": e_ms, "h2d_bytes_per_step": world * (1 << n_local) * 16,
-               "d2h_bytes_per_step": world * (1 << n_local) * 16,
+        nl_e2e = sum(pr.num_launches for pr in run_e2e.programs if pr is not None)
+        e2e = {"value": world * nl_e2e * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
+               "part_pass_equivalent_gbs": world * num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9,
+               "launches_per_step": nl_e2e, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": world * (1 << n_local) * 16, "d2h_bytes_per_step": world * (1 << n_local) * 16,
                "path": "public API ShardedRun.run per rank: shard uploaded from pinned host, every part and "
                        "layout switch, shard downloaded; max over ranks"}
     if not dist and not args.no_e2e:
-        # a caller's initial state arrives in natural order: the e2e program
-        # is planned without an initial layout of its own
-        run_e2e = HierarchicalRun(circuit, part, device=dev, options=args.plan_options, basis_start=False)
-        # pinned host inputs / outputs alternate; three device buffers let
-        # the streams overlap step i+1's upload, step i's parts and step
-        # i-1's download
-        host_in = [torch.zeros(1 << n, dtype=torch.complex128).pin_memory() for _ in range(2)]
-        for h in host_in:
-            h[0] = 1.0
-        host_out = [torch.empty(1 << n, dtype=torch.complex128).pin_memory() for _ in range(2)]
-        bufs = [state, torch.empty_like(state), torch.empty_like(state)]
+        shard_bytes = (1 << n) * 16
+        if shard_bytes > E2E_MAX_STATE_BYTES:
+            e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                   "skipped": f"a {shard_bytes >> 30} GiB state needs three device buffers and two pinned host "
+                              f"buffers of its size for the overlapped stream (host RAM); measured up to "
+                              f"{E2E_MAX_STATE_BYTES >> 30} GiB"}
+        else:
+            # a caller's initial state arrives in natural order: the e2e
+            # program is planned without an initial layout of its own
+            run_e2e = HierarchicalRun(circuit, part, device=dev, options=args.plan_options, basis_start=False)
+            if run_e2e.program.needs_scratch and run.program.needs_scratch:
+                run_e2e.program.share_scratch(run.program._scratch)
+            # one pinned host input and one output (16 GiB each at c3);
+            # three device buffers let the streams overlap step i+1's
+            # upload, step i's passes and step i-1's download
+            host_in = torch.zeros(1 << n, dtype=torch.complex128).pin_memory()
+            host_in[0] = 1.0
+            host_out = torch.empty(1 << n, dtype=torch.complex128).pin_memory()
+            bufs = [state, torch.empty_like(state), torch.empty_like(state)]
 
-        def e2e_steps(k):
-            run_e2e.run_stream([host_in[i % 2] for i in range(k)], [host_out[i % 2] for i in range(k)],
-                               buffers=bufs, stream=stream)
+            def e2e_steps(k):
+                run_e2e.run_stream([host_in] * k, [host_out] * k, buffers=bufs, stream=stream)
 
-        e2e_steps(max(2, args.warmup))
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        e2e_steps(args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1) / args.steps
-        for h in host_out:
-            assert abs(float(h.abs().pow(2).sum()) - 1.0) < 1e-9
-        e2e = {"value": num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
-               "launches_per_step": run_e2e.program.num_launches,
-               "ms_per_step": e_ms, "h2d_bytes_per_step": (1 << n) * 16, "d2h_bytes_per_step": (1 << n) * 16,
-               "path": "public API HierarchicalRun.run_stream: each step uploads an initial state from pinned host, "
-                       "runs every part and downloads the final state; upload/parts/download of consecutive "
-                       "steps overlap on three streams over three device buffers"}
+            e2e_steps(max(2, args.warmup))
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_steps(args.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e_ms = e0.elapsed_time(e1) / args.steps
+            assert abs(float(host_out.abs().pow(2).sum()) - 1.0) < 1e-9
+            nl_e2e = run_e2e.program.num_launches
+            e2e = {"value": nl_e2e * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
+                   "part_pass_equivalent_gbs": num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9,
+                   "launches_per_step": nl_e2e, "ms_per_step": e_ms, "h2d_bytes_per_step": shard_bytes,
+                   "d2h_bytes_per_step": shard_bytes,
+                   "path": "public API HierarchicalRun.run_stream: each step uploads an initial state from pinned "
+                           "host, runs every pass and downloads the final state; upload/passes/download of "
+                           "consecutive steps overlap on three streams over three device buffers"}
+            del bufs, run_e2e
 
     info = ([run.program.info(i) for i in range(num_launches)] if not dist else run.part_infos())
     # FP64 roofline: issued FP64 pipe work of the part kernels vs a measured DFMA peak
     import ctypes
 
-    from paper_2205_06973_b200 import _native
-
     peak = ctypes.c_double()
     _native.check(_native.load().hs_fp64_peak(ctypes.byref(peak), stream.cuda_stream))
     fp64_instr = sum(i["fp64_instr_per_amp"] for i in info) * (1 << n_local)
     part_ms = sum(durs) / n_marked if durs else (seg_ms / n_marked if dist else ms_step)
-    fp64 = {"bound_note": "random-circuit parts are FP64-bound, not HBM-bound (SURVEY.md 7.3)",
+    fp64 = {"bound_note": "random-circuit passes are FP64-bound, not HBM-bound (SURVEY.md 7.3)",
             "instr_per_step": fp64_instr, "achieved_tflops": 2 * fp64_instr / (part_ms / 1e3) / 1e12,
             "peak_tflops_measured": peak.value,
             "frac": (2 * fp64_instr / (part_ms / 1e3) / 1e12) / peak.value if peak.value else None,
             "part_kernel_ms_per_step": part_ms}
+    comm = None
+    if dist:
+        sw = [sum(c) / len(c) for c in zip(*switch_list)] if switch_list and switch_list[0] else []
+        sw_ms = sum(sw)
+        comm = dict(run.comm_summary(), switch_ms_per_step=sw_ms, per_switch_ms=[round(x, 4) for x in sw],
+                    parts_ms_per_step=seg_ms / n_marked,
+                    nvlink_gbs_per_rank=(run.stats.total_bytes / world / (sw_ms / 1e3) / 1e9 if sw_ms > 0 else None),
+                    nvlink_note="bytes each rank sends over all switches (closed-form CommStats / ranks) / switch time")
     return {
-        "ms_step": ms_step, "value": value, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
+        "ms_step": ms_step, "value": value, "moved": moved, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
         "launch_ms": [sum(c) / len(c) for c in zip(*launch_ms)] if launch_ms else [],
         "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
-        "num_launches": num_launches, "restore_ms_per_step": restore_ms / n_marked, "fp64": fp64,
-        "init_ms_per_step": init_ms,
-        "comm": (dict(run.comm_summary(), switch_ms_per_step=switch_ms / n_marked,
-                      parts_ms_per_step=seg_ms / n_marked,
-                      nvlink_gbs_per_rank=(run.stats.total_bytes / world / (switch_ms / n_marked / 1e3) / 1e9
-                                           if switch_ms > 0 else None))
-                 if dist else None),
+        "num_launches": num_launches, "restore_ms_per_step": restore_ms / n_marked if n_marked else 0.0,
+        "fp64": fp64, "init_ms_per_step": init_ms, "plan_s": plan_s, "jit": jit_stats, "literal": literal,
+        "comm": comm,
     }
+
+
+#: largest single-GPU state the e2e leg streams (three device buffers, two
+#: pinned host buffers of the state's size)
+E2E_MAX_STATE_BYTES = 32 << 30
 
 
 def main(argv=None):
@@ -443,12 +564,13 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3", help="BASELINE config (c1 .. c5; c3 is the largest single-GPU one)")
     ap.add_argument("--strategy", default="dfs", choices=["nat", "dfs", "dagp"])
     ap.add_argument("--limit", type=int, default=None, help="part size k (default: the config's)")
     ap.add_argument("--cpu-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-literal", action="store_true", help="skip the one-pass-per-part comparison run")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the program's kernels one by one instead of as one CUDA graph")
     ap.add_argument("--plan-add", type=lambda x: int(x, 0), default=0,
@@ -456,16 +578,24 @@ def main(argv=None):
     ap.add_argument("--plan-options", type=lambda x: int(x, 0), default=None,
                     help="planner option bits (HS_PLAN_*) of the single-GPU program (default: the engine "
                          "default + JIT + LAYOUT, chosen by state size)")
+    ap.add_argument("--no-warm-plan", action="store_true", help="skip the second-process planning probe")
+    ap.add_argument("--plan-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
     if args.plan_add:
         from paper_2205_06973_b200 import _native
 
         _native._default_options |= args.plan_add
-    if args.warmup < 3:
+    if args.warmup < 3 and not args.plan_probe:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    from paper_2205_06973_b200 import configs
+
+    args.workload, scaling = configs.bench_workload(args.config, max(world, args.gpus if args.impl == "reference"
+                                                                      else world))
+    if args.plan_probe:
+        return plan_probe(args)
     if world > 1:
         import torch.distributed as tdist
 
@@ -474,85 +604,102 @@ def main(argv=None):
                 return 0
         else:
             tdist.init_process_group("nccl")
-    # weak scaling: n + log2 N qubits (the reference arm times the same
-    # workload on rank 0's host cores)
-    extra = int(math.log2(world)) if world > 1 else 0
     if args.impl == "reference":
         world = 1
-    cfg, circuit, part, t_part = build_workload(args.config, args.strategy, extra, args.limit)
+    cfg, circuit, part, t_part = build_workload(args.workload, args.strategy, args.limit)
     n = circuit.num_qubits
-    config = {"workload": f"{args.config}: {cfg.description}" + (f", scaled to {n} qubits" if extra else ""),
-              "num_qubits": n, "limit": args.limit or cfg.limit, "strategy": args.strategy, "parts": part.num_parts,
-              "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
-              "state_bytes_per_gpu": (1 << (n - extra)) * 16,
-              "l2_policy": "inputs larger than L2: the state (>= 1 GiB) exceeds the 126 MB L2",
-              "partition_seconds_host": round(t_part, 4), "plan_add": hex(args.plan_add),
-              "launch": "per-kernel" if (args.no_graph or world > 1) else "one CUDA graph per step (PartProgram.run_graph)", "parallelism": (f"qubit-sharded x{world}" if world > 1 else "single GPU") if args.impl != "reference"
-              else f"host CPU threads (rank 0 of {args.gpus})"}
+    gpus = args.gpus if args.impl == "reference" else world
+    p_bits = int(math.log2(gpus))
+    config = {"workload": f"{args.workload}: {cfg.description}" + (f", at {n} qubits" if args.workload != cfg.name
+                                                                    else ""),
+              "config": args.config, "num_qubits": n, "limit": args.limit or cfg.limit, "strategy": args.strategy,
+              "parts": part.num_parts, "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
+              "state_bytes_per_gpu": (1 << (n - p_bits)) * 16,
+              "l2_policy": ("inputs larger than L2: the state exceeds the 126 MB L2" if (1 << (n - p_bits)) * 16 > (126 << 20)
+                            else "L2-resident state (16 MiB c1): no flush between steps"),
+              "partition_seconds_host": round(t_part, 4),
+              "parallelism": f"qubit-sharded x{gpus}" if gpus > 1 else "single GPU"}
 
     if args.impl == "reference":
         r = cpu_arm(args, cfg, circuit, part, t_part, args.steps, args.warmup)
+        np_c1 = numpy_port_c1_seconds()
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
                 "config": config, "impl": "reference",
                 "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
-                                 "sample": r["sample"]},
+                                 "sample": r["sample"], "numpy_port_c1_seconds": np_c1},
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "projected_time_to_solution_s": r["projected_time_to_solution_s"]}
+                "part_pass_equivalent_gbs": r["value"],
+                "projected_time_to_solution_s": r["projected_time_to_solution_s"],
+                "note": "host CPU, rank 0 only: the C restatement of the reference's per-part gather/gates/scatter "
+                        "(oracle/sv_oracle.c; the reference is pure Python/numpy and compiles to nothing) on every "
+                        "host thread over a bounded sample of each part's fixings; numpy_port_c1_seconds = the "
+                        "reference's numpy algorithm (oracle/hisim_oracle.py) on all of c1, one core"}
         print(json.dumps(line), flush=True)
         return 0
 
-    g = gpu_arm(args, cfg, circuit, part, t_part, rank, world)
+    # cold planning: a fresh on-disk cubin cache for this process
+    if "HISVSIM_CACHE_DIR" not in os.environ:
+        import tempfile
+
+        os.environ["HISVSIM_CACHE_DIR"] = tempfile.mkdtemp(prefix="hisvsim_bench_cache_")
+    g = gpu_arm(args, circuit, part, rank, world)
     if rank != 0:
         return 0
+    warm = _warm_plan_seconds(args) if world == 1 and not args.no_warm_plan else None
     peak, peak_kind = _peaks()
     durs = g["durations_ms"]
-    # average duration of a launch that carries gates over the timed region:
-    # the timed part time less the gate-free layout launches (their share
-    # from the event pass). Wide parts take several launches (sub-passes,
-    # regrouped across parts), so a launch is not always a part: the per
-    # part-pass figure (value's unit) is reported beside it.
-    gate_launches = (sum(1 for i in g["info"] if i["user_part"] >= 0) if world == 1 else g["num_parts"])
-    avg_ms = (g["ms_step"] - g["restore_ms_per_step"]) / max(1, gate_launches)
-    part_pass_ms = (g["ms_step"] - g["restore_ms_per_step"]) / g["num_parts"]
+    # average duration of a launch over the timed region (every launch is one
+    # pass over the shard: tile passes and gate-free layout launches alike)
+    avg_ms = g["ms_step"] / max(1, g["num_launches"])
     achieved = g["bytes_per_pass"] / (avg_ms / 1e3) / 1e9
-    traffic = _traffic_from_profiles(args.config, args.strategy)
+    traffic = _traffic_from_profiles(args.workload, args.strategy)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "kernel": "compiled part kernel (one launch = one pass over the state)",
+                "kernel": "compiled part kernel hs_jit_part (one launch = one pass over the shard)",
                 "algorithmic_bytes_per_launch": g["bytes_per_pass"],
-                "avg_launch_ms": avg_ms, "gate_launches_per_step": gate_launches,
+                "avg_launch_ms": avg_ms, "launches_per_step": g["num_launches"],
+                "gate_launches_per_step": sum(1 for i in g["info"] if i["user_part"] >= 0),
                 "part_passes_per_step": g["num_parts"],
-                "effective_gbs_per_part_pass": g["bytes_per_pass"] / (part_pass_ms / 1e3) / 1e9,
-                "avg_launch_ms_event_pass": (sum(durs) / len(durs)) if durs else None,
                 "per_part_gbs": [g["bytes_per_pass"] / (d / 1e3) / 1e9 if d > 0 else None
                                  for d in durs[: g["num_parts"]]],
                 "per_launch_ms": [round(x, 4) for x in g["launch_ms"]],
                 "per_launch_gbs": [round(g["bytes_per_pass"] / (x / 1e3) / 1e9, 1) for x in g["launch_ms"] if x > 0]}
     infos = g["info"]
     flops = sum(i["fp_ops_per_amp"] for i in infos) * (1 << g["n_local"])
-    # binding roofline per part: max(bytes / HBM peak, FP64
+    # binding roofline per launch: max(bytes / HBM peak, FP64
     # instructions / measured DFMA rate); its sum over the circuit vs the
-    # measured part time
+    # measured step
     fp_rate = g["fp64"]["peak_tflops_measured"] * 1e12 / 2  # instructions/s (FMA = 2 flops)
     bind_ms = 0.0
-    for i in (infos if world == 1 else []):  # every launch is one pass over the state
+    for i in (infos if world == 1 else []):
         ins = i["fp64_instr_per_amp"] * (1 << g["n_local"])
         bind_ms += max(g["bytes_per_pass"] / (peak * 1e9), ins / fp_rate if fp_rate else 0.0) * 1e3
     if world == 1:
         roofline["binding"] = {"what": "sum over launches of max(HBM bytes / peak, FP64 instructions / measured DFMA rate)",
-                             "bound_ms_per_step": bind_ms, "measured_ms_per_step": g["ms_step"],
-                             "frac": bind_ms / g["ms_step"]}
+                               "bound_ms_per_step": bind_ms, "measured_ms_per_step": g["ms_step"],
+                               "frac": bind_ms / g["ms_step"]}
+    pp_equiv = world * g["num_parts"] * g["bytes_per_pass"] / (g["ms_step"] / 1e3) / 1e9
     line = {"metric": METRIC, "value": g["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": g["ms_step"], "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": g["ms_step"], "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
-            "config": config, "roofline": roofline, "clocks": g["clocks"],
-            "gpu_launches": args.steps * g["num_launches"] + (args.steps * g["e2e"]["launches_per_step"] if g["e2e"] else 0),
+            "config": config,
+            "launch": ("per-kernel" if (args.no_graph or world > 1) else "one CUDA graph per step (PartProgram.run_graph)"),
+            "plan_add": hex(args.plan_add),
+            "value_definition": "HBM bytes moved per step (launches x 2 x 2^l x 16 B, all ranks) / device step time",
+            "part_pass_equivalent_gbs": pp_equiv,
+            "roofline": roofline, "clocks": g["clocks"],
+            "gpu_launches": args.steps * g["num_launches"],
             "layout_restore_ms_per_step": g["restore_ms_per_step"],
             "init_ms_per_step": g["init_ms_per_step"],
             "e2e": g["e2e"],
             "time_to_solution_ms": g["ms_step"],
+            "host_seconds": {"partition": round(t_part, 4), "plan_cold": round(g["plan_s"], 4),
+                             "plan_cold_jit": g["jit"], "plan_second_process": warm,
+                             "note": "plan = planner + NVRTC of every pass; cold = empty on-disk cubin cache; "
+                                     "second process = the same plan in a new process that finds the cubins"},
+            "one_pass_per_part": g["literal"],
             "fp64_flops_per_step_paper_count": flops,
             "fp64": g["fp64"],
             "phases_per_launch": [i["phases"] for i in infos],
@@ -561,7 +708,7 @@ def main(argv=None):
     if not args.no_cpu_baseline and world == 1:
         r = cpu_arm(args, cfg, circuit, part, t_part, 2, 1)
         line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
-                                "sample": r["sample"]}
+                                "sample": r["sample"], "numpy_port_c1_seconds": numpy_port_c1_seconds()}
     print(json.dumps(line), flush=True)
     return 0
 

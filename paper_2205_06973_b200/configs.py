@@ -130,12 +130,22 @@ def random_3_regular(n: int, rng: random.Random) -> list[tuple[int, int]]:
             return sorted(edges)
 
 
+def qaoa_graph(n: int, rng: random.Random) -> list[tuple[int, int]]:
+    """c3's MaxCut graph: a seeded 3-regular graph on n vertices. For odd n,
+    where no 3-regular graph exists (weak-scaled c3 at 31 / 33 qubits), a
+    seeded 3-regular graph on n + 1 vertices with vertex n removed (its three
+    neighbours keep degree 2)."""
+    if n % 2 == 0:
+        return random_3_regular(n, rng)
+    return [(a, b) for a, b in random_3_regular(n + 1, rng) if b != n]
+
+
 def qaoa_config(n: int = 30, layers: int = 4, seed: int = 0) -> Circuit:
     """c3: H on all; per layer ZZ(gamma) on every edge of a seeded
-    3-regular graph as CX, RZ(2 gamma), CX (bench.qaoa convention), then
-    RX(2 beta) on every qubit; gamma, beta ~ U[0, pi)."""
+    3-regular graph (``qaoa_graph``) as CX, RZ(2 gamma), CX (bench.qaoa
+    convention), then RX(2 beta) on every qubit; gamma, beta ~ U[0, pi)."""
     rng = random.Random(seed)
-    edges = random_3_regular(n, rng)
+    edges = qaoa_graph(n, rng)
     angles = [(rng.uniform(0, _PI), rng.uniform(0, _PI)) for _ in range(layers)]
     ops = [_op(GateKind.H, q) for q in range(n)]
     for gamma, beta in angles:
@@ -204,15 +214,49 @@ def build(name: str, seed: int = 0) -> Circuit:
         return qaoa_config(int(size) if size else 30, 4, seed)
     if base == "c4":
         return ising_config(int(size) if size else 33, 50, seed)
-    if base == "c5":
-        return random_grid_circuit(6, 6, 24, seed)
-    if base == "c5_35":
-        return random_grid_circuit(6, 6, 24, seed, drop=((5, 5),))
-    if base == "c5_34":
-        return random_grid_circuit(6, 6, 24, seed, drop=((5, 5), (0, 5)))
-    if base == "c5_33":
-        return random_grid_circuit(6, 6, 24, seed, drop=((5, 5), (0, 5), (5, 0)))
+    if base.startswith("c5"):
+        # c5 (36 q on 8 GPUs) and its weak-scaling members: 6x6 grid minus
+        # corners (5,5), (0,5), (5,0) for 35 / 34 / 33 qubits
+        sizes = {"c5": 36, "c5_35": 35, "c5_34": 34, "c5_33": 33}
+        if base not in sizes:
+            raise KeyError(f"unknown config {name!r}")
+        n = int(size) if size else sizes[base]
+        if size and base != "c5":
+            raise KeyError(f"{base} has a fixed size; use c5@{n}")
+        corners = ((5, 5), (0, 5), (5, 0))
+        if not 33 <= n <= 36:
+            raise KeyError(f"c5 is defined for 33..36 qubits, not {n}")
+        return random_grid_circuit(6, 6, 24, seed, drop=corners[:36 - n])
     raise KeyError(f"unknown config {name!r}")
+
+
+#: what ``bench.py --config X --gpus N`` runs: (circuit name, scaling).
+#: c1 / c2 / c3 weak-scale (n + log2 N qubits: a fixed 2^n shard per GPU);
+#: c4 is BASELINE's strong-scaling case (33 qubits over 2 / 4 / 8 GPUs; one
+#: GPU holds all 128 GiB in place); c5 is 36 qubits on 8 GPUs with BASELINE's
+#: weak-scaling members 35 / 4, 34 / 2 and their one-GPU share 33 / 1.
+C5_BY_GPUS = {1: "c5_33", 2: "c5_34", 4: "c5_35", 8: "c5"}
+
+
+def bench_workload(config: str, gpus: int) -> tuple[str, str]:
+    if gpus < 1 or gpus & (gpus - 1):
+        raise ValueError(f"--gpus must be a power of two, not {gpus}")
+    extra = gpus.bit_length() - 1
+    base, _, size = config.partition("@")
+    if base not in CONFIGS:
+        raise KeyError(f"unknown config {config!r}")
+    if base == "c4":
+        return (config, "strong")
+    if base.startswith("c5"):
+        if base == "c5" and not size:
+            if gpus not in C5_BY_GPUS:
+                raise ValueError(f"c5 runs on 1, 2, 4 or 8 GPUs, not {gpus}")
+            return (C5_BY_GPUS[gpus], "weak")
+        if gpus != 1:
+            raise ValueError(f"{config} is one member of c5's weak-scaling family; run --config c5 --gpus {gpus}")
+        return (config, "weak")
+    n = int(size) if size else CONFIGS[base].num_qubits
+    return ((f"{base}@{n + extra}" if extra else config), "weak")
 
 
 def _fix_drop(rows: int, cols: int, sites: int):

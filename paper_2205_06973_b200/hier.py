@@ -526,6 +526,56 @@ def multilevel_trace(circuit: Circuit, partition: MultiLevelPartition) -> Execut
     return tr
 
 
+def timed_launches(program: "PartProgram", data, stream=None) -> list[float]:
+    """Run every launch of ``program`` on ``data`` one at a time with CUDA
+    events between launches on the launch stream; returns the seconds of
+    each launch (synchronizes)."""
+    import torch
+
+    s = stream or torch.cuda.current_stream(program.device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(program.num_launches + 1)]
+    ev[0].record(s)
+    for i in range(program.num_launches):
+        program.run(data, i, 1, stream=s)
+        ev[i + 1].record(s)
+    ev[-1].synchronize()
+    return [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(program.num_launches)]
+
+
+def launch_times_by_part(program: "PartProgram", launch_s: Sequence[float]) -> dict[int, tuple[float, int]]:
+    """{program part index: (seconds, launches)}. A launch carries the gates
+    of the part it reports (``user_part``; regrouped tile passes report the
+    part that contributes most of their gates); a gate-free layout launch
+    (user_part -1) is charged to the part before it (part 0 if first), so
+    the parts' times add up to the program's."""
+    out: dict[int, list] = {}
+    prev = 0
+    for i, t in enumerate(launch_s):
+        u = program.info(i)["user_part"]
+        u = prev if u < 0 else u
+        prev = u
+        acc = out.setdefault(u, [0.0, 0])
+        acc[0] += t
+        acc[1] += 1
+    return {k: (v[0], v[1]) for k, v in out.items()}
+
+
+def _timed_trace(trace: "ExecutionTrace", rows: Sequence[int], program: "PartProgram", launch_s) -> "ExecutionTrace":
+    """Fill ``time_s`` / ``hbm_bytes`` of trace row ``rows[j]`` from the
+    launches of the program's part j (rows without launches: 0 s, 0 B)."""
+    from dataclasses import replace
+
+    amp = 16 if str(program.dtype).endswith("complex128") else 8
+    per_pass = 2 * (1 << program.n_local) * amp
+    got = launch_times_by_part(program, launch_s)
+    parts = list(trace.parts)
+    for j, r in enumerate(rows):
+        t, k = got.get(j, (0.0, 0))
+        parts[r] = replace(parts[r], time_s=t, hbm_bytes=k * per_pass)
+    trace.parts = parts
+    return trace
+
+
 # --- drivers ----------------------------------------------------------------------
 
 def start_state(circuit: Circuit, initial, max_qubits, dtype="complex128", device=None) -> StateVector:
@@ -621,16 +671,23 @@ def execute_hierarchical(
     initial: StateVector | None = None,
     max_qubits: int | None = None,
     with_trace: bool = False,
+    with_timing: bool = False,
     dtype="complex128",
     device=None,
 ):
     """Run a partitioned circuit part by part on one device state
-    (hier.py:342-368): parts in the given order, one kernel pass each.
-    Returns a device ``StateVector`` (and the ``ExecutionTrace``)."""
+    (hier.py:342-368): parts in the given order, as planned tile passes.
+    Returns a device ``StateVector`` (and the ``ExecutionTrace``).
+    ``with_timing`` (with ``with_trace``): launches run one by one between
+    CUDA events and each trace row gets ``time_s``, ``hbm_bytes`` (2 x 2^n x
+    amplitude size per launch) and ``gbps``."""
     state = start_state(circuit, initial, max_qubits, dtype, device)
     # from |0..0> (one amplitude, the same in every layout) the planner may
     # choose the initial layout; a caller's state arrives in natural order
     run = HierarchicalRun(circuit, partition, dtype=dtype, device=device, basis_start=initial is None)
+    if with_trace and with_timing:
+        launch_s = timed_launches(run.program, state.data)
+        return state, _timed_trace(run.trace(), range(len(run.exes)), run.program, launch_s)
     run.program.run(state.data)
     if with_trace:
         return state, run.trace()
@@ -644,6 +701,7 @@ def execute_multilevel(
     initial: StateVector | None = None,
     max_qubits: int | None = None,
     with_trace: bool = False,
+    with_timing: bool = False,
     dtype="complex128",
     device=None,
 ):
@@ -655,17 +713,27 @@ def execute_multilevel(
     _check_covers(circuit, [p for sub in partition.sublevels for p in sub.parts])
     n = circuit.num_qubits
     exes: list[ExecutablePart] = []
+    rows: list[int] = []  # trace row of each executed part
+    row = 0
     for i, parent in enumerate(partition.level1.parts):
         sub = partition.sublevels[i]
         padded = partition.padded_qubits[i]
         if len(sub.parts) == 1 and padded[0] == parent.qubits:
             exes.append(remap_part(circuit, sub.parts[0]))
+            rows.append(row)
+            row += 1
             continue
         exes += [remap_part(circuit, sp, stage_qubits=padded[j]) for j, sp in enumerate(sub.parts)]
+        rows += [row + 1 + j for j in range(len(sub.parts))]
+        row += 1 + len(sub.parts)
     trace = multilevel_trace(circuit, partition)
     state = start_state(circuit, initial, max_qubits, dtype, device)
     if exes:
-        PartProgram(n, exes, dtype=dtype, device=device).run(state.data)
+        prog = PartProgram(n, exes, dtype=dtype, device=device)
+        if with_trace and with_timing:
+            trace = _timed_trace(trace, rows, prog, timed_launches(prog, state.data))
+        else:
+            prog.run(state.data)
     if with_trace:
         return state, trace
     return state

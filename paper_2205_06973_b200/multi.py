@@ -315,10 +315,12 @@ class ShardedRun:
             finish(pending)
         return shard
 
-    def run(self, shard, events=None, run_part=None):
+    def run(self, shard, events=None, run_part=None, with_timing: bool = False):
         """All parts in order on this rank's shard (switches included);
         returns the final shard in natural order of the last layout.
-        ``events`` receives ("switch" | "parts", cuda event) marks."""
+        ``events`` receives ("switch" | "parts", cuda event) marks.
+        ``with_timing``: ``self.stats.switch_time_s`` gets this rank's device
+        seconds of every switch (synchronizes at the end)."""
         import torch
 
         def mark(kind):
@@ -327,11 +329,19 @@ class ShardedRun:
                 ev.record()
                 events.append((kind, ev))
 
+        sw_marks = []
         for si, (a, b) in enumerate(self.segments):
             if a in self.switch_at:
                 old, new, _ = self.switch_at[a]
                 phys = self.seg_phys_out[si - 1] if run_part is None and self.programs else None
+                if with_timing:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
                 shard = self.switch(shard, old, new, phys)
+                if with_timing:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    sw_marks.append((e0, e1))
                 mark("switch")
                 if run_part is not None:  # host stand-ins run parts in natural order
                     shard = self.ops.to_natural(shard, self.arrival_layout(old, new))
@@ -344,6 +354,9 @@ class ShardedRun:
                 self._share_scratch(shard)
                 self.programs[si].run(shard)
             mark("parts")
+        if sw_marks:
+            sw_marks[-1][1].synchronize()
+            self.stats.switch_time_s = [a.elapsed_time(b) / 1e3 for a, b in sw_marks]
         return shard
 
 
@@ -401,7 +414,7 @@ class ShardedState:
 
 
 def simulate_distributed_group(circuit, partition, num_rank_bits, *, group=None, initial=None, dtype="complex128",
-                               device=None, policy: str = "reference") -> DistributedRun:
+                               device=None, policy: str = "reference", with_timing: bool = False) -> DistributedRun:
     """``simulate_distributed`` over a process group: every rank returns its
     own shard (``DistributedRun.state`` is a ``ShardedState``)."""
     import torch
@@ -417,7 +430,7 @@ def simulate_distributed_group(circuit, partition, num_rank_bits, *, group=None,
             shard.zero_()
     else:
         raise NotImplementedError("initial= with a process group: load each rank's shard instead")
-    shard = run.run(shard)
+    shard = run.run(shard, with_timing=with_timing)
     torch.cuda.synchronize()
     return DistributedRun(ShardedState(run.n, shard, run.layouts[-1], run.rank), run.stats, run.layouts)
 

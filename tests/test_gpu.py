@@ -638,3 +638,100 @@ def test_part_apply_c_abi_runs_every_launch(w):
         finally:
             lib.hs_engine_set_options(eng, _native.default_options())
         assert float(np.max(np.abs(dev.cpu().numpy() - want))) < 1e-10, hex(opts)
+
+
+def test_trace_timing_rows_sum_to_the_program_time():
+    """with_timing: every part row carries time_s / hbm_bytes / gbps from
+    per-launch CUDA events; the rows add up to the graph-launched program's
+    device time within 5 % (the bench's step)."""
+    c = configs.build("c2")
+    part = partition_dfs(build_dag(c), 12)
+    st, tr = execute_hierarchical(c, part, with_trace=True, with_timing=True)
+    rows = tr.part_rows()
+    assert len(rows) == part.num_parts and all("gbps" in r for r in rows)
+    total = sum(r["time_s"] for r in rows)
+    run = HierarchicalRun(c, part, basis_start=True)
+    from paper_2205_06973_b200.statevec import allocate
+
+    buf = allocate(c.num_qubits)
+    for _ in range(3):
+        run.program.init_basis(buf, 0)
+        run.program.run_graph(buf)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(5):
+        run.program.init_basis(buf, 0)
+        e0.record()
+        run.program.run_graph(buf)
+        e1.record()
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    graph_s = sorted(ms)[2] / 1e3
+    assert abs(total - graph_s) < 0.05 * graph_s, (total, graph_s)
+    assert sum(r["hbm_bytes"] for r in rows) == run.program.num_launches * 2 * (1 << 26) * 16
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert max_abs_diff(st, ref) < 1e-10
+    # multilevel rows: every level-2 row (or lone level-1 row) is timed
+    ml = partition_multilevel(build_dag(configs.build("c2@20")), 12, 8)
+    c20 = configs.build("c2@20")
+    st, tr = execute_multilevel(c20, ml, with_trace=True, with_timing=True)
+    timed = [r for r in tr.part_rows() if "time_s" in r]
+    assert timed and sum(r["hbm_bytes"] for r in timed) > 0
+
+
+def test_distributed_switch_times():
+    c = configs.build("c1@16")
+    part = partition_dfs(build_dag(c), 8)
+    run = simulate_distributed(c, part, 2, with_timing=True)
+    stats = run.stats
+    assert stats.num_switches > 0 and len(stats.switch_time_s) == stats.num_switches
+    doc = stats.to_json()
+    assert all(s["time_s"] > 0 for s in doc["switches"]) and doc["totals"]["switch_time_s"] > 0
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_benched_programs_match_c_oracle_at_full_size(name):
+    """The exact programs bench.py times, at BASELINE size (c2: 26 qubits,
+    c3: 30 qubits, 16 GiB), against the multi-threaded C oracle run on the
+    box's host over the same partition (c3: ~70 s on 16 cores) at 1e-10:
+    the timed program (|0..0> prepared in its own initial layout, ping-pong
+    passes, one CUDA graph launch), the e2e program (natural-order input,
+    run_stream from pinned host memory) and the one-pass-per-part program."""
+    from paper_2205_06973_b200.statevec import allocate
+
+    c = configs.build(name)
+    n = c.num_qubits
+    part = partition_dfs(build_dag(c), 12)
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    ref_dev = torch.from_numpy(ref).cuda()
+    del ref
+
+    def err(buf):
+        from paper_2205_06973_b200.statevec import StateVector
+
+        return max_abs_diff(StateVector(n, buf), ref_dev)
+
+    buf = allocate(n)
+    timed = HierarchicalRun(c, part, basis_start=True)
+    assert timed.program.initial_layout != tuple(range(n)) and timed.program.needs_scratch
+    assert all(timed.program.info(j)["compiled"] for j in range(timed.program.num_launches))
+    for _ in range(2):  # graph capture, then replay
+        timed.program.init_basis(buf, 0)
+        timed.program.run_graph(buf)
+        assert err(buf) < 1e-10
+    literal = HierarchicalRun(c, part, basis_start=True, options=(timed.program.options & ~_native.HS_PLAN_MERGE)
+                              | _native.HS_PLAN_PART_LOCAL)
+    assert [literal.program.info(j)["user_part"] for j in range(part.num_parts)] == list(range(part.num_parts))
+    literal.program.share_scratch(timed.program._scratch)
+    literal.program.init_basis(buf, 0)
+    literal.program.run_graph(buf)
+    assert err(buf) < 1e-10
+    e2e = HierarchicalRun(c, part, basis_start=False)
+    e2e.program.share_scratch(timed.program._scratch)
+    host_in = torch.zeros(1 << n, dtype=torch.complex128).pin_memory()
+    host_in[0] = 1.0
+    host_out = torch.empty(1 << n, dtype=torch.complex128).pin_memory()
+    e2e.run_stream([host_in, host_in], [host_out, host_out], buffers=[buf])
+    torch.cuda.synchronize()
+    buf.copy_(host_out)
+    assert err(buf) < 1e-10
