@@ -287,6 +287,42 @@ int hs_unpack_segments_range(const void* src, void* dst, int num_bits, int dtype
                              const int32_t* seg_pos, int num_seg_bits,
                              int64_t inner_begin, int64_t inner_count, void* stream);
 
+/* Pull form of the unpack (a layout switch over peer memory): packed
+ * element m of slot k is read from src_by_slot[k][m] - a device pointer that
+ * may live on another GPU (peer access or an IPC mapping) - and written to
+ * inner offset inner_begin + m of segment k of dst. 2^num_seg_bits pointers. */
+int hs_unpack_segments_range_from(const void* const* src_by_slot, void* dst, int num_bits, int dtype,
+                                  const int32_t* seg_pos, int num_seg_bits, int64_t inner_begin,
+                                  int64_t inner_count, void* stream);
+
+/* Multi-device engine: 2^p shards driven by one process, shard r on
+ * devices[r] (several shards may share a device; distinct devices get peer
+ * access over NVLink / NVSwitch). Two staging buffers of staging_bytes per
+ * shard. Replaces the exchange of RedistributionPlan.apply
+ * (pkg/src/hisim/dist.py:261-268) across GPUs. */
+typedef struct hs_group hs_group;
+int hs_group_create(int num_shards, const int32_t* devices, size_t staging_bytes, hs_group** out);
+int hs_group_destroy(hs_group* group);
+/* In-place qubit-remap switch of every shard (2^n_local amplitudes each):
+ * the num_seg_bits positions seg_pos[] (ascending) of shard r spell a
+ * segment k that moves to shard seg_dst[r << num_seg_bits | k], where it
+ * lands in the positions of its segment src_slot[r]; the other bits keep
+ * their positions. Chunk by chunk of inner offsets: every shard packs its
+ * outgoing segments into local staging, then pulls its incoming segments
+ * from the senders' staging over peer memory into its own shard. Launches
+ * on streams[r] (NULL: the group's own streams) with cross-shard event
+ * ordering; asynchronous unless *seconds is requested (then the max over
+ * shards of the switch's device time is written after a sync). */
+int hs_group_switch(hs_group* group, void* const* shards, int n_local, int dtype, const int32_t* seg_pos,
+                    int num_seg_bits, const int32_t* seg_dst, const int32_t* src_slot, void* const* streams,
+                    double* seconds);
+/* one process per GPU: export / map another process's device buffer
+ * (cudaIpcMemHandle_t, 64 bytes) so hs_unpack_segments_range_from can pull
+ * from a peer's staging */
+int hs_ipc_get_handle(const void* device_ptr, void* handle_out);
+int hs_ipc_open_handle(const void* handle, void** device_ptr);
+int hs_ipc_close(void* device_ptr);
+
 #ifdef __cplusplus
 }
 #endif

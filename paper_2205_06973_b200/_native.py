@@ -37,6 +37,8 @@ EXPORTS = (
     "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_plan_program_layouts", "hs_jit_source", "hs_structure_2x2", "hs_dagp_merge", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
     "hs_pack_segments", "hs_unpack_segments", "hs_pack_segments_range", "hs_unpack_segments_range",
+    "hs_unpack_segments_range_from", "hs_group_create", "hs_group_destroy", "hs_group_switch",
+    "hs_ipc_get_handle", "hs_ipc_open_handle", "hs_ipc_close",
 )
 
 
@@ -132,6 +134,16 @@ def _declare(lib) -> None:
         "hs_unpack_segments": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, P]),
         "hs_pack_segments_range": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, I64, I64, P]),
         "hs_unpack_segments_range": (I, [P, P, I, I, ctypes.POINTER(ctypes.c_int32), I, I64, I64, P]),
+        "hs_unpack_segments_range_from": (I, [ctypes.POINTER(P), P, I, I, ctypes.POINTER(ctypes.c_int32), I, I64, I64,
+                                              P]),
+        "hs_group_create": (I, [I, ctypes.POINTER(ctypes.c_int32), ctypes.c_size_t, ctypes.POINTER(P)]),
+        "hs_group_destroy": (I, [P]),
+        "hs_group_switch": (I, [P, ctypes.POINTER(P), I, I, ctypes.POINTER(ctypes.c_int32), I,
+                                ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(P),
+                                ctypes.POINTER(D)]),
+        "hs_ipc_get_handle": (I, [P, P]),
+        "hs_ipc_open_handle": (I, [P, ctypes.POINTER(P)]),
+        "hs_ipc_close": (I, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -25,6 +26,8 @@ cudaError_t launch_segments(bool pack, const void* in, void* out, int nbits, int
 cudaError_t launch_maxdiff(const void* a, int dtype, const void* b, int64_t n, unsigned long long* dres,
                            int num_sms, cudaStream_t s);
 cudaError_t measure_fp64_peak(double* tflops, int num_sms, cudaStream_t s);
+cudaError_t launch_segments_from(const void* const* src, void* out, int nbits, int dtype, const int32_t* seg_pos,
+                                 int nseg, int64_t begin, int64_t count, int num_sms, cudaStream_t s);
 }  // namespace hs
 
 using namespace hs;
@@ -37,6 +40,22 @@ struct hs_engine {
   int tile_c64 = 13;
   uint32_t options = HS_PLAN_DEFAULT;
   unsigned long long* d_scratch = nullptr;  // reductions
+};
+
+// A group of 2^p shards driven by one process: each shard on its own device
+// (peer access enabled between distinct devices) or several on one device.
+// Layout switches move amplitudes between shards over peer memory
+// (NVLink / NVSwitch), in place and chunk by chunk: pack the chunk's
+// outgoing segments into local staging, then every shard pulls its incoming
+// segments straight from the owners' staging into its own positions.
+struct hs_group {
+  int num_shards = 0;
+  std::vector<int> devices;
+  std::vector<int> sms;
+  size_t staging_bytes = 0;           // per staging buffer (two per shard)
+  std::vector<void*> staging[2];      // [buffer][shard]
+  std::vector<cudaStream_t> streams;  // one per shard (non-blocking)
+  std::vector<cudaEvent_t> packed[2], pulled[2], t0, t1;
 };
 
 struct hs_program {
@@ -585,6 +604,210 @@ int hs_pack_segments_range(const void* src, void* dst, int num_bits, int dtype, 
 int hs_unpack_segments_range(const void* src, void* dst, int num_bits, int dtype, const int32_t* seg_pos, int nseg,
                              int64_t inner_begin, int64_t inner_count, void* stream) {
   return segments_range(false, src, dst, num_bits, dtype, seg_pos, nseg, inner_begin, inner_count, stream);
+}
+
+int hs_unpack_segments_range_from(const void* const* src_by_slot, void* dst, int num_bits, int dtype,
+                                  const int32_t* seg_pos, int nseg, int64_t inner_begin, int64_t inner_count,
+                                  void* stream) {
+  if (!src_by_slot || !dst || (nseg && !seg_pos)) return fail(HS_ERR_INVALID, "NULL argument");
+  if (int s = check_dtype(dtype)) return s;
+  if (nseg < 0 || nseg > 8 || num_bits < nseg || num_bits > 62)
+    return fail(HS_ERR_INVALID, "segment bits outside range");
+  for (int k = 0; k < nseg; ++k) {
+    if (seg_pos[k] < 0 || seg_pos[k] >= num_bits) return fail(HS_ERR_INVALID, "segment position outside state");
+    if (k && seg_pos[k] <= seg_pos[k - 1]) return fail(HS_ERR_INVALID, "segment positions not ascending");
+  }
+  for (int k = 0; k < (1 << nseg); ++k)
+    if (!src_by_slot[k]) return fail(HS_ERR_INVALID, "NULL source slot");
+  const int64_t inner = int64_t(1) << (num_bits - nseg);
+  if (inner_begin < 0 || inner_count < 0 || inner_begin + inner_count > inner)
+    return fail(HS_ERR_INVALID, "inner range outside the segments");
+  if (inner_count == 0) return HS_OK;
+  HS_CUDA(launch_segments_from(src_by_slot, dst, num_bits, dtype, seg_pos, nseg, inner_begin, inner_count,
+                               sms_of_current(), (cudaStream_t)stream),
+          "segment pull kernel");
+  return HS_OK;
+}
+
+int hs_group_create(int num_shards, const int32_t* devices, size_t staging_bytes, hs_group** out) {
+  if (!out || !devices) return fail(HS_ERR_INVALID, "NULL argument");
+  *out = nullptr;
+  if (num_shards < 1 || num_shards > 256 || (num_shards & (num_shards - 1)))
+    return fail(HS_ERR_INVALID, "num_shards must be a power of two in [1, 256]");
+  if (staging_bytes < 4096) return fail(HS_ERR_INVALID, "staging_bytes below 4 KiB");
+  int count = 0;
+  HS_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  for (int r = 0; r < num_shards; ++r)
+    if (devices[r] < 0 || devices[r] >= count) return fail(HS_ERR_INVALID, "device index outside the node");
+  std::unique_ptr<hs_group> g(new (std::nothrow) hs_group);
+  if (!g) return fail(HS_ERR_CAPACITY, "out of host memory");
+  g->num_shards = num_shards;
+  g->devices.assign(devices, devices + num_shards);
+  g->staging_bytes = staging_bytes;
+  // peer access between every pair of distinct devices (NVLink / NVSwitch)
+  for (int a : g->devices)
+    for (int b : g->devices) {
+      if (a == b) continue;
+      int ok = 0;
+      HS_CUDA(cudaDeviceCanAccessPeer(&ok, a, b), "cudaDeviceCanAccessPeer");
+      if (!ok) return fail(HS_ERR_UNSUPPORTED, "devices " + std::to_string(a) + " and " + std::to_string(b) +
+                                                     " have no peer access");
+      HS_CUDA(cudaSetDevice(a), "cudaSetDevice");
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+  auto cleanup = [](hs_group* h) { hs_group_destroy(h); };
+  std::unique_ptr<hs_group, decltype(cleanup)> guard(g.release(), cleanup);
+  hs_group* G = guard.get();
+  for (int b = 0; b < 2; ++b) {
+    G->staging[b].assign(num_shards, nullptr);
+    G->packed[b].assign(num_shards, nullptr);
+    G->pulled[b].assign(num_shards, nullptr);
+  }
+  G->streams.assign(num_shards, nullptr);
+  G->t0.assign(num_shards, nullptr);
+  G->t1.assign(num_shards, nullptr);
+  G->sms.assign(num_shards, 0);
+  for (int r = 0; r < num_shards; ++r) {
+    HS_CUDA(cudaSetDevice(G->devices[r]), "cudaSetDevice");
+    HS_CUDA(cudaDeviceGetAttribute(&G->sms[r], cudaDevAttrMultiProcessorCount, G->devices[r]), "attr");
+    HS_CUDA(cudaStreamCreateWithFlags(&G->streams[r], cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int b = 0; b < 2; ++b) {
+      HS_CUDA(cudaMalloc(&G->staging[b][r], staging_bytes), "cudaMalloc staging");
+      HS_CUDA(cudaEventCreateWithFlags(&G->packed[b][r], cudaEventDisableTiming), "cudaEventCreate");
+      HS_CUDA(cudaEventCreateWithFlags(&G->pulled[b][r], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    HS_CUDA(cudaEventCreate(&G->t0[r]), "cudaEventCreate");
+    HS_CUDA(cudaEventCreate(&G->t1[r]), "cudaEventCreate");
+  }
+  *out = guard.release();
+  return HS_OK;
+}
+
+int hs_group_destroy(hs_group* g) {
+  if (!g) return HS_OK;
+  for (int r = 0; r < g->num_shards; ++r) {
+    if (r < (int)g->devices.size()) cudaSetDevice(g->devices[r]);
+    for (int b = 0; b < 2; ++b) {
+      if (r < (int)g->staging[b].size() && g->staging[b][r]) cudaFree(g->staging[b][r]);
+      if (r < (int)g->packed[b].size() && g->packed[b][r]) cudaEventDestroy(g->packed[b][r]);
+      if (r < (int)g->pulled[b].size() && g->pulled[b][r]) cudaEventDestroy(g->pulled[b][r]);
+    }
+    if (r < (int)g->t0.size() && g->t0[r]) cudaEventDestroy(g->t0[r]);
+    if (r < (int)g->t1.size() && g->t1[r]) cudaEventDestroy(g->t1[r]);
+    if (r < (int)g->streams.size() && g->streams[r]) cudaStreamDestroy(g->streams[r]);
+  }
+  delete g;
+  return HS_OK;
+}
+
+int hs_group_switch(hs_group* g, void* const* shards, int n_local, int dtype, const int32_t* seg_pos, int nseg,
+                    const int32_t* seg_dst, const int32_t* src_slot, void* const* streams, double* seconds) {
+  if (!g || !shards || !seg_dst || !src_slot || (nseg && !seg_pos)) return fail(HS_ERR_INVALID, "NULL argument");
+  if (int s = check_dtype(dtype)) return s;
+  const int R = g->num_shards, S = 1 << nseg;
+  if (nseg < 0 || nseg > 8 || n_local < nseg || n_local > 62) return fail(HS_ERR_INVALID, "segment bits outside range");
+  for (int k = 0; k < nseg; ++k)
+    if (seg_pos[k] < 0 || seg_pos[k] >= n_local || (k && seg_pos[k] <= seg_pos[k - 1]))
+      return fail(HS_ERR_INVALID, "segment positions must be ascending positions of the shard");
+  // who pulls what: slot j of shard r comes from the source s whose data
+  // lands in slot j (src_slot[s] == j) and whose segment k goes to r
+  std::vector<int32_t> from_src((size_t)R * S, -1), from_seg((size_t)R * S, -1);
+  for (int s = 0; s < R; ++s) {
+    if (src_slot[s] < 0 || src_slot[s] >= S) return fail(HS_ERR_INVALID, "src_slot outside the segments");
+    for (int k = 0; k < S; ++k) {
+      const int d = seg_dst[(size_t)s * S + k];
+      if (d < 0 || d >= R) return fail(HS_ERR_INVALID, "seg_dst outside the group");
+      int32_t& f = from_src[(size_t)d * S + src_slot[s]];
+      if (f >= 0) return fail(HS_ERR_INVALID, "two segments land in the same slot of a shard");
+      f = s;
+      from_seg[(size_t)d * S + src_slot[s]] = k;
+    }
+  }
+  for (size_t i = 0; i < from_src.size(); ++i)
+    if (from_src[i] < 0) return fail(HS_ERR_INVALID, "a slot of a shard receives nothing");
+  const size_t amp = dtype == HS_C128 ? 16 : 8;
+  const int64_t inner = int64_t(1) << (n_local - nseg);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(inner, int64_t(g->staging_bytes / (amp * S))));
+  auto stream_of = [&](int r) { return streams && streams[r] ? (cudaStream_t)streams[r] : g->streams[r]; };
+  if (seconds)
+    for (int r = 0; r < R; ++r) {
+      HS_CUDA(cudaSetDevice(g->devices[r]), "cudaSetDevice");
+      HS_CUDA(cudaEventRecord(g->t0[r], stream_of(r)), "cudaEventRecord");
+    }
+  std::vector<const void*> srcs(S);
+  int m = 0;
+  for (int64_t begin = 0; begin < inner; begin += chunk, ++m) {
+    const int64_t cnt = std::min(chunk, inner - begin);
+    const int b = m & 1;
+    for (int r = 0; r < R; ++r) {
+      HS_CUDA(cudaSetDevice(g->devices[r]), "cudaSetDevice");
+      cudaStream_t st = stream_of(r);
+      // staging buffer b was last read by the pulls of chunk m - 2
+      if (m >= 2)
+        for (int s = 0; s < R; ++s) HS_CUDA(cudaStreamWaitEvent(st, g->pulled[b][s], 0), "wait");
+      HS_CUDA(launch_segments_range(true, shards[r], g->staging[b][r], n_local, dtype, seg_pos, nseg, begin, cnt,
+                                    g->sms[r], st),
+              "pack");
+      HS_CUDA(cudaEventRecord(g->packed[b][r], st), "cudaEventRecord");
+    }
+    for (int r = 0; r < R; ++r) {
+      HS_CUDA(cudaSetDevice(g->devices[r]), "cudaSetDevice");
+      cudaStream_t st = stream_of(r);
+      for (int j = 0; j < S; ++j) {
+        const int s = from_src[(size_t)r * S + j];
+        HS_CUDA(cudaStreamWaitEvent(st, g->packed[b][s], 0), "wait");
+        srcs[j] = (const char*)g->staging[b][s] + (size_t)from_seg[(size_t)r * S + j] * cnt * amp;
+      }
+      HS_CUDA(launch_segments_from(srcs.data(), shards[r], n_local, dtype, seg_pos, nseg, begin, cnt, g->sms[r], st),
+              "pull");
+      HS_CUDA(cudaEventRecord(g->pulled[b][r], st), "cudaEventRecord");
+    }
+  }
+  // no shard runs ahead into the next pass before every pull has read its data
+  for (int r = 0; r < R; ++r) {
+    HS_CUDA(cudaSetDevice(g->devices[r]), "cudaSetDevice");
+    for (int s = 0; s < R; ++s)
+      for (int b = 0; b < 2 && b < m; ++b) HS_CUDA(cudaStreamWaitEvent(stream_of(r), g->pulled[b][s], 0), "wait");
+  }
+  if (seconds) {
+    double worst = 0;
+    for (int r = 0; r < R; ++r) {
+      HS_CUDA(cudaSetDevice(g->devices[r]), "cudaSetDevice");
+      HS_CUDA(cudaEventRecord(g->t1[r], stream_of(r)), "cudaEventRecord");
+    }
+    for (int r = 0; r < R; ++r) {
+      HS_CUDA(cudaEventSynchronize(g->t1[r]), "cudaEventSynchronize");
+      float ms = 0;
+      HS_CUDA(cudaEventElapsedTime(&ms, g->t0[r], g->t1[r]), "cudaEventElapsedTime");
+      worst = std::max(worst, double(ms) / 1e3);
+    }
+    *seconds = worst;
+  }
+  return HS_OK;
+}
+
+int hs_ipc_get_handle(const void* device_ptr, void* handle_out) {
+  if (!device_ptr || !handle_out) return fail(HS_ERR_INVALID, "NULL argument");
+  cudaIpcMemHandle_t h;
+  HS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr)), "cudaIpcGetMemHandle");
+  std::memcpy(handle_out, &h, sizeof(h));
+  return HS_OK;
+}
+
+int hs_ipc_open_handle(const void* handle, void** device_ptr) {
+  if (!handle || !device_ptr) return fail(HS_ERR_INVALID, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  HS_CUDA(cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return HS_OK;
+}
+
+int hs_ipc_close(void* device_ptr) {
+  if (!device_ptr) return fail(HS_ERR_INVALID, "NULL argument");
+  HS_CUDA(cudaIpcCloseMemHandle(device_ptr), "cudaIpcCloseMemHandle");
+  return HS_OK;
 }
 
 int hs_fp64_peak(double* tflops, void* stream) {

@@ -14,6 +14,7 @@
 //      order (undoing SWAP relabels), then coalesced stores to HBM.
 // Shared memory slots are XOR-swizzled so phase exchanges are conflict-free.
 #include <cuda_runtime.h>
+#include <cstring>
 
 #include <cstdint>
 
@@ -620,6 +621,73 @@ cudaError_t launch_segments_range(bool pack, const void* in, void* out, int nbit
     if (pack) seg_range_kernel<float2, true><<<(unsigned)blocks, 256, 0, s>>>((const float2*)in, (float2*)out, p);
     else seg_range_kernel<float2, false><<<(unsigned)blocks, 256, 0, s>>>((const float2*)in, (float2*)out, p);
   }
+  return cudaGetLastError();
+}
+
+// unpack from per-slot sources (a layout switch's pull over peer memory):
+// packed element m of slot k lives at src[k][m], which may be another
+// GPU's staging buffer (peer access / an IPC mapping); it lands at inner
+// offset begin + m of segment k of the local shard. One pass reads every
+// remote amplitude once over NVLink and writes it once to local HBM.
+struct SegFromParams {
+  const void* src[256];
+  int8_t seg_pos[8];
+  int32_t nseg;
+  int32_t nbits;
+  int64_t begin, count;
+  int32_t kfast;
+  int32_t count_log;
+};
+
+template <typename C>
+__global__ void seg_from_kernel(C* __restrict__ out, const SegFromParams p) {
+  const uint64_t total = uint64_t(p.count) << p.nseg;
+  const uint64_t kmask = (uint64_t(1) << p.nseg) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k, m;
+    if (p.kfast) {
+      k = i & kmask;
+      m = i >> p.nseg;
+    } else if (p.count_log >= 0) {
+      k = i >> p.count_log;
+      m = i & ((uint64_t(1) << p.count_log) - 1);
+    } else {
+      k = i / uint64_t(p.count);
+      m = i - k * uint64_t(p.count);
+    }
+    uint64_t idx = uint64_t(p.begin) + m;
+    for (int b = 0; b < p.nseg; ++b) {
+      const int q = p.seg_pos[b];
+      const uint64_t lo = idx & ((1ull << q) - 1);
+      idx = ((idx ^ lo) << 1) | lo | (((k >> b) & 1ull) << q);
+    }
+    out[idx] = reinterpret_cast<const C*>(p.src[k])[m];
+  }
+}
+
+cudaError_t launch_segments_from(const void* const* src, void* out, int nbits, int dtype, const int32_t* seg_pos,
+                                 int nseg, int64_t begin, int64_t count, int num_sms, cudaStream_t s) {
+  SegFromParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.nbits = nbits;
+  p.nseg = nseg;
+  p.begin = begin;
+  p.count = count;
+  for (int k = 0; k < (1 << nseg); ++k) p.src[k] = src[k];
+  for (int k = 0; k < nseg; ++k) p.seg_pos[k] = (int8_t)seg_pos[k];
+  p.kfast = (nseg > 0 && seg_pos[0] < (dtype == HS_C128 ? 3 : 4)) ? 1 : 0;
+  p.count_log = -1;
+  if (count > 0 && (count & (count - 1)) == 0) {
+    p.count_log = 0;
+    while ((int64_t(1) << p.count_log) < count) ++p.count_log;
+  }
+  const uint64_t n = uint64_t(count) << nseg;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > (uint64_t)num_sms * 16) blocks = (uint64_t)num_sms * 16;
+  if (blocks < 1) blocks = 1;
+  if (dtype == HS_C128) seg_from_kernel<double2><<<(unsigned)blocks, 256, 0, s>>>((double2*)out, p);
+  else seg_from_kernel<float2><<<(unsigned)blocks, 256, 0, s>>>((float2*)out, p);
   return cudaGetLastError();
 }
 

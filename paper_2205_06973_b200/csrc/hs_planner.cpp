@@ -459,6 +459,95 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     }
     return Yield{taken, mixed};
   };
+  // write-back relabel rho: the qubit in tile bit b is stored at tile
+  // position rho[b] (a permutation of the tile's own positions, so the store
+  // stays in place). It is how the program's layout evolves: qubits staged
+  // soonest move to the lowest physical positions so later tiles read long
+  // contiguous runs, and the final launches steer every qubit home.
+  std::vector<int> rho(T);
+  for (int b = 0; b < T; ++b) rho[b] = b;
+  if (lay && lay->mode != LAYOUT_KEEP) {
+    std::vector<int> occ(T);  // logical position living at tile[b]
+    for (int b = 0; b < T; ++b) occ[b] = lay->inv_in ? lay->inv_in[tile[b]] : tile[b];
+    auto index_in_tile = [&](int p) {
+      auto it = std::find(tile.begin(), tile.end(), p);
+      return it == tile.end() ? -1 : int(it - tile.begin());
+    };
+    if (lay->mode == LAYOUT_OOP) {
+      // out of place: store slot bit r = the r-th lowest output position
+      // among the tile's qubits
+      std::vector<int> outp(T);
+      for (int b = 0; b < T; ++b) outp[b] = lay->target[occ[b]];
+      for (int b = 0; b < T; ++b) {
+        int r = 0;
+        for (int c = 0; c < T; ++c) r += outp[c] < outp[b];
+        rho[b] = r;
+      }
+    } else if (lay->mode == LAYOUT_PRIORITY) {
+      // the lowest 3 tile positions (the coalescing bits when they are the
+      // physical bits 0..2) go to the qubits staged soonest; qubits never
+      // staged again go home when home is in the tile (less to restore at
+      // the end); the rest fill the remaining positions by next use
+      std::vector<int> order(T);
+      for (int b = 0; b < T; ++b) order[b] = b;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int x, int y) { return lay->next_use[occ[x]] < lay->next_use[occ[y]]; });
+      const int32_t never = 1 << 29;
+      std::vector<char> taken(T, 0), placed(T, 0);
+      const int hot = std::min(3, T);
+      for (int r = 0; r < hot; ++r) {
+        rho[order[r]] = r;
+        taken[r] = placed[order[r]] = 1;
+      }
+      for (int r = hot; r < T; ++r) {
+        const int b = order[r];
+        if (lay->next_use[occ[b]] < never) continue;
+        int h = index_in_tile(occ[b]);
+        if (h >= hot && !taken[h]) { rho[b] = h; taken[h] = placed[b] = 1; }
+      }
+      int next = 0;
+      for (int r = 0; r < T; ++r) {
+        const int b = order[r];
+        if (placed[b]) continue;
+        while (taken[next]) ++next;
+        rho[b] = next;
+        taken[next] = 1;
+      }
+    } else {  // LAYOUT_TARGET: each occupant to target[occ] when that lies in the tile
+      std::vector<char> taken(T, 0), placed(T, 0);
+      for (int b = 0; b < T; ++b) {
+        int t = index_in_tile(lay->target[occ[b]]);
+        if (t >= 0 && !taken[t]) { rho[b] = t; taken[t] = 1; placed[b] = 1; }
+      }
+      int next = 0;
+      for (int b = 0; b < T; ++b) {
+        if (placed[b]) continue;
+        while (taken[next]) ++next;
+        rho[b] = next;
+        taken[next] = 1;
+      }
+    }
+    if (lay->phys_out) {
+      if (lay->mode == LAYOUT_OOP)
+        for (int q = 0; q < n_local; ++q) lay->phys_out[q] = lay->target[q];
+      else
+        for (int b = 0; b < T; ++b) lay->phys_out[occ[b]] = tile[rho[b]];
+    }
+  }
+  // Locations whose store slot is 0..hot-1 (the 128 B store runs): when the
+  // last phase keeps them off its register bits, its registers can go
+  // straight to HBM (direct store, below), saving a shared-memory round trip
+  // of the whole tile. SWAP relabels can move them; the final check decides.
+  const int hot_store = dtype == HS_C128 ? 3 : 4;
+  uint32_t want_mask = 0;
+  if ((options & HS_PLAN_JIT) && cluster_log == 0 && T - RB >= hot_store)
+    for (int loc = 0; loc < T; ++loc)
+      if (rho[bit_at[loc]] < hot_store) want_mask |= 1u << loc;
+  auto nondiag_left = [&]() {
+    int c = 0;
+    for (int g = 0; g < num_gates; ++g) c += !done[g] && gs[g].cls != C_DIAG && gs[g].cls != C_SWAP;
+    return c;
+  };
   while (remaining > 0) {
     R.clear();
     // compiled parts pay a shared-memory exchange per phase: pick the
@@ -471,6 +560,11 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     if ((options & HS_PLAN_JIT) && T <= 16) {
       Yield best = phase_yield(~0u, false);
       best.mixed = 1 << 30;  // first come: mixed count unknown, any exact set with as many gates wins
+      // a phase that takes every gate left is the last one: among equally
+      // productive register sets, one that leaves the store-run locations
+      // to the lanes enables the direct store
+      const int left = nondiag_left();
+      bool best_direct = false;
       for (uint32_t m = 0; m < (1u << T); ++m) {
         if (__builtin_popcount(m) != RB) continue;
         Yield y = phase_yield(m, false);
@@ -479,10 +573,13 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
           const Yield yd = phase_yield(m, true);
           if (yd.taken == y.taken) { y = yd; d = true; }
         }
-        if (y.taken > best.taken || (y.taken == best.taken && y.mixed < best.mixed)) {
+        const bool direct_ok = want_mask && y.taken == left && !d && (m & want_mask) == 0;
+        if (y.taken > best.taken ||
+            (y.taken == best.taken && (direct_ok > best_direct || (direct_ok == best_direct && y.mixed < best.mixed)))) {
           best = y;
           allow = m;
           defer = d;
+          best_direct = direct_ok;
         }
       }
     }
@@ -603,81 +700,6 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     choose_npos(nonreg, dtype, ph.npos);
     P.prog.push_back(ph);
     phases = 1;
-  }
-  // write-back relabel rho: the qubit in tile bit b is stored at tile
-  // position rho[b] (a permutation of the tile's own positions, so the store
-  // stays in place). It is how the program's layout evolves: qubits staged
-  // soonest move to the lowest physical positions so later tiles read long
-  // contiguous runs, and the final launches steer every qubit home.
-  std::vector<int> rho(T);
-  for (int b = 0; b < T; ++b) rho[b] = b;
-  if (lay && lay->mode != LAYOUT_KEEP) {
-    std::vector<int> occ(T);  // logical position living at tile[b]
-    for (int b = 0; b < T; ++b) occ[b] = lay->inv_in ? lay->inv_in[tile[b]] : tile[b];
-    auto index_in_tile = [&](int p) {
-      auto it = std::find(tile.begin(), tile.end(), p);
-      return it == tile.end() ? -1 : int(it - tile.begin());
-    };
-    if (lay->mode == LAYOUT_OOP) {
-      // out of place: store slot bit r = the r-th lowest output position
-      // among the tile's qubits
-      std::vector<int> outp(T);
-      for (int b = 0; b < T; ++b) outp[b] = lay->target[occ[b]];
-      for (int b = 0; b < T; ++b) {
-        int r = 0;
-        for (int c = 0; c < T; ++c) r += outp[c] < outp[b];
-        rho[b] = r;
-      }
-    } else if (lay->mode == LAYOUT_PRIORITY) {
-      // the lowest 3 tile positions (the coalescing bits when they are the
-      // physical bits 0..2) go to the qubits staged soonest; qubits never
-      // staged again go home when home is in the tile (less to restore at
-      // the end); the rest fill the remaining positions by next use
-      std::vector<int> order(T);
-      for (int b = 0; b < T; ++b) order[b] = b;
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int x, int y) { return lay->next_use[occ[x]] < lay->next_use[occ[y]]; });
-      const int32_t never = 1 << 29;
-      std::vector<char> taken(T, 0), placed(T, 0);
-      const int hot = std::min(3, T);
-      for (int r = 0; r < hot; ++r) {
-        rho[order[r]] = r;
-        taken[r] = placed[order[r]] = 1;
-      }
-      for (int r = hot; r < T; ++r) {
-        const int b = order[r];
-        if (lay->next_use[occ[b]] < never) continue;
-        int h = index_in_tile(occ[b]);
-        if (h >= hot && !taken[h]) { rho[b] = h; taken[h] = placed[b] = 1; }
-      }
-      int next = 0;
-      for (int r = 0; r < T; ++r) {
-        const int b = order[r];
-        if (placed[b]) continue;
-        while (taken[next]) ++next;
-        rho[b] = next;
-        taken[next] = 1;
-      }
-    } else {  // LAYOUT_TARGET: each occupant to target[occ] when that lies in the tile
-      std::vector<char> taken(T, 0), placed(T, 0);
-      for (int b = 0; b < T; ++b) {
-        int t = index_in_tile(lay->target[occ[b]]);
-        if (t >= 0 && !taken[t]) { rho[b] = t; taken[t] = 1; placed[b] = 1; }
-      }
-      int next = 0;
-      for (int b = 0; b < T; ++b) {
-        if (placed[b]) continue;
-        while (taken[next]) ++next;
-        rho[b] = next;
-        taken[next] = 1;
-      }
-    }
-    if (lay->phys_out) {
-      if (lay->mode == LAYOUT_OOP)
-        for (int q = 0; q < n_local; ++q) lay->phys_out[q] = lay->target[q];
-      else
-        for (int b = 0; b < T; ++b) lay->phys_out[occ[b]] = tile[rho[b]];
-    }
   }
   // final store: register k holds location R[k] of the last phase, which is
   // tile bit bit_at[R[k]]; it is written to tile position rho[bit_at[R[k]]]

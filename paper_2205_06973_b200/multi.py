@@ -396,6 +396,112 @@ def run_loopback(run: ShardedRun, shards):
     return shards
 
 
+class GroupRun:
+    """One process driving 2^p shards on ``devices`` (one per GPU of the
+    node, or several on one GPU): ``ShardedRun``'s plan (layouts, segment
+    programs starting from each switch's arrival layout) with every layout
+    switch done by the C engine over peer memory (``hs_group_switch``: per
+    chunk, pack into local staging, then each shard pulls its incoming
+    segments from the senders' staging over NVLink into its own positions,
+    ordered by CUDA events across the shards' streams, no host round trip).
+    The C-ABI form of the reference's distributed run (dist.py:485-529)."""
+
+    def __init__(self, circuit, partition, num_rank_bits: int, devices, dtype="complex128", policy: str = "lookahead",
+                 staging_bytes: int = SWITCH_CHUNK_BYTES, basis_start: bool = True):
+        import ctypes
+
+        R = 1 << num_rank_bits
+        self.devices = [int(d) for d in devices]
+        if len(self.devices) != R:
+            raise ValueError(f"{len(self.devices)} devices for {R} shards")
+        # programs are per device (compiled kernels, device arenas)
+        self.runs = {d: ShardedRun(circuit, partition, num_rank_bits, loopback=True, device=f"cuda:{d}", dtype=dtype,
+                                   policy=policy, basis_start=basis_start) for d in sorted(set(self.devices))}
+        plan = self.plan = self.runs[self.devices[0]]
+        self.n_local, self.stats, self.layouts = plan.n_local, plan.stats, plan.layouts
+        self.dtype = dtype
+        lib = _native.load()
+        out = ctypes.c_void_p()
+        devs = (ctypes.c_int32 * R)(*self.devices)
+        _native.check(lib.hs_group_create(R, devs, int(staging_bytes), ctypes.byref(out)))
+        self._h, self._lib = out.value, lib
+        # per switch: segment positions, destinations and arrival slots
+        self.switch_args = {}
+        for si, (a, _) in enumerate(plan.segments):
+            if a not in plan.switch_at:
+                continue
+            old, new, _ = plan.switch_at[a]
+            A, _, pa = plan.switch_plan(old, new, plan.seg_phys_out[si - 1])
+            sched = [switch_schedule(old, new, r, A) for r in range(R)]
+            c = sched[0][4]
+            dst = [0] * (R << c)
+            slot = [-1] * R
+            for r in range(R):
+                for seg in sched[r][1]:
+                    dst[(r << c) | seg.index] = seg.peer
+                for src, j in sched[r][2].items():
+                    slot[src] = j
+            self.switch_args[a] = ((ctypes.c_int32 * max(1, c))(*pa), c, (ctypes.c_int32 * (R << c))(*dst),
+                                   (ctypes.c_int32 * R)(*slot))
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            try:
+                self._lib.hs_group_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+
+    def allocate(self):
+        """One shard per device entry, |0..0> (shard 0 holds amplitude 1)."""
+        import torch
+
+        from .statevec import allocate, init_basis
+
+        shards = [allocate(self.n_local, self.dtype, f"cuda:{d}") for d in self.devices]
+        for r, sh in enumerate(shards):
+            with torch.cuda.device(sh.device):
+                if r == 0:
+                    init_basis(sh, 0)
+                else:
+                    sh.zero_()
+        return shards
+
+    def run(self, shards, with_timing: bool = False):
+        """Every part and switch on the shards (in place); returns them in
+        natural order of the last layout. ``with_timing``:
+        ``stats.switch_time_s`` = each switch's device time, max over shards."""
+        import ctypes
+
+        import torch
+
+        from .statevec import native_dtype
+
+        R = len(self.devices)
+        ptrs = (ctypes.c_void_p * R)(*[sh.data_ptr() for sh in shards])
+        streams = (ctypes.c_void_p * R)(*[torch.cuda.current_stream(sh.device).cuda_stream for sh in shards])
+        code = native_dtype(shards[0])
+        times = []
+        for si, (a, _) in enumerate(self.plan.segments):
+            if a in self.switch_args:
+                pa, c, dst, slot = self.switch_args[a]
+                sec = ctypes.c_double()
+                _native.check(self._lib.hs_group_switch(self._h, ptrs, self.n_local, code, pa, c, dst, slot, streams,
+                                                        ctypes.byref(sec) if with_timing else None))
+                times.append(sec.value)
+            for d, run in self.runs.items():
+                if run.programs[si] is None:
+                    continue
+                mine = [sh for r, sh in enumerate(shards) if self.devices[r] == d]
+                with torch.cuda.device(d):
+                    run._share_scratch(mine[0])
+                    for sh in mine:
+                        run.programs[si].run(sh)
+        if with_timing:
+            self.stats.switch_time_s = times
+        return shards
+
+
 def _wire(t):
     """complex tensors travel as their real view (NCCL has no complex type)."""
     import torch
@@ -448,5 +554,5 @@ def shard_positions(layout: RankLayout, rank: int):
     return g
 
 
-__all__ = ["ShardedRun", "ShardedState", "DeviceOps", "switch_schedule", "simulate_distributed_group", "run_loopback",
+__all__ = ["ShardedRun", "GroupRun", "ShardedState", "DeviceOps", "switch_schedule", "simulate_distributed_group", "run_loopback",
            "shard_positions", "storage_order", "math"]

@@ -735,3 +735,44 @@ def test_benched_programs_match_c_oracle_at_full_size(name):
     torch.cuda.synchronize()
     buf.copy_(host_out)
     assert err(buf) < 1e-10
+
+
+@pytest.mark.parametrize("policy", ["reference", "lookahead"])
+def test_group_run_peer_switches_on_one_gpu(golden, policy):
+    """GroupRun: the C multi-device engine (hs_group_switch: pack into
+    staging, pull over peer memory with hs_unpack_segments_range_from,
+    event-ordered across shard streams) with every shard on device 0, on the
+    corpus against the reference's distributed results, and at 24 qubits
+    over 4 shards with a small staging buffer (many double-buffered chunks)
+    against the C oracle, with per-switch device times."""
+    from paper_2205_06973_b200.multi import GroupRun, shard_positions
+
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    checked = 0
+    for i, doc in enumerate(docs):
+        c = parse_qasm(doc["qasm"])
+        for d in doc["dist"]:
+            if not d["switches"] or c.num_qubits < 8:
+                continue
+            R = 1 << d["p"]
+            run = GroupRun(c, partition_of(d["parts"]), d["p"], [0] * R, policy=policy, staging_bytes=4096)
+            if policy == "reference":
+                assert [[list(x.local), list(x.process)] for x in run.layouts] == d["layouts"]
+            shards = run.run(run.allocate())
+            full = np.zeros(1 << c.num_qubits, dtype=np.complex128)
+            for r in range(R):
+                full[shard_positions(run.layouts[-1], r)] = shards[r].cpu().numpy()
+            assert np.max(np.abs(full - states[f"c{i}"])) < 1e-10, (i, d["p"])
+            checked += 1
+    assert checked >= 5
+    c = configs.build("c3@24")
+    part = partition_dfs(build_dag(c), 12)
+    run = GroupRun(c, part, 2, [0, 0, 0, 0], policy=policy, staging_bytes=1 << 20)
+    assert run.stats.num_switches > 0
+    shards = run.run(run.allocate(), with_timing=True)
+    assert len(run.stats.switch_time_s) == run.stats.num_switches and min(run.stats.switch_time_s) > 0
+    full = np.zeros(1 << c.num_qubits, dtype=np.complex128)
+    for r in range(4):
+        full[shard_positions(run.layouts[-1], r)] = shards[r].cpu().numpy()
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert float(np.max(np.abs(full - ref))) < 1e-10
