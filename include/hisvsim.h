@@ -310,9 +310,10 @@ int hs_group_destroy(hs_group* group);
  * their positions. Chunk by chunk of inner offsets: every shard packs its
  * outgoing segments into local staging, then pulls its incoming segments
  * from the senders' staging over peer memory into its own shard. Launches
- * on streams[r] (NULL: the group's own streams) with cross-shard event
- * ordering; asynchronous unless *seconds is requested (then the max over
- * shards of the switch's device time is written after a sync). */
+ * on streams[r] (a NULL entry is the legacy default stream; a NULL array:
+ * the group's own streams) with cross-shard event ordering; asynchronous
+ * unless *seconds is requested (then the max over shards of the switch's
+ * device time is written after a sync). */
 int hs_group_switch(hs_group* group, void* const* shards, int n_local, int dtype, const int32_t* seg_pos,
                     int num_seg_bits, const int32_t* seg_dst, const int32_t* src_slot, void* const* streams,
                     double* seconds);

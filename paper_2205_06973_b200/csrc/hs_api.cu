@@ -730,7 +730,8 @@ int hs_group_switch(hs_group* g, void* const* shards, int n_local, int dtype, co
   const size_t amp = dtype == HS_C128 ? 16 : 8;
   const int64_t inner = int64_t(1) << (n_local - nseg);
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(inner, int64_t(g->staging_bytes / (amp * S))));
-  auto stream_of = [&](int r) { return streams && streams[r] ? (cudaStream_t)streams[r] : g->streams[r]; };
+  // a given array is taken as is (a NULL entry is the legacy default stream)
+  auto stream_of = [&](int r) { return streams ? (cudaStream_t)streams[r] : g->streams[r]; };
   if (seconds)
     for (int r = 0; r < R; ++r) {
       HS_CUDA(cudaSetDevice(g->devices[r]), "cudaSetDevice");

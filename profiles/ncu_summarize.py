@@ -27,6 +27,10 @@ KEYS = {
     "stall_lg": "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
     "stall_branch": "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
     "inst": "smsp__inst_executed.sum",
+    "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "lsu_wavefronts_pct_peak": "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "dram_pct_peak": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm_mhz": "sm__cycles_elapsed.avg.per_second",
 }
 
 
@@ -49,6 +53,10 @@ def raw(rep):
                     v /= 1e9
                 if units[idx[m]] == "us":
                     v /= 1e3
+                if units[idx[m]] == "Ghz":
+                    v *= 1e3  # sm_mhz
+                elif units[idx[m]] == "Mhz":
+                    pass
                 d[k] = v
         res.append(d)
     return res
@@ -76,18 +84,15 @@ def mix(rep):
             for op, _ in ex.most_common(12)}
 
 
-if __name__ == "__main__":
-    rep = sys.argv[1]
-    print(json.dumps({"launches": raw(rep), "first_launch_sass_mix": mix(rep)}, indent=1))
-
-
-def write_summary(rep: str, workload: str, out: str, note: str = "") -> dict:
+def write_summary(rep: str, workload: str, out: str, note: str = "", seq: int = 0, command: str = "") -> dict:
     """Condensed, committed form of one capture (read by bench.py for
     roofline.traffic): per-launch metrics + instruction mix."""
     launches = raw(rep)
     per = [1e9 * (l.get("dram_read_GB", 0) + l.get("dram_write_GB", 0)) for l in launches]
     doc = {
+        "capture_seq": seq,
         "workload": workload,
+        "command": command,
         "source_report": rep,
         "note": note,
         "dram_bytes_per_launch": sum(per) / len(per) if per else None,
@@ -97,3 +102,12 @@ def write_summary(rep: str, workload: str, out: str, note: str = "") -> dict:
     with open(out, "w") as f:
         json.dump(doc, f, indent=1)
     return doc
+
+
+if __name__ == "__main__":
+    if len(sys.argv) >= 4:  # rep workload out [seq] [note] [command]
+        a = sys.argv
+        write_summary(a[1], a[2], a[3], note=a[5] if len(a) > 5 else "", seq=int(a[4]) if len(a) > 4 else 0,
+                      command=a[6] if len(a) > 6 else "")
+    else:
+        print(json.dumps({"launches": raw(sys.argv[1]), "first_launch_sass_mix": mix(sys.argv[1])}, indent=1))
