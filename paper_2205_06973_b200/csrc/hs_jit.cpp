@@ -43,6 +43,14 @@ uint32_t swz_host(uint32_t s, bool c128) {
 
 int sizeof_amp(bool c128) { return c128 ? 16 : 8; }
 
+// tiles ahead the compiled kernels prefetch into L2 ($HISVSIM_L2_PREFETCH,
+// default 2; 0 disables)
+int l2_prefetch_ahead() {
+  const char* e = std::getenv("HISVSIM_L2_PREFETCH");
+  if (!e || !*e) return 2;
+  return std::max(0, std::min(8, std::atoi(e)));
+}
+
 std::string lit(double v, bool c128) {
   char buf[64];
   std::snprintf(buf, sizeof(buf), "%a", v);
@@ -708,6 +716,28 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   }
   o << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"((unsigned)__cvta_generic_to_shared(&full[b])) : \"memory\");\n";
   o << "    if (tid0 == 0) issued[b] = (int)(i / 3);\n";
+  // L2 prefetch of the tile `ahead` loads later: the three tile buffers keep
+  // at most one tile (64 KB) of reads in flight per SM, below what HBM
+  // latency x per-SM bandwidth needs; lines prefetched into L2 a few tiles
+  // early make those cp.async loads L2 hits. One prefetch per 128 B line:
+  // only threads / registers whose tile bits on storage positions 0..2 are
+  // zero issue one.
+  const int ahead = l2_prefetch_ahead();
+  if (ahead > 0 && cl == 0) {
+    uint32_t lane_mask = 0, reg_mask = 0;
+    for (int k = 0; k < low; ++k)
+      if (pl.launch.tpos[k] < 3) lane_mask |= 1u << k;
+    for (int k = 0; k < RB; ++k)
+      if (pl.launch.tpos[low + k] < 3) reg_mask |= 1u << k;
+    o << "    { const long long tp = cid + (i + " << ahead << ") * (long long)ncl;\n";
+    o << "      if (tp < ntiles && (tid0 & " << lane_mask << "u) == 0u) {\n";
+    o << "        const unsigned long long pb = tile_base(tp);\n";
+    for (int j = 0; j < g.nreg; ++j) {
+      if (uint32_t(j) & reg_mask) continue;
+      o << "        asm volatile(\"prefetch.global.L2 [%0];\" :: \"l\"(psi + (pb | " << hi_of(j) << "ull)));\n";
+    }
+    o << "      } }\n";
+  }
   o << "  };\n";
   o << "  issue(team);\n  if (team == 0) issue(2);\n";
   o << "  for (long long i = team;; i += 2) {\n";

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <functional>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "hs_common.h"
@@ -1162,9 +1164,17 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
         if (s != HS_OK) return s;
         size_t la = 0;
         if ((s = planned(ap, ag, &la)) != HS_OK) return s;
+        if (std::getenv("HISVSIM_PLAN_DEBUG"))
+          std::fprintf(stderr, "[plan] grouping %d: %zu passes, %zu launches, cost %.1f\n", (int)mode, ap.size(), la, c);
         // fewest launches; among as few, the lowest pass_cost (measured c3:
         // 13 launches with one short-read pass 96.3 ms, 14 coalesced 96.6-97.4)
-        if (la < best_launches || (regrouped && la == best_launches && c < cost)) {
+        static const bool by_cost = [] {
+          const char* e = std::getenv("HISVSIM_PLAN_SELECT");
+          return e && std::string(e) == "cost";
+        }();
+        const bool better = by_cost ? (c < cost || (c == cost && la < best_launches))
+                                    : (la < best_launches || (regrouped && la == best_launches && c < cost));
+        if (better) {
           xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c; best_launches = la;
           regrouped = true;
         }
