@@ -43,11 +43,21 @@ uint32_t swz_host(uint32_t s, bool c128) {
 
 int sizeof_amp(bool c128) { return c128 ? 16 : 8; }
 
-// tiles ahead the compiled kernels prefetch into L2 ($HISVSIM_L2_PREFETCH,
-// default 2; 0 disables)
+// tiles ahead the compiled kernels prefetch into L2 ($HISVSIM_L2_PREFETCH;
+// default 0 = off: measured on c3, 1 / 2 / 3 / 5 tiles ahead cost 88.5 ->
+// 97.8 / 98.5 / 115.9 / 126.8 ms, c2 5.26 -> 5.51 ms at 2)
+// experiment switches read at code generation (part of the source, hence of
+// the cubin cache key): HISVSIM_STORE_CS=1 stores the tile with st.global.cs
+// (evict-first), HISVSIM_TILE_ORDER=chunk gives each CTA a contiguous range
+// of tiles instead of the grid stride
+bool env_on(const char* name, const char* value) {
+  const char* e = std::getenv(name);
+  return e && std::string(e) == value;
+}
+
 int l2_prefetch_ahead() {
   const char* e = std::getenv("HISVSIM_L2_PREFETCH");
-  if (!e || !*e) return 2;
+  if (!e || !*e) return 0;
   return std::max(0, std::min(8, std::atoi(e)));
 }
 
@@ -647,6 +657,14 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   } else {
     o << "  const unsigned rank = 0, cid = blockIdx.x, ncl = gridDim.x, sw_rank = 0;\n";
   }
+  if (cl == 0 && env_on("HISVSIM_TILE_ORDER", "chunk")) {
+    o << "  const long long per_cta = (ntiles + ncl - 1) / ncl;\n";
+    o << "#define TILE(i) ((long long)cid * per_cta + (i))\n";
+    o << "#define TILE_OK(i, t) ((i) < per_cta && (t) < ntiles)\n";
+  } else {
+    o << "#define TILE(i) ((long long)cid + (i) * (long long)ncl)\n";
+    o << "#define TILE_OK(i, t) ((t) < ntiles)\n";
+  }
   o << "  if (threadIdx.x == 0) {\n";
   o << "    for (int b = 0; b < 3; ++b) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], " << NT
     << ";\" :: \"r\"((unsigned)__cvta_generic_to_shared(&full[b])) : \"memory\");\n";
@@ -703,8 +721,8 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   };
   // issue the loads of CTA tile i into buffer i % 3 (this thread's share)
   o << "  auto issue = [&](long long i) {\n";
-  o << "    const long long tt = cid + i * (long long)ncl;\n";
-  o << "    if (tt >= ntiles) return;\n";
+  o << "    const long long tt = TILE(i);\n";
+  o << "    if (!TILE_OK(i, tt)) return;\n";
   o << "    const unsigned long long base = tile_base(tt);\n";
   o << "    const int b = (int)(i % 3);\n";
   o << "    const unsigned sb = (unsigned)__cvta_generic_to_shared(smem_raw) + b * " << tile_bytes << "u;\n";
@@ -729,8 +747,8 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       if (pl.launch.tpos[k] < 3) lane_mask |= 1u << k;
     for (int k = 0; k < RB; ++k)
       if (pl.launch.tpos[low + k] < 3) reg_mask |= 1u << k;
-    o << "    { const long long tp = cid + (i + " << ahead << ") * (long long)ncl;\n";
-    o << "      if (tp < ntiles && (tid0 & " << lane_mask << "u) == 0u) {\n";
+    o << "    { const long long tp = TILE(i + " << ahead << ");\n";
+    o << "      if (TILE_OK(i + " << ahead << ", tp) && (tid0 & " << lane_mask << "u) == 0u) {\n";
     o << "        const unsigned long long pb = tile_base(tp);\n";
     for (int j = 0; j < g.nreg; ++j) {
       if (uint32_t(j) & reg_mask) continue;
@@ -741,8 +759,8 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "  };\n";
   o << "  issue(team);\n  if (team == 0) issue(2);\n";
   o << "  for (long long i = team;; i += 2) {\n";
-  o << "    const long long tt = cid + i * (long long)ncl;\n";
-  o << "    if (tt >= ntiles) break;\n";
+  o << "    const long long tt = TILE(i);\n";
+  o << "    if (!TILE_OK(i, tt)) break;\n";
   o << "    const unsigned long long base = tile_base(tt);\n";
   o << "    unsigned tid = tid0 | (rank << " << low << "); asm volatile(\"\" : \"+r\"(tid));  // keep phase addresses in the loop\n";
   o << "    const int b = (int)(i % 3);\n";
@@ -782,6 +800,10 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       uint64_t off = 0;
       for (int k = 0; k < RB; ++k)
         if (i >> k & 1) off |= 1ull << pos[pl.launch.fin_rpos[k]];
+      if (env_on("HISVSIM_STORE_CS", "1"))
+      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; __stcs(&" << (oop ? "psi_out" : "psi")
+        << "[dbase | " << off << "ull], v); }\n";
+    else
       o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; " << (oop ? "psi_out" : "psi") << "[dbase | "
         << off << "ull] = v; }\n";
     }
@@ -789,7 +811,11 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   } else {
     for (int j = 0; j < g.nreg; ++j) {
       const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
-      o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
+      if (env_on("HISVSIM_STORE_CS", "1"))
+        o << "    __stcs(&" << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull], sm[sw_tid ^ " << sx
+          << "u]);\n";
+      else
+        o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
     }
     o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
     o << "    issue(i + 3);\n";
