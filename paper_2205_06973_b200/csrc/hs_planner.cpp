@@ -1112,6 +1112,14 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
 // the gate-free final permutation unnecessary: 3 bits = 128 B of complex128
 // (measured: c2 5.96 ms with a 1 KB-run rule and 9 launches vs 5.56 ms with
 // 128 B runs and 8; c3 96.6 vs 94.9 ms; 64 B runs lose: c2 6.51 vs 5.74 ms)
+// positions at the bottom of an out-of-place pass's next layout given to the
+// next pass's qubits ($HISVSIM_NEXT_LOW; 3 = the store run only)
+int next_low_positions() {
+  const char* e = std::getenv("HISVSIM_NEXT_LOW");
+  if (!e || !*e) return 3;
+  return std::max(3, std::min(62, std::atoi(e)));
+}
+
 int final_hot(int n_local, int tile_max) {
   return std::min(3, std::max(1, std::min(n_local, tile_max / 2)));
 }
@@ -1308,14 +1316,27 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
           for (int pp_ : tpos)
             if ((nxt[inv[pp_]] != 0) == (pass == 0)) cand.push_back(inv[pp_]);
         std::vector<int32_t> tinv(inv);
-        for (int r = 0; r < hot && r < (int)cand.size(); ++r) {
-          const int q = cand[r], pq = tgt[q];
-          if (pq == r) continue;
+        auto place = [&](int q, int r) {  // q to position r, its occupant to q's old one
+          const int pq = tgt[q];
+          if (pq == r) return;
           const int o = tinv[r];
           tgt[o] = pq;
           tinv[pq] = o;
           tgt[q] = r;
           tinv[r] = q;
+        };
+        for (int r = 0; r < hot && r < (int)cand.size(); ++r) place(cand[r], r);
+        // Out of place any permutation of the positions above the store run
+        // is free (stores stay 128 B runs): the next pass's other qubits -
+        // tile or free - take the positions right above, so its tile reads
+        // longer runs / fewer DRAM pages (HISVSIM_NEXT_LOW positions in all)
+        const int next_low = std::min(n_local, next_low_positions());
+        int r = hot;
+        for (int p = 0; p < n_local && r < next_low; ++p) {
+          const int q = tinv[p];
+          if (p < hot || !nxt[q]) continue;
+          if (p >= r) place(q, r);
+          ++r;
         }
       }
       lay.target = tgt.data();
