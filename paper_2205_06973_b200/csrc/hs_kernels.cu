@@ -285,8 +285,15 @@ constexpr int max_threads() {
   return ((sizeof(R) == 8 ? 4096 : 8192) >> RB) > 1024 ? 1024 : ((sizeof(R) == 8 ? 4096 : 8192) >> RB);
 }
 
+// two CTAs per SM; a 1024-thread CTA alone (two would leave 32 registers a
+// thread: 176-244 B of spills per thread)
+template <typename R, int RB>
+constexpr int min_ctas() {
+  return max_threads<R, RB>() >= 1024 ? 1 : 2;
+}
+
 template <typename R, int RB, bool CPROG>
-__global__ void __launch_bounds__(max_threads<R, RB>(), 2)
+__global__ void __launch_bounds__(max_threads<R, RB>(), min_ctas<R, RB>())
 hs_part_kernel(const KParams p) {
   using C = typename Cx<R>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -432,10 +432,27 @@ def run_part(data, exe: ExecutablePart) -> None:
     if not t.is_contiguous():
         raise ValueError("arr must be C-contiguous")
     if exe.ops:
-        prog = PartProgram(m, [exe], dtype=t.dtype, device=t.device)
-        prog.run(t)
+        _run_part_program(m, exe, t.dtype, t.device).run(t)
     if back is not None:
         back()
+
+
+#: planned one-part programs of recent ``run_part`` / ``apply_op`` calls: a
+#: gate-by-gate caller (apply_gate in a loop, statevec.py:241-266) plans and
+#: uploads each distinct (state size, part) once instead of per call
+_RUN_PART_CACHE: "dict[tuple, PartProgram]" = {}
+RUN_PART_CACHE_SIZE = 256
+
+
+def _run_part_program(m: int, exe: ExecutablePart, dtype, device) -> "PartProgram":
+    key = (m, str(dtype), str(device), exe.slot_map.qubits, exe.ops, exe.op_slots, _native.default_options())
+    prog = _RUN_PART_CACHE.pop(key, None)
+    if prog is None:
+        prog = PartProgram(m, [exe], dtype=dtype, device=device)
+        while len(_RUN_PART_CACHE) >= RUN_PART_CACHE_SIZE:
+            _RUN_PART_CACHE.pop(next(iter(_RUN_PART_CACHE)))
+    _RUN_PART_CACHE[key] = prog  # most recently used last
+    return prog
 
 
 # --- traces ---------------------------------------------------------------------

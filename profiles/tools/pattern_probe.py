@@ -40,13 +40,30 @@ def program(staged, dense):
     return PartProgram(N, [exe], options=opts)
 
 
+SWEEP = {  # which tile positions make a pass slow (only the Z cases)
+    "0-2 + 12..20": [0, 1, 2] + list(range(12, 21)),
+    "0-3 + 13..20": [0, 1, 2, 3] + list(range(13, 21)),
+    "0-2,5 + 13..20": [0, 1, 2, 5] + list(range(13, 21)),
+    "0-2,7 + 13..20": [0, 1, 2, 7] + list(range(13, 21)),
+    "0-2,9 + 13..20": [0, 1, 2, 9] + list(range(13, 21)),
+    "0-2,11 + 13..20": [0, 1, 2, 11] + list(range(13, 21)),
+    "0-2 + 20..28": [0, 1, 2] + list(range(20, 29)),
+    "0-2 + even 12..28": [0, 1, 2] + list(range(12, 29, 2)),
+    "0-5 + 20..25": list(range(6)) + list(range(20, 26)),
+    "0-2,4,6,8 + 14..19": [0, 1, 2, 4, 6, 8] + list(range(14, 20)),
+}
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "sweep":
+        CASES.clear()
+        CASES.update(SWEEP)
     state = allocate(N)
     state.zero_()
     state[0] = 1
     out = {}
     for name, staged in CASES.items():
-        for dense in (False, True):
+        for dense in ((False,) if len(sys.argv) > 1 else (False, True)):
             prog = program(staged, dense)
             for _ in range(3):
                 prog.run(state)

@@ -776,3 +776,18 @@ def test_group_run_peer_switches_on_one_gpu(golden, policy):
         full[shard_positions(run.layouts[-1], r)] = shards[r].cpu().numpy()
     ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
     assert float(np.max(np.abs(full - ref))) < 1e-10
+
+
+def test_c_host_program_runs_a_sharded_circuit(tmp_path):
+    """A C program (no Python) runs 12 qubits over 2 shards through the C ABI:
+    part, hs_group_switch over peer memory, part; it checks the shards
+    against its own host simulation and exits 0 below 1e-12."""
+    import json
+    import subprocess
+
+    from test_native_abi import _build_group_demo
+
+    exe = _build_group_demo(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert json.loads(out.stdout.strip().splitlines()[-1])["max_abs_delta"] < 1e-12

@@ -415,3 +415,24 @@ def test_final_layout_is_natural_unless_no_restore(name, limit):
     for q in range(n):
         where |= ((idx >> q) & 1) << fp[q]
     assert np.max(np.abs(psi[0][where] - want)) < 1e-12
+
+
+def _build_group_demo(tmp_path):
+    import shutil
+    import subprocess
+
+    root = Path(__file__).resolve().parent.parent
+    lib = root / "paper_2205_06973_b200" / "_lib"
+    exe = tmp_path / "group_demo"
+    cc = shutil.which("gcc") or "gcc"
+    cmd = [cc, "-O2", "-std=c11", "-I", str(root / "include"), "-I", "/usr/local/cuda/include",
+           str(root / "tests" / "c" / "group_demo.c"), "-L", str(lib), "-lhisvsim", "-L", "/usr/local/cuda/lib64",
+           "-lcudart", "-lm", f"-Wl,-rpath,{lib}", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_host_program_builds_against_the_header(tmp_path):
+    """tests/c/group_demo.c drives a sharded run (programs, hs_group_switch)
+    through include/hisvsim.h alone: it compiles and links with gcc."""
+    assert _build_group_demo(tmp_path).exists()
