@@ -24,6 +24,15 @@
 
 namespace hs {
 
+// lowest storage positions each pass hands to the next pass's qubits from
+// its own tile ($HISVSIM_HOT, default 3: 128 B runs of complex128)
+int layout_hot() {
+  const char* e = std::getenv("HISVSIM_HOT");
+  if (!e || !*e) return 3;
+  return std::max(1, std::min(8, std::atoi(e)));
+}
+
+
 bool base_matrix(int kind, const double* p, double m[8]) {
   const double r2 = 1.0 / std::sqrt(2.0);
   auto set = [&](double a, double b, double c, double d, double e, double f, double g,
@@ -496,7 +505,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
                        [&](int x, int y) { return lay->next_use[occ[x]] < lay->next_use[occ[y]]; });
       const int32_t never = 1 << 29;
       std::vector<char> taken(T, 0), placed(T, 0);
-      const int hot = std::min(3, T);
+      const int hot = std::min(layout_hot(), T);
       for (int r = 0; r < hot; ++r) {
         rho[order[r]] = r;
         taken[r] = placed[order[r]] = 1;
@@ -1246,7 +1255,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
   // runs) c2 5.42 vs 5.55 ms, c3 95.0 vs 95.4 ms, c1 equal (an earlier
   // planner measured the opposite: c3 126 vs 121 ms). The gate-free final
   // permutation stages at most 2 * hot qubits.
-  const int hot = std::min(3, std::max(1, std::min(n_local, tile_max / 2)));
+  const int hot = std::min(layout_hot(), std::max(1, std::min(n_local, tile_max / 2)));
   const bool no_restore = (options & HS_PLAN_NO_RESTORE) != 0;
   // The last part's tile takes the lowest logical qubits it does not stage
   // as its extra bits; it writes natural order itself when those and its
