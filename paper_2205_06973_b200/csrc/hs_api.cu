@@ -75,6 +75,7 @@ struct hs_program {
   void* graph_scratch = nullptr;
   int64_t graph_batch = 0;
   cudaStream_t graph_stream = nullptr;
+  int teams = 2;  // teams per CTA of the compiled kernels (jit_teams at compile time)
 };
 
 namespace {
@@ -196,6 +197,7 @@ static int program_create(hs_engine* eng, int n_local, int dtype, const hs_part*
   prog->user_parts = num_parts;
   if (eng->options & HS_PLAN_JIT) {
     std::string err;
+    prog->teams = jit_teams();
     HS_CUDA(cudaSetDevice(eng->device), "cudaSetDevice");
     int s = jit_compile_program(prog->plans, dtype, n_local, eng->device, eng->smem_optin, err);
     if (s != HS_OK) prog->jit_error = err;  // interpreter fallback on the GPU, reported
@@ -296,9 +298,10 @@ static int run_range(hs_program* prog, void* state, int64_t batch, int first, in
       // one CTA per SM, two teams, three tile buffers + their mbarriers (hs_jit.cpp)
       const size_t smem = 3 * (size_t(prog->dtype == HS_C128 ? 16 : 8) << pl.launch.T) + 64;
       long long grid = (long long)eng->num_sms;
-      if (grid > (ntiles + 1) / 2) grid = (ntiles + 1) / 2;
-      HS_CUDA(cudaLaunchKernel((const void*)pl.jit, dim3((unsigned)grid), dim3(2u << (pl.launch.T - pl.launch.RB)),
-                               args, smem, s),
+      const int teams = prog->teams;
+      if (grid > (ntiles + teams - 1) / teams) grid = (ntiles + teams - 1) / teams;
+      HS_CUDA(cudaLaunchKernel((const void*)pl.jit, dim3((unsigned)grid),
+                               dim3((unsigned)teams << (pl.launch.T - pl.launch.RB)), args, smem, s),
               "compiled part kernel launch");
       continue;
     }

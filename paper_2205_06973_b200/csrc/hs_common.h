@@ -80,6 +80,7 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
                         std::string& err);
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local);
 void jit_cache_stats(int* disk_hits, int* compiles);
+int jit_teams();
 
 // Program-level qubit layout: logical position q (what parts stage) lives at
 // physical bit phys[q] of the buffer. A part's write-back may permute the

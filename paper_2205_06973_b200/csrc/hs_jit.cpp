@@ -34,6 +34,8 @@
 
 namespace hs {
 
+int jit_teams();
+
 namespace {
 
 uint32_t swz_host(uint32_t s, bool c128) {
@@ -637,7 +639,10 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       << "  ++k;\n}\n";
     o << "#define TEAM_CSYNC() team_csync(tb_team, csync_k, bar_id, tid0)\n";
   }
-  o << "extern \"C\" __global__ void __launch_bounds__(" << 2 * NT << ", 1) hs_jit_part(C* psi, C* psi_out, long long ntiles) {\n";
+  // teams per CTA ($HISVSIM_TEAMS): 2 (default) alternate tiles; 1 keeps two
+  // tile loads in flight while the single team computes (cluster tiles: 2)
+  const int TEAMS = cl > 0 ? 2 : jit_teams();
+  o << "extern \"C\" __global__ void __launch_bounds__(" << TEAMS * NT << ", 1) hs_jit_part(C* psi, C* psi_out, long long ntiles) {\n";
   o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
   o << "  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + " << 3 * tile_bytes << ");\n";
   o << "  volatile int* issued = reinterpret_cast<volatile int*>(smem_raw + " << 3 * tile_bytes + 32 << ");\n";
@@ -757,8 +762,13 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
     o << "      } }\n";
   }
   o << "  };\n";
-  o << "  issue(team);\n  if (team == 0) issue(2);\n";
-  o << "  for (long long i = team;; i += 2) {\n";
+  if (TEAMS == 2) {
+    o << "  issue(team);\n  if (team == 0) issue(2);\n";
+    o << "  for (long long i = team;; i += 2) {\n";
+  } else {
+    o << "  issue(0);\n  issue(1);\n  issue(2);\n";
+    o << "  for (long long i = 0;; ++i) {\n";
+  }
   o << "    const long long tt = TILE(i);\n";
   o << "    if (!TILE_OK(i, tt)) break;\n";
   o << "    const unsigned long long base = tile_base(tt);\n";
@@ -993,6 +1003,11 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
 }
 
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local) { return jit_source(pl, dtype, n_local); }
+
+int jit_teams() {
+  const char* e = std::getenv("HISVSIM_TEAMS");
+  return (e && std::atoi(e) == 1) ? 1 : 2;
+}
 
 void jit_cache_stats(int* disk_hits, int* compiles) {
   if (disk_hits) *disk_hits = g_disk_hits.load();
