@@ -396,6 +396,31 @@ def run_loopback(run: ShardedRun, shards):
     return shards
 
 
+def group_switch_args(plan: "ShardedRun", si: int):
+    """hs_group_switch arguments of the switch before segment ``si`` of a
+    planned run: (seg_pos, c, seg_dst[R << c], src_slot[R]). Shard r's
+    segment k (its outgoing qubits A, on physical positions seg_pos, spell k)
+    goes to shard seg_dst[r << c | k] and lands in the positions of segment
+    src_slot[r] there (the values of r's incoming qubits B)."""
+    a = plan.segments[si][0]
+    old, new, _ = plan.switch_at[a]
+    # the layout the previous segment leaves (None: natural, e.g. host-side
+    # plans without device programs)
+    phys = plan.seg_phys_out[si - 1] if 0 < si <= len(plan.seg_phys_out) else None
+    A, _, pa = plan.switch_plan(old, new, phys)
+    R = 1 << plan.p
+    sched = [switch_schedule(old, new, r, A) for r in range(R)]
+    c = sched[0][4]
+    dst = [0] * (R << c)
+    slot = [-1] * R
+    for r in range(R):
+        for seg in sched[r][1]:
+            dst[(r << c) | seg.index] = seg.peer
+        for src, j in sched[r][2].items():
+            slot[src] = j
+    return list(pa), c, dst, slot
+
+
 class GroupRun:
     """One process driving 2^p shards on ``devices`` (one per GPU of the
     node, or several on one GPU): ``ShardedRun``'s plan (layouts, segment
@@ -430,17 +455,7 @@ class GroupRun:
         for si, (a, _) in enumerate(plan.segments):
             if a not in plan.switch_at:
                 continue
-            old, new, _ = plan.switch_at[a]
-            A, _, pa = plan.switch_plan(old, new, plan.seg_phys_out[si - 1])
-            sched = [switch_schedule(old, new, r, A) for r in range(R)]
-            c = sched[0][4]
-            dst = [0] * (R << c)
-            slot = [-1] * R
-            for r in range(R):
-                for seg in sched[r][1]:
-                    dst[(r << c) | seg.index] = seg.peer
-                for src, j in sched[r][2].items():
-                    slot[src] = j
+            pa, c, dst, slot = group_switch_args(plan, si)
             self.switch_args[a] = ((ctypes.c_int32 * max(1, c))(*pa), c, (ctypes.c_int32 * (R << c))(*dst),
                                    (ctypes.c_int32 * R)(*slot))
 
@@ -554,5 +569,5 @@ def shard_positions(layout: RankLayout, rank: int):
     return g
 
 
-__all__ = ["ShardedRun", "GroupRun", "ShardedState", "DeviceOps", "switch_schedule", "simulate_distributed_group", "run_loopback",
+__all__ = ["ShardedRun", "GroupRun", "group_switch_args", "ShardedState", "DeviceOps", "switch_schedule", "simulate_distributed_group", "run_loopback",
            "shard_positions", "storage_order", "math"]

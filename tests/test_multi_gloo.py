@@ -132,3 +132,70 @@ def test_sharded_run_over_gloo_matches_reference(golden, world, policy):
             assert out[0][2] == ref_bytes
         else:  # the lookahead schedule never moves more
             assert out[0][2] <= ref_bytes
+
+
+def _emulate_group_switch(shards, nbits, seg_pos, c, seg_dst, src_slot, chunk):
+    """numpy model of hs_group_switch's contract (include/hisvsim.h): per
+    chunk of inner offsets every shard packs its segments into staging, then
+    pulls slot j from the staging segment of the shard whose data lands in
+    slot j and whose segment goes here."""
+    R, S = len(shards), 1 << c
+    inner = 1 << (nbits - c)
+    src_of = {}
+    for s in range(R):
+        for k in range(S):
+            src_of[(seg_dst[s * S + k], src_slot[s])] = (s, k)
+    for begin in range(0, inner, chunk):
+        m = np.arange(begin, min(inner, begin + chunk), dtype=np.int64)
+        staging = [[sh[_compose(k, m, seg_pos, nbits)].copy() for k in range(S)] for sh in shards]
+        for r in range(R):
+            for j in range(S):
+                s, k = src_of[(r, j)]
+                shards[r][_compose(j, m, seg_pos, nbits)] = staging[s][k]
+    return shards
+
+
+def test_group_switch_arguments_reproduce_the_reference_runs(golden):
+    """multi.group_switch_args + the hs_group_switch contract (emulated in
+    numpy, small chunks) with numpy part passes reproduce the reference's
+    distributed states on the corpus (both remap policies)."""
+    from conftest import partition_of
+    from oracle import hisim_oracle as orc
+    from paper_2205_06973_b200.multi import ShardedRun, group_switch_args, shard_positions
+    from paper_2205_06973_b200.qasm import parse_qasm
+
+    docs, states = golden.json("corpus"), golden.npz("corpus")
+    checked = 0
+    for i, doc in enumerate(docs[:40]):
+        c = parse_qasm(doc["qasm"])
+        for d in doc["dist"]:
+            if not d["switches"]:
+                continue
+            for policy in ("reference", "lookahead"):
+                run = ShardedRun(c, partition_of(d["parts"]), d["p"], loopback=True, program=False, policy=policy)
+                R, l = 1 << d["p"], run.n_local
+                shards = [np.zeros(1 << l, dtype=np.complex128) for _ in range(R)]
+                shards[0][0] = 1.0
+                for si, (a, b) in enumerate(run.segments):
+                    if a in run.switch_at:
+                        pa, cc, dst, slot = group_switch_args(run, si)
+                        _emulate_group_switch(shards, l, pa, cc, dst, slot, chunk=3)
+                        # the host passes address the new layout in natural order:
+                        # offset bit j of it sits on physical bit arrival[j]
+                        old, new, _ = run.switch_at[a]
+                        arrival = run.arrival_layout(old, new)
+                        idx = np.arange(1 << l, dtype=np.int64)
+                        src = np.zeros_like(idx)
+                        for j, ph in enumerate(arrival):
+                            src |= ((idx >> j) & 1) << ph
+                        shards = [sh[src] for sh in shards]
+                    for j in range(run.bounds[a][0], run.bounds[b - 1][0] + run.bounds[b - 1][1]) if b > a else ():
+                        e = run.exes[j]
+                        for sh in shards:
+                            orc.run_part(sh, e.slot_map.qubits, e.ops, e.op_slots)
+                full = np.zeros(1 << c.num_qubits, dtype=np.complex128)
+                for r in range(R):
+                    full[shard_positions(run.layouts[-1], r)] = shards[r]
+                assert np.max(np.abs(full - states[f"c{i}"])) < 1e-12, (i, d["p"], policy)
+                checked += 1
+    assert checked >= 10
