@@ -296,7 +296,9 @@ def gpu_arm(args, circuit, part, rank, world):
     if dist:
         from paper_2205_06973_b200.multi import ShardedRun
 
-        run = ShardedRun(circuit, part, int(math.log2(world)), device=dev)
+        # layout switches pull over peer memory (CUDA IPC) when every rank can
+        # map its peers' staging, else batched NCCL send/recv
+        run = ShardedRun(circuit, part, int(math.log2(world)), device=dev, transport="auto")
         n_local = run.n_local
     else:
         # the timed runs start from |0..0>, prepared in the program's layout
@@ -441,11 +443,18 @@ def gpu_arm(args, circuit, part, rank, world):
 
     # e2e through the public API: host initial state in, host state out
     e2e = None
-    if dist and not args.no_e2e:
+    host_total = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    e2e_fits = world * 2 * ((1 << n_local) * 16) <= 0.4 * host_total and (1 << n_local) * 16 <= E2E_MAX_STATE_BYTES
+    if dist and not args.no_e2e and not e2e_fits:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "skipped": f"{world} ranks x 2 pinned host buffers of a {((1 << n_local) * 16) >> 30} GiB shard exceed "
+                          f"40% of the host's {host_total >> 30} GiB (or the {E2E_MAX_STATE_BYTES >> 30} GiB cap)"}
+    elif dist and not args.no_e2e:
         # every rank uploads its shard of the initial state (natural order of
         # the first layout) from pinned host memory, runs all parts and
         # switches, and downloads its final shard; max over ranks
         run_e2e = ShardedRun(circuit, part, int(math.log2(world)), device=dev, basis_start=False)
+        run_e2e.transport, run_e2e._peer = run.transport, run._peer  # one staging pair per rank
         run_e2e._scratch = getattr(run, "_scratch", None)  # one ping-pong scratch per rank, not two
         host_in = torch.zeros(1 << n_local, dtype=torch.complex128).pin_memory()
         if rank == 0:
@@ -539,7 +548,8 @@ def gpu_arm(args, circuit, part, rank, world):
     if dist:
         sw = [sum(c) / len(c) for c in zip(*switch_list)] if switch_list and switch_list[0] else []
         sw_ms = sum(sw)
-        comm = dict(run.comm_summary(), switch_ms_per_step=sw_ms, per_switch_ms=[round(x, 4) for x in sw],
+        comm = dict(run.comm_summary(), transport=run.transport, transport_note=run.transport_note,
+                    switch_ms_per_step=sw_ms, per_switch_ms=[round(x, 4) for x in sw],
                     parts_ms_per_step=seg_ms / n_marked,
                     nvlink_gbs_per_rank=(run.stats.total_bytes / world / (sw_ms / 1e3) / 1e9 if sw_ms > 0 else None),
                     nvlink_note="bytes each rank sends over all switches (closed-form CommStats / ranks) / switch time")

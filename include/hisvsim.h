@@ -319,7 +319,10 @@ int hs_group_switch(hs_group* group, void* const* shards, int n_local, int dtype
                     double* seconds);
 /* one process per GPU: export / map another process's device buffer
  * (cudaIpcMemHandle_t, 64 bytes) so hs_unpack_segments_range_from can pull
- * from a peer's staging */
+ * from a peer's staging. Buffers to export come from hs_device_alloc (a
+ * whole allocation: the mapped pointer is its base). */
+int hs_device_alloc(size_t bytes, void** device_ptr);
+int hs_device_free(void* device_ptr);
 int hs_ipc_get_handle(const void* device_ptr, void* handle_out);
 int hs_ipc_open_handle(const void* handle, void** device_ptr);
 int hs_ipc_close(void* device_ptr);

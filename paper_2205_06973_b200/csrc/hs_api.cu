@@ -792,6 +792,24 @@ int hs_group_switch(hs_group* g, void* const* shards, int n_local, int dtype, co
   return HS_OK;
 }
 
+int hs_device_alloc(size_t bytes, void** device_ptr) {
+  if (!device_ptr) return fail(HS_ERR_INVALID, "NULL argument");
+  *device_ptr = nullptr;
+  if (bytes == 0) return fail(HS_ERR_INVALID, "zero-byte allocation");
+  cudaError_t e = cudaMalloc(device_ptr, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(HS_ERR_CAPACITY, "cudaMalloc of " + std::to_string(bytes) + " bytes: out of device memory");
+  }
+  HS_CUDA(e, "cudaMalloc");
+  return HS_OK;
+}
+
+int hs_device_free(void* device_ptr) {
+  if (device_ptr) HS_CUDA(cudaFree(device_ptr), "cudaFree");
+  return HS_OK;
+}
+
 int hs_ipc_get_handle(const void* device_ptr, void* handle_out) {
   if (!device_ptr || !handle_out) return fail(HS_ERR_INVALID, "NULL argument");
   cudaIpcMemHandle_t h;

@@ -131,6 +131,86 @@ class DeviceOps:
 SWITCH_CHUNK_BYTES = 256 << 20
 
 
+#: staging per buffer of the peer-memory switch (two per rank; fewer chunks
+#: means fewer rank barriers)
+P2P_STAGING_BYTES = 4 << 30
+
+
+class PeerStaging:
+    """Two staging buffers per rank (``hs_device_alloc``: whole allocations,
+    so an IPC mapping's base is the buffer) exported with CUDA IPC and mapped
+    by every peer (``hs_ipc_open_handle``). Setup is collective: if any rank
+    fails to map any peer, every rank raises."""
+
+    def __init__(self, nbytes: int, group=None, device=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        self.bytes = int(nbytes)
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._lib = lib = _native.load()
+        self.local, self._opened = [], []
+        self._remote = {}
+        err = None
+        if device is not None:
+            torch.cuda.set_device(torch.device(device))
+        handles = []
+        try:
+            for _ in range(2):
+                ptr = ctypes.c_void_p()
+                _native.check(lib.hs_device_alloc(self.bytes, ctypes.byref(ptr)))
+                self.local.append(ptr.value)
+                h = ctypes.create_string_buffer(64)
+                _native.check(lib.hs_ipc_get_handle(ptr, h))
+                handles.append(h.raw)
+        except Exception as exc:
+            err = f"rank {self.rank}: {exc}"
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, (handles, err), group=group)
+        if err is None:
+            try:
+                for r, (hs, e) in enumerate(gathered):
+                    if r == self.rank or e is not None:
+                        continue
+                    for b, h in enumerate(hs):
+                        ptr = ctypes.c_void_p()
+                        buf = ctypes.create_string_buffer(h, 64)
+                        _native.check(lib.hs_ipc_open_handle(buf, ctypes.byref(ptr)))
+                        self._remote[(r, b)] = ptr.value
+                        self._opened.append(ptr.value)
+            except Exception as exc:
+                err = f"rank {self.rank}: {exc}"
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)
+        bad = [e for e in errs if e] + [e for _, e in gathered if e]
+        if bad:
+            self.close()
+            raise RuntimeError("; ".join(sorted(set(bad))))
+
+    def ptr(self, rank: int, b: int) -> int:
+        return self.local[b] if rank == self.rank else self._remote[(rank, b)]
+
+    def close(self) -> None:
+        lib = getattr(self, "_lib", None)
+        if lib is None:
+            return
+        for p in self._opened:
+            lib.hs_ipc_close(p)
+        for p in self.local:
+            lib.hs_device_free(p)
+        self._opened, self.local, self._remote = [], [], {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
 class ShardedRun:
     """Plan once (layouts, switch schedules, one device program per run of
     parts between switches, in rank-local coordinates), run many times.
@@ -143,7 +223,8 @@ class ShardedRun:
 
     def __init__(self, circuit, partition, num_rank_bits: int, group=None, device=None, ops=None,
                  dtype="complex128", program=True, chunk_bytes: int = SWITCH_CHUNK_BYTES, basis_start: bool = True,
-                 loopback: bool = False, policy: str = "lookahead"):
+                 loopback: bool = False, policy: str = "lookahead", transport: str = "nccl",
+                 staging_bytes: int | None = None):
         """``loopback``: all ranks live in this process on one device
         (``run_loopback``); no process group is used. ``policy``: layout
         schedule (``dist.plan_layouts``): "lookahead" (default: fewest remap
@@ -207,6 +288,25 @@ class ShardedRun:
         self.program = self.programs[0] if self.programs else None
         self.stats = CommStats(self.n, num_rank_bits, len(self.layouts),
                                [st for _, _, st in self.switch_at.values()])
+        # switch transport: "nccl" (batched send/recv), "p2p" (pull from the
+        # peers' staging over peer memory, CUDA IPC mappings), "auto" (p2p
+        # when every rank can map every peer's staging, else nccl)
+        if transport not in ("nccl", "p2p", "auto"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = "nccl"
+        self.transport_note = None
+        self._peer = None
+        if transport != "nccl" and not loopback and self.world > 1 and self.switch_at:
+            amp = 16 if str(dtype) in ("complex128", "c128", "torch.complex128") else 8
+            shard = amp << self.n_local
+            sb = int(staging_bytes) if staging_bytes else max(SWITCH_CHUNK_BYTES, min(P2P_STAGING_BYTES, shard))
+            try:
+                self._peer = PeerStaging(sb, self.group, device)
+                self.transport = "p2p"
+            except Exception as exc:  # decided collectively inside PeerStaging
+                if transport == "p2p":
+                    raise
+                self.transport_note = f"p2p unavailable, nccl used: {exc}"
 
     def _share_scratch(self, shard) -> None:
         """One ping-pong scratch buffer for all segment programs (each would
@@ -288,6 +388,8 @@ class ShardedRun:
         so chunk m + 1 is packed (and chunk m - 1 unpacked) while chunk m is
         on the wire. Returns the shard (same buffer) in
         ``arrival_layout(old, new)``."""
+        if self.transport == "p2p":
+            return self._switch_p2p(shard, old, new, phys)
         A, B, pa = self.switch_plan(old, new, phys)
         _, out_segs, incoming, _, c = switch_schedule(old, new, self.rank, A)
         l = self.n_local
@@ -313,6 +415,62 @@ class ShardedRun:
             pending = (works, recv, begin, cnt)
         if pending is not None:
             finish(pending)
+        return shard
+
+    def _switch_p2p(self, shard, old: RankLayout, new: RankLayout, phys=None):
+        """The in-place switch over peer memory (one process per GPU): chunk
+        by chunk of inner offsets, every rank packs its outgoing segments
+        into its own staging buffer (exported to the peers through CUDA IPC),
+        then - once every rank's pack is complete - pulls its incoming
+        segments straight from the senders' staging into the positions of
+        the segments it sent (``hs_unpack_segments_range_from``: one NVLink
+        read and one local write per remote amplitude). Two staging buffers
+        alternate; the ranks meet at one process-group barrier per chunk
+        (after a stream sync, so a chunk's pulls are done before its buffer
+        is packed again). Same data movement as ``switch``."""
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from .statevec import native_dtype
+
+        A, B, pa = self.switch_plan(old, new, phys)
+        _, out_segs, incoming, _, c = switch_schedule(old, new, self.rank, A)
+        # slot j of this shard <- segment k of source s
+        from_slot = {}
+        for src, j in incoming.items():
+            for k, dst in switch_out_peers(old, new, src, A):
+                if dst == self.rank:
+                    from_slot[j] = (src, k)
+        S = 1 << c
+        if sorted(from_slot) != list(range(S)):
+            raise RuntimeError("switch schedule does not fill every slot")
+        l = self.n_local
+        inner = 1 << (l - c)
+        amp = shard.element_size()
+        chunk = max(1, min(inner, self._peer.bytes // (amp << c)))
+        lib = _native.load()
+        code = native_dtype(shard)
+        sp = (ctypes.c_int32 * max(1, c))(*pa)
+        stream = torch.cuda.current_stream(shard.device)
+        for m, begin in enumerate(range(0, inner, chunk)):
+            b = m & 1
+            cnt = min(chunk, inner - begin)
+            _native.check(lib.hs_pack_segments_range(shard.data_ptr(), self._peer.local[b], l, code, sp, c, begin, cnt,
+                                                     stream.cuda_stream))
+            # this rank's pack of chunk m (and its pull of chunk m - 1) are done;
+            # after the barrier every rank's are
+            stream.synchronize()
+            dist.barrier(self.group)
+            srcs = (ctypes.c_void_p * S)()
+            for j in range(S):
+                src, k = from_slot[j]
+                srcs[j] = self._peer.ptr(src, b) + k * cnt * amp
+            _native.check(lib.hs_unpack_segments_range_from(srcs, shard.data_ptr(), l, code, sp, c, begin, cnt,
+                                                            stream.cuda_stream))
+        stream.synchronize()
+        dist.barrier(self.group)  # nobody packs into a staging buffer a peer still reads
         return shard
 
     def run(self, shard, events=None, run_part=None, with_timing: bool = False):
@@ -535,14 +693,16 @@ class ShardedState:
 
 
 def simulate_distributed_group(circuit, partition, num_rank_bits, *, group=None, initial=None, dtype="complex128",
-                               device=None, policy: str = "reference", with_timing: bool = False) -> DistributedRun:
+                               device=None, policy: str = "reference", with_timing: bool = False,
+                               transport: str = "auto") -> DistributedRun:
     """``simulate_distributed`` over a process group: every rank returns its
     own shard (``DistributedRun.state`` is a ``ShardedState``)."""
     import torch
 
     from .statevec import allocate, init_basis
 
-    run = ShardedRun(circuit, partition, num_rank_bits, group=group, device=device, dtype=dtype, policy=policy)
+    run = ShardedRun(circuit, partition, num_rank_bits, group=group, device=device, dtype=dtype, policy=policy,
+                     transport=transport)
     shard = allocate(run.n_local, dtype, device)
     if initial is None:
         if run.rank == 0:
