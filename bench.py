@@ -285,7 +285,10 @@ def gpu_arm(args, circuit, part, rank, world):
     from paper_2205_06973_b200.hier import HierarchicalRun
     from paper_2205_06973_b200.statevec import allocate, init_basis
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    # HISVSIM_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0, to run the
+    # N > 1 path on a one-GPU box with HISVSIM_BENCH_BACKEND=gloo
+    local = 0 if os.environ.get("HISVSIM_BENCH_ONE_DEVICE") == "1" else int(os.environ.get("LOCAL_RANK", 0))
+    dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     _native.engine(dev.index or 0)
     n = circuit.num_qubits
@@ -613,7 +616,7 @@ def main(argv=None):
             if rank != 0:
                 return 0
         else:
-            tdist.init_process_group("nccl")
+            tdist.init_process_group(os.environ.get("HISVSIM_BENCH_BACKEND", "nccl"))
     if args.impl == "reference":
         world = 1
     cfg, circuit, part, t_part = build_workload(args.workload, args.strategy, args.limit)
