@@ -632,7 +632,7 @@ class HierarchicalRun:
         self.program = PartProgram(circuit.num_qubits, self.exes, dtype=dtype, device=device, options=options,
                                    basis_start=basis_start)
 
-    def run_stream(self, inputs, outputs, buffers=None, stream=None, copy_streams: int = 2,
+    def run_stream(self, inputs, outputs, buffers=None, stream=None, copy_streams: int = 1,
                    copy_chunks: int = 4) -> None:
         """Simulate the circuit on a sequence of host states: ``inputs[i]``
         (pinned host tensors, natural order, e.g. many initial states) ->
@@ -641,9 +641,9 @@ class HierarchicalRun:
         upload, step i's passes and step i - 1's download all overlap (with
         two buffers an upload waits for the download before it). Each copy is
         split into ``copy_chunks`` pieces over ``copy_streams`` streams per
-        direction: with both directions busy, one copy per direction moves
-        ~34 GB/s each way over PCIe, two or more in flight ~48 GB/s (measured,
-        profiles/r02m_pcie.log). Returns when the last download is queued
+        direction (measured on c3, ms per step: 1 stream x 1 piece 440, 1 x 4
+        419, 2 x 2 481, 2 x 4 446, 4 x 4 494; the pipeline is PCIe / host
+        memory bound at ~41 GB/s each way). Returns when the last download is queued
         (synchronize to read outputs). The program must accept natural-order
         input (``basis_start=False``)."""
         import torch

@@ -791,3 +791,29 @@ def test_c_host_program_runs_a_sharded_circuit(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert json.loads(out.stdout.strip().splitlines()[-1])["max_abs_delta"] < 1e-12
+
+
+def test_bench_two_ranks_share_one_gpu(tmp_path):
+    """bench.py's N > 1 path end to end under torchrun with two ranks on this
+    one GPU (gloo for the process group; the test-only HISVSIM_BENCH_* switches):
+    weak-scaled workload, sharded run, layout switches over peer memory
+    (transport p2p), max-over-ranks timing, e2e and the JSON line."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, HISVSIM_BENCH_ONE_DEVICE="1", HISVSIM_BENCH_BACKEND="gloo",
+               HISVSIM_CACHE_DIR=str(tmp_path / "cubins"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", str(root / "bench.py"), "--gpus", "2",
+           "--config", "c2", "--steps", "3", "--warmup", "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["config"]["num_qubits"] == 27
+    assert line["comm"]["transport"] == "p2p" and line["comm"]["switches"] >= 1
+    assert line["comm"]["switch_ms_per_step"] > 0 and line["value"] > 0
+    assert line["e2e"]["value"] > 0
