@@ -630,7 +630,6 @@ def main(argv=None):
               "state_bytes_per_gpu": (1 << (n - p_bits)) * 16,
               "l2_policy": ("inputs larger than L2: the state exceeds the 126 MB L2" if (1 << (n - p_bits)) * 16 > (126 << 20)
                             else "L2-resident state (16 MiB c1): no flush between steps"),
-              "partition_seconds_host": round(t_part, 4),
               "parallelism": f"qubit-sharded x{gpus}" if gpus > 1 else "single GPU"}
 
     if args.impl == "reference":
@@ -645,6 +644,7 @@ def main(argv=None):
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 "part_pass_equivalent_gbs": r["value"],
                 "projected_time_to_solution_s": r["projected_time_to_solution_s"],
+                "host_seconds": {"partition": round(t_part, 4)},
                 "note": "host CPU, rank 0 only: the C restatement of the reference's per-part gather/gates/scatter "
                         "(oracle/sv_oracle.c; the reference is pure Python/numpy and compiles to nothing) on every "
                         "host thread over a bounded sample of each part's fixings; numpy_port_c1_seconds = the "

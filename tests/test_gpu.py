@@ -817,3 +817,24 @@ def test_bench_two_ranks_share_one_gpu(tmp_path):
     assert line["comm"]["transport"] == "p2p" and line["comm"]["switches"] >= 1
     assert line["comm"]["switch_ms_per_step"] > 0 and line["value"] > 0
     assert line["e2e"]["value"] > 0
+
+
+@pytest.mark.skipif(__import__("os").environ.get("HISVSIM_BIG_ORACLE") != "1",
+                    reason="opt-in: ~10 min and 128 GiB of host RAM (HISVSIM_BIG_ORACLE=1)")
+def test_full_size_c5_33_matches_c_oracle():
+    """c5's per-GPU share at full size (33 qubits, 128 GiB in place, k = 14:
+    wide parts as tile sub-passes + restore launches) against the C oracle on
+    the box's host (128 GiB, 16 threads), compared chunk by chunk at 1e-10."""
+    c = configs.build("c5_33")
+    part = partition_dfs(build_dag(c), 14)
+    st = execute_hierarchical(c, part)
+    torch.cuda.synchronize()
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    step = 1 << 26
+    worst = 0.0
+    for s in range(0, ref.size, step):
+        chunk = torch.from_numpy(ref[s:s + step]).cuda()
+        worst = max(worst, float((st.data[s:s + step] - chunk).abs().max()))
+        del chunk
+    print(f"c5_33 full-size max |delta| {worst:.3e}")
+    assert worst < 1e-10
