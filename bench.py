@@ -126,14 +126,19 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None, "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def build_workload(name: str, strategy: str, limit: int | None = None):
+def build_workload(name: str, strategy: str, limit: int | None = None, partition_file: str | None = None):
     """Circuit + partition of a bench workload (``configs.bench_workload``'s
-    circuit name) and the host partitioning time."""
+    circuit name) and the host partitioning time; ``partition_file``: a
+    partition JSON (the reference's document, e.g. from ``cli partition``)."""
     from paper_2205_06973_b200 import build_dag, configs, partition_dagp, partition_dfs, partition_nat
+    from paper_2205_06973_b200.partition import partition_from_json
 
     cfg = configs.CONFIGS[name.split("@")[0]]
     circuit = configs.build(name)
     t0 = time.perf_counter()
+    if partition_file:
+        part = partition_from_json(build_dag(circuit), Path(partition_file).read_text())
+        return cfg, circuit, part, time.perf_counter() - t0
     fn = {"nat": partition_nat, "dfs": partition_dfs, "dagp": partition_dagp}[strategy]
     part = fn(build_dag(circuit), limit or cfg.limit)
     t_part = time.perf_counter() - t0
@@ -236,7 +241,7 @@ def plan_probe(args) -> int:
     from paper_2205_06973_b200 import _native
     from paper_2205_06973_b200.hier import HierarchicalRun
 
-    _, circuit, part, _ = build_workload(args.workload, args.strategy, args.limit)
+    _, circuit, part, _ = build_workload(args.workload, args.strategy, args.limit, args.partition)
     torch.cuda.init()
     _native.engine(0)
     t0 = time.perf_counter()
@@ -580,6 +585,7 @@ def main(argv=None):
     ap.add_argument("--config", default="c3", help="BASELINE config (c1 .. c5; c3 is the largest single-GPU one)")
     ap.add_argument("--strategy", default="dfs", choices=["nat", "dfs", "dagp"])
     ap.add_argument("--limit", type=int, default=None, help="part size k (default: the config's)")
+    ap.add_argument("--partition", default=None, help="run this partition JSON instead of --strategy")
     ap.add_argument("--cpu-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -619,13 +625,14 @@ def main(argv=None):
             tdist.init_process_group(os.environ.get("HISVSIM_BENCH_BACKEND", "nccl"))
     if args.impl == "reference":
         world = 1
-    cfg, circuit, part, t_part = build_workload(args.workload, args.strategy, args.limit)
+    cfg, circuit, part, t_part = build_workload(args.workload, args.strategy, args.limit, args.partition)
     n = circuit.num_qubits
     gpus = args.gpus if args.impl == "reference" else world
     p_bits = int(math.log2(gpus))
     config = {"workload": f"{args.workload}: {cfg.description}" + (f", at {n} qubits" if args.workload != cfg.name
                                                                     else ""),
-              "config": args.config, "num_qubits": n, "limit": args.limit or cfg.limit, "strategy": args.strategy,
+              "config": args.config, "num_qubits": n, "limit": args.limit or cfg.limit,
+              "strategy": f"file:{Path(args.partition).name}" if args.partition else args.strategy,
               "parts": part.num_parts, "gates": circuit.num_ops, "seed": cfg.seed, "dtype": "complex128",
               "state_bytes_per_gpu": (1 << (n - p_bits)) * 16,
               "l2_policy": ("inputs larger than L2: the state exceeds the 126 MB L2" if (1 << (n - p_bits)) * 16 > (126 << 20)
