@@ -81,6 +81,8 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local);
 void jit_cache_stats(int* disk_hits, int* compiles);
 int jit_teams();
+// on-disk cache directory ($HISVSIM_CACHE_DIR, default ~/.cache/hisvsim; empty = off)
+std::string hs_cache_dir();
 
 // Program-level qubit layout: logical position q (what parts stage) lives at
 // physical bit phys[q] of the buffer. A part's write-back may permute the

@@ -1004,6 +1004,8 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
 
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local) { return jit_source(pl, dtype, n_local); }
 
+std::string hs_cache_dir() { return cache_dir(); }
+
 int jit_teams() {
   const char* e = std::getenv("HISVSIM_TEAMS");
   return (e && std::atoi(e) == 1) ? 1 : 2;

@@ -22,6 +22,9 @@
 
 #include "hs_common.h"
 
+#include <sys/stat.h>
+#include <unistd.h>
+
 namespace hs {
 
 // lowest storage positions each pass hands to the next pass's qubits from
@@ -909,8 +912,16 @@ namespace {
 // (c2: 9 parts + a permutation launch -> 8 passes). A pass belongs to the
 // caller's part that contributes most of its gates (ties: the earlier one).
 // plan_program plans every grouping in full and keeps the fewest launches.
+// GROUP_BEAM_* search the reversed stream breadth-first instead of greedily:
+// at every step each of the best partial groupings tries the frontier growth
+// from the empty set, from 1-3 qubits of its previous pass and several
+// randomised growths (deterministic xorshift), and the BEAM_WIDTH best by
+// (passes + penalty, gates left) survive; PEN charges 0.5 pass for a pass
+// sharing fewer than 3 qubits with its neighbour (short reads). Measured on c3
+// (one B200): 12 launches 88.4 ms vs 13 (greedy reverse) 90.6 on the same box.
 enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
-                GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6 };
+                GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6, GROUP_BEAM_REVERSE,
+                GROUP_BEAM_REVERSE_PEN };
 
 // Cost of a pass in units of one coalesced HBM pass: a full-width pass that
 // shares fewer than 3 qubits with the pass before it cannot find its qubits
@@ -1055,6 +1066,117 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
     }
     return HS_OK;
   };
+  // beam search over the reversed stream (GROUP_BEAM_*): passes go to `held`
+  auto beam = [&](const std::vector<Ref>& stream, uint64_t first_seed, double penalty) -> int {
+    constexpr int BEAM_WIDTH = 16, RANDOM_GROWTHS = 6;
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto rnd = [&]() {  // xorshift64*: deterministic plans
+      rng ^= rng >> 12; rng ^= rng << 25; rng ^= rng >> 27;
+      return double((rng * 2685821657736338717ull) >> 11) / 9007199254740992.0;
+    };
+    // growth with randomised choice among the best few additions
+    auto grow_r = [&](const std::vector<int>& rem, uint64_t in) -> uint64_t {
+      for (;;) {
+        const int base = runnable(stream, rem, in, nullptr);
+        uint64_t blocked = 0;
+        std::vector<std::pair<double, uint64_t>> adds;
+        std::vector<uint64_t> seen;
+        for (int g : rem) {
+          const uint64_t m = stream[g].mask;
+          if (m & blocked) continue;
+          blocked |= m;
+          const uint64_t add = m & ~in;
+          if (!add || __builtin_popcountll(in | add) > tile_max) continue;
+          if (std::find(seen.begin(), seen.end(), add) != seen.end()) continue;
+          seen.push_back(add);
+          adds.push_back({double(runnable(stream, rem, in | add, nullptr) - base) / __builtin_popcountll(add), add});
+        }
+        std::stable_sort(adds.begin(), adds.end(), [](const std::pair<double, uint64_t>& x,
+                                                      const std::pair<double, uint64_t>& y) { return x.first > y.first; });
+        if (adds.empty() || adds[0].first <= 0) return in;
+        const double r = rnd();
+        const size_t k = std::min(adds.size() - 1, size_t(r * r * r * std::min<size_t>(3, adds.size())));
+        in |= adds[adds[k].first > 0 ? k : 0].second;
+      }
+    };
+    struct State {
+      std::vector<std::pair<std::vector<int>, uint64_t>> passes;
+      std::vector<int> rem;
+      uint64_t prev = 0;
+      double pen = 0.0;
+    };
+    std::vector<State> states(1);
+    states[0].rem.resize(stream.size());
+    for (size_t g = 0; g < stream.size(); ++g) states[0].rem[g] = (int)g;
+    for (;;) {
+      for (const State& st : states)
+        if (st.rem.empty()) {
+          held = st.passes;
+          for (size_t j = 0; j < held.size(); ++j)
+            total += pass_cost(held[j].second, j ? held[j - 1].second : 0, tile_max);
+          return HS_OK;
+        }
+      std::vector<State> next;
+      for (const State& st : states) {
+        std::vector<uint64_t> cands;
+        auto add_cand = [&](uint64_t in) {
+          if (std::find(cands.begin(), cands.end(), in) == cands.end()) cands.push_back(in);
+        };
+        if (!st.prev) {
+          add_cand(grow(stream, st.rem, first_seed));
+        } else {
+          add_cand(grow(stream, st.rem, 0));
+          std::vector<int> pb;
+          for (int b = 0; b < 64; ++b)
+            if (st.prev >> b & 1) pb.push_back(b);
+          for (int k = 1; k <= 3 && k <= (int)pb.size(); ++k)
+            for (int t = 0; t < 2; ++t) {
+              std::vector<int> pick(pb);
+              for (int j = 0; j < k; ++j) std::swap(pick[j], pick[j + size_t(rnd() * (pick.size() - j))]);
+              uint64_t seed = 0;
+              for (int j = 0; j < k; ++j) seed |= 1ull << pick[j];
+              add_cand(grow(stream, st.rem, seed));
+            }
+        }
+        for (int t = 0; t < RANDOM_GROWTHS; ++t) add_cand(grow_r(st.rem, 0));
+        for (uint64_t in : cands) {
+          std::vector<int> took;
+          runnable(stream, st.rem, in, &took);
+          if (took.empty()) continue;
+          uint64_t used = 0;
+          for (int g : took) used |= stream[g].mask;
+          State ns;
+          ns.passes = st.passes;
+          ns.passes.push_back({took, used});
+          ns.prev = used;
+          ns.pen = st.pen + ((st.prev && __builtin_popcountll(used & st.prev) < 3) ? penalty : 0.0);
+          // the last pass (the search's first) writes natural order only when
+          // it covers the seed positions; else a permutation launch follows
+          if (!st.prev && (in & first_seed) != first_seed) ns.pen += 1.0;
+          ns.rem.reserve(st.rem.size() - took.size());
+          size_t c = 0;
+          for (int g : st.rem) {
+            if (c < took.size() && took[c] == g) ++c;
+            else ns.rem.push_back(g);
+          }
+          next.push_back(std::move(ns));
+        }
+      }
+      if (next.empty()) { err = "internal: beam grouping made no progress"; return HS_ERR_INVALID; }
+      std::stable_sort(next.begin(), next.end(), [](const State& x, const State& y) {
+        const double a = x.passes.size() + x.pen, b = y.passes.size() + y.pen;
+        return a != b ? a < b : x.rem.size() < y.rem.size();
+      });
+      states.clear();
+      for (State& ns : next) {
+        bool dup = false;
+        for (const State& kept : states) dup |= kept.rem == ns.rem;
+        if (dup) continue;
+        states.push_back(std::move(ns));
+        if ((int)states.size() >= BEAM_WIDTH) break;
+      }
+    }
+  };
   std::vector<Ref> all;
   for (int i = 0; i < num_parts; ++i) {
     const hs_part& p = parts[i];
@@ -1099,11 +1221,16 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
   if (mode >= GROUP_REVERSE_LOW3) {
     const int n = (int)all.size();
     std::vector<Ref> rev(all.rbegin(), all.rend());
-    const bool low3 = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_PLAIN_LOW3;
+    const bool beam_mode = mode == GROUP_BEAM_REVERSE || mode == GROUP_BEAM_REVERSE_PEN;
+    const bool low3 = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_PLAIN_LOW3 || beam_mode;
     const bool seeded = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6;
     // (the seed never names a position the state does not have)
     const uint64_t avail = n_local >= 64 ? ~0ull : ((1ull << n_local) - 1);
-    if (int s = group(rev, true, seeded, true, (low3 ? 0x7ull : 0x3Full) & avail)) return s;
+    if (beam_mode) {
+      if (int s = beam(rev, 0x7ull & avail, mode == GROUP_BEAM_REVERSE_PEN ? 0.5 : 0.0)) return s;
+    } else if (int s = group(rev, true, seeded, true, (low3 ? 0x7ull : 0x3Full) & avail)) {
+      return s;
+    }
     for (auto it = held.rbegin(); it != held.rend(); ++it) {  // back to program order
       std::vector<int> fwd;
       for (int g : it->first) fwd.push_back(n - 1 - g);
@@ -1117,16 +1244,101 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
   return HS_OK;
 }
 
-// the run (in storage bits) a last pass must write in natural order to make
-// the gate-free final permutation unnecessary: 3 bits = 128 B of complex128
-// (measured: c2 5.96 ms with a 1 KB-run rule and 9 launches vs 5.56 ms with
-// 128 B runs and 8; c3 96.6 vs 94.9 ms; 64 B runs lose: c2 6.51 vs 5.74 ms)
 // positions at the bottom of an out-of-place pass's next layout given to the
 // next pass's qubits ($HISVSIM_NEXT_LOW; 3 = the store run only)
 int next_low_positions() {
   const char* e = std::getenv("HISVSIM_NEXT_LOW");
   if (!e || !*e) return 3;
   return std::max(3, std::min(62, std::atoi(e)));
+}
+
+// the run (in storage bits) a last pass must write in natural order to make
+// the gate-free final permutation unnecessary: 3 bits = 128 B of complex128
+// (measured: c2 5.96 ms with a 1 KB-run rule and 9 launches vs 5.56 ms with
+// 128 B runs and 8; c3 96.6 vs 94.9 ms; 64 B runs lose: c2 6.51 vs 5.74 ms)
+// streams up to this many gates also try the beam-search groupings
+constexpr int BEAM_MAX_GATES = 2000;
+
+// ---- on-disk cache of the chosen tile-pass grouping. Planning every
+// grouping candidate (the beam searches above all) costs up to ~1 s of host
+// time for a 1000-gate stream; the grouping is a pure function of the
+// program's inputs, so a second process reuses it. Key: FNV-1a over the
+// inputs and GROUPING_VERSION; value: the passes (hs_part / hs_gate, POD) and
+// their owners. A cached grouping is always a valid one for these inputs.
+constexpr uint64_t GROUPING_VERSION = 2;
+
+uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
+                      const hs_gate* gates, int num_gates, const int32_t* given_init) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+  };
+  const int64_t head[6] = {(int64_t)GROUPING_VERSION, n_local, dtype, tile_max, (int64_t)options, num_parts};
+  mix(head, sizeof(head));
+  mix(parts, sizeof(hs_part) * (size_t)num_parts);
+  mix(&num_gates, sizeof(num_gates));
+  for (int g = 0; g < num_gates; ++g) {  // field by field: the struct has padding
+    const hs_gate& G = gates[g];
+    mix(&G.kind, sizeof(G.kind));
+    mix(&G.num_slots, sizeof(G.num_slots));
+    mix(G.slots, sizeof(G.slots));
+    mix(G.params, sizeof(G.params));
+  }
+  if (given_init) mix(given_init, sizeof(int32_t) * (size_t)n_local);
+  return h;
+}
+
+std::string grouping_path(uint64_t key) {
+  const std::string dir = hs_cache_dir();
+  if (dir.empty()) return std::string();
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), "/%016llx.grouping", (unsigned long long)key);
+  return dir + buf;
+}
+
+bool grouping_load(uint64_t key, std::vector<hs_part>& xp, std::vector<hs_gate>& xg, std::vector<int>& owner) {
+  const std::string path = grouping_path(key);
+  if (path.empty()) return false;
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  uint64_t head[4] = {0, 0, 0, 0};
+  bool ok = std::fread(head, sizeof(head), 1, f) == 1 && head[0] == key && head[1] < (1u << 20) && head[2] < (1u << 24);
+  if (ok) {
+    xp.resize(head[1]);
+    xg.resize(head[2]);
+    owner.resize(head[1]);
+    std::vector<int32_t> own(head[1]);
+    ok = std::fread(xp.data(), sizeof(hs_part), xp.size(), f) == xp.size() &&
+         std::fread(xg.data(), sizeof(hs_gate), xg.size(), f) == xg.size() &&
+         std::fread(own.data(), sizeof(int32_t), own.size(), f) == own.size();
+    for (size_t i = 0; ok && i < own.size(); ++i) owner[i] = own[i];
+  }
+  std::fclose(f);
+  return ok;
+}
+
+void grouping_store(uint64_t key, const std::vector<hs_part>& xp, const std::vector<hs_gate>& xg,
+                    const std::vector<int>& owner) {
+  const std::string path = grouping_path(key);
+  if (path.empty()) return;
+  const std::string dir = path.substr(0, path.rfind('/'));
+  for (size_t i = 1; i <= dir.size(); ++i)
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+  char suffix[48];
+  std::snprintf(suffix, sizeof(suffix), ".tmp.%d", (int)getpid());
+  const std::string tmp = path + suffix;
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  const uint64_t head[4] = {key, xp.size(), xg.size(), 0};
+  std::vector<int32_t> own(owner.begin(), owner.end());
+  bool ok = std::fwrite(head, sizeof(head), 1, f) == 1 &&
+            std::fwrite(xp.data(), sizeof(hs_part), xp.size(), f) == xp.size() &&
+            std::fwrite(xg.data(), sizeof(hs_gate), xg.size(), f) == xg.size() &&
+            std::fwrite(own.data(), sizeof(int32_t), own.size(), f) == own.size();
+  ok = (std::fclose(f) == 0) && ok;
+  if (ok) std::rename(tmp.c_str(), path.c_str());
+  else std::remove(tmp.c_str());
 }
 
 int final_hot(int n_local, int tile_max) {
@@ -1149,7 +1361,19 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     double cost = 0.0;
     int s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
     if (s != HS_OK) return s;
-    if (!(options & HS_PLAN_PART_LOCAL)) {
+    const uint64_t gkey = (options & HS_PLAN_PART_LOCAL)
+                              ? 0
+                              : grouping_key(n_local, dtype, tile_max, options, parts, num_parts, gates, num_gates,
+                                             given_init);
+    std::vector<hs_part> cp;
+    std::vector<hs_gate> cg;
+    std::vector<int> co;
+    const bool cached = gkey && grouping_load(gkey, cp, cg, co);
+    if (cached) {
+      xp.swap(cp);
+      xg.swap(cg);
+      owner.swap(co);
+    } else if (!(options & HS_PLAN_PART_LOCAL)) {
       // regroup the whole gate stream when that takes fewer launches; among
       // regroupings with as few, the lowest pass_cost. Every candidate is
       // planned in full (host only, ~20 ms each) and judged by its real
@@ -1171,8 +1395,15 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       size_t best_launches = 0;
       if ((s = planned(xp, xg, &best_launches)) != HS_OK) return s;
       bool regrouped = false;
-      for (Grouping mode : {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
-                            GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6}) {
+      int stream_gates = 0;
+      for (int i = 0; i < num_parts; ++i) stream_gates += parts[i].num_gates;
+      std::vector<Grouping> modes = {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
+                                     GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6};
+      if (stream_gates <= BEAM_MAX_GATES) {  // the beam's host time grows with the stream
+        modes.push_back(GROUP_BEAM_REVERSE);
+        modes.push_back(GROUP_BEAM_REVERSE_PEN);
+      }
+      for (Grouping mode : modes) {
         std::vector<hs_part> ap;
         std::vector<hs_gate> ag;
         std::vector<int> ao;
@@ -1200,6 +1431,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     s = plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
                      err, init_phys, given_init, final_phys);
     if (s != HS_OK) return s;
+    if (gkey && !cached) grouping_store(gkey, xp, xg, owner);
     for (auto& pl : plans)
       if (pl.info.user_part >= 0) pl.info.user_part = owner[pl.info.user_part];
     return HS_OK;

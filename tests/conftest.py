@@ -1,4 +1,5 @@
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -13,6 +14,12 @@ GOLDEN = ROOT / "tests" / "golden"
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run with -m gpu)")
+    # a fresh on-disk cache (compiled cubins, chosen pass groupings) per test
+    # session, so every run exercises the planner and NVRTC as built
+    if "HISVSIM_CACHE_DIR" not in os.environ:
+        import tempfile
+
+        os.environ["HISVSIM_CACHE_DIR"] = tempfile.mkdtemp(prefix="hisvsim_test_cache_")
 
 
 class Golden:

@@ -436,3 +436,31 @@ def test_c_host_program_builds_against_the_header(tmp_path):
     """tests/c/group_demo.c drives a sharded run (programs, hs_group_switch)
     through include/hisvsim.h alone: it compiles and links with gcc."""
     assert _build_group_demo(tmp_path).exists()
+
+
+def test_grouping_cache_reuses_the_chosen_passes(tmp_path, monkeypatch):
+    """The chosen tile-pass grouping is cached on disk: a second plan of the
+    same program finds it and emits identical launches; a damaged entry is
+    ignored (planned again)."""
+    import os
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parent.parent
+    code = ("import sys; sys.path[:0] = [%r, %r]\n"
+            "import program_emulator as emu, hashlib\n"
+            "from paper_2205_06973_b200 import _native, build_dag, configs, partition_dfs\n"
+            "from paper_2205_06973_b200.hier import remap_part\n"
+            "c = configs.build('c3@20'); ex = [remap_part(c, p) for p in partition_dfs(build_dag(c), 9).parts]\n"
+            "L = emu.plan_program(_native, 20, 0, 12, ex, 0x47d | 0x8 | 0x20)\n"
+            "print(len(L), hashlib.sha1(b''.join(l.tobytes() + p.tobytes() for l, p in L)).hexdigest())\n"
+            % (str(root), str(root / "tests")))
+    env = dict(os.environ, HISVSIM_CACHE_DIR=str(tmp_path))
+    first = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True).stdout
+    files = list(tmp_path.glob("*.grouping"))
+    assert len(files) == 1
+    second = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True).stdout
+    assert first == second
+    files[0].write_bytes(b"garbage")
+    third = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True).stdout
+    assert third == first
