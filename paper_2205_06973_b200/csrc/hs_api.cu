@@ -709,8 +709,8 @@ int hs_group_switch(hs_group* g, void* const* shards, int n_local, int dtype, co
                     const int32_t* seg_dst, const int32_t* src_slot, void* const* streams, double* seconds) {
   if (!g || !shards || !seg_dst || !src_slot || (nseg && !seg_pos)) return fail(HS_ERR_INVALID, "NULL argument");
   if (int s = check_dtype(dtype)) return s;
-  const int R = g->num_shards, S = 1 << nseg;
   if (nseg < 0 || nseg > 8 || n_local < nseg || n_local > 62) return fail(HS_ERR_INVALID, "segment bits outside range");
+  const int R = g->num_shards, S = 1 << nseg;
   for (int k = 0; k < nseg; ++k)
     if (seg_pos[k] < 0 || seg_pos[k] >= n_local || (k && seg_pos[k] <= seg_pos[k - 1]))
       return fail(HS_ERR_INVALID, "segment positions must be ascending positions of the shard");

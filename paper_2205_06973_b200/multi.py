@@ -449,7 +449,9 @@ class ShardedRun:
         l = self.n_local
         inner = 1 << (l - c)
         amp = shard.element_size()
-        chunk = max(1, min(inner, self._peer.bytes // (amp << c)))
+        if self._peer.bytes < (amp << c):
+            raise ValueError(f"staging of {self._peer.bytes} B holds no chunk of {1 << c} segments")
+        chunk = min(inner, self._peer.bytes // (amp << c))
         lib = _native.load()
         code = native_dtype(shard)
         sp = (ctypes.c_int32 * max(1, c))(*pa)
