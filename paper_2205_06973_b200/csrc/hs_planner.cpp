@@ -1286,6 +1286,7 @@ uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, co
     mix(G.params, sizeof(G.params));
   }
   if (given_init) mix(given_init, sizeof(int32_t) * (size_t)n_local);
+  if (const char* e = std::getenv("HISVSIM_PLAN_SELECT")) mix(e, std::strlen(e));  // selection experiments
   return h;
 }
 
