@@ -1286,7 +1286,8 @@ uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, co
     mix(G.params, sizeof(G.params));
   }
   if (given_init) mix(given_init, sizeof(int32_t) * (size_t)n_local);
-  if (const char* e = std::getenv("HISVSIM_PLAN_SELECT")) mix(e, std::strlen(e));  // selection experiments
+  for (const char* v : {"HISVSIM_PLAN_SELECT", "HISVSIM_BEAM"})  // grouping experiments
+    if (const char* e = std::getenv(v)) mix(e, std::strlen(e));
   return h;
 }
 
@@ -1400,7 +1401,8 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       for (int i = 0; i < num_parts; ++i) stream_gates += parts[i].num_gates;
       std::vector<Grouping> modes = {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                                      GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6};
-      if (stream_gates <= BEAM_MAX_GATES) {  // the beam's host time grows with the stream
+      const char* beam_env = std::getenv("HISVSIM_BEAM");  // "0": greedy groupings only (A/B)
+      if (stream_gates <= BEAM_MAX_GATES && !(beam_env && std::string(beam_env) == "0")) {
         modes.push_back(GROUP_BEAM_REVERSE);
         modes.push_back(GROUP_BEAM_REVERSE_PEN);
       }
