@@ -917,8 +917,11 @@ namespace {
 // from the empty set, from 1-3 qubits of its previous pass and several
 // randomised growths (deterministic xorshift), and the BEAM_WIDTH best by
 // (passes + penalty, gates left) survive; PEN charges 0.5 pass for a pass
-// sharing fewer than 3 qubits with its neighbour (short reads). Measured on c3
-// (one B200): 12 launches 88.4 ms vs 13 (greedy reverse) 90.6 on the same box.
+// sharing fewer than 3 qubits with its neighbour (short reads); a last pass
+// missing positions 0..2 costs a permutation launch. A beam grouping wins only
+// with fewer launches: c1 7 -> 6 (0.100 -> 0.080 ms), c5_33 17 -> 16 (1.240 ->
+// 1.213 s); c3 stays at the greedy 13 (the beam's 13 without short reads ran
+// 90.9 vs 90.3 ms on one box; a hand-run 12-launch beam grouping 88.4 vs 90.6).
 enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                 GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6, GROUP_BEAM_REVERSE,
                 GROUP_BEAM_REVERSE_PEN };
@@ -1265,7 +1268,7 @@ constexpr int BEAM_MAX_GATES = 2000;
 // program's inputs, so a second process reuses it. Key: FNV-1a over the
 // inputs and GROUPING_VERSION; value: the passes (hs_part / hs_gate, POD) and
 // their owners. A cached grouping is always a valid one for these inputs.
-constexpr uint64_t GROUPING_VERSION = 2;
+constexpr uint64_t GROUPING_VERSION = 3;
 
 uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                       const hs_gate* gates, int num_gates, const int32_t* given_init) {
@@ -1423,8 +1426,13 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
           const char* e = std::getenv("HISVSIM_PLAN_SELECT");
           return e && std::string(e) == "cost";
         }();
+        // a beam grouping replaces a greedy one only with fewer launches (c3,
+        // same box: beam's 13 short-read-free launches 90.9 ms vs the greedy
+        // 13 with three short reads 90.3; c1 7 -> 6, c5_33 17 -> 16 launches)
+        const bool beam_mode = mode == GROUP_BEAM_REVERSE || mode == GROUP_BEAM_REVERSE_PEN;
         const bool better = by_cost ? (c < cost || (c == cost && la < best_launches))
-                                    : (la < best_launches || (regrouped && la == best_launches && c < cost));
+                                    : (la < best_launches ||
+                                       (regrouped && !beam_mode && la == best_launches && c < cost));
         if (better) {
           xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c; best_launches = la;
           regrouped = true;
