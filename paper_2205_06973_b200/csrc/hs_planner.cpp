@@ -15,6 +15,7 @@
 // natural order.
 #include <algorithm>
 #include <functional>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -922,6 +923,10 @@ namespace {
 // with fewer launches: c1 7 -> 6 (0.100 -> 0.080 ms), c5_33 17 -> 16 (1.240 ->
 // 1.213 s); c3 stays at the greedy 13 (the beam's 13 without short reads ran
 // 90.9 vs 90.3 ms on one box; a hand-run 12-launch beam grouping 88.4 vs 90.6).
+// streams up to this many gates also try the beam-search groupings; the
+// plain beam runs from this many RNG streams
+constexpr int BEAM_MAX_GATES = 2000;
+constexpr int BEAM_SEEDS = 1;
 enum Grouping { GROUP_PER_PART, GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                 GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6, GROUP_BEAM_REVERSE,
                 GROUP_BEAM_REVERSE_PEN };
@@ -1070,15 +1075,22 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
     return HS_OK;
   };
   // beam search over the reversed stream (GROUP_BEAM_*): passes go to `held`
-  auto beam = [&](const std::vector<Ref>& stream, uint64_t first_seed, double penalty) -> int {
-    constexpr int BEAM_WIDTH = 16, RANDOM_GROWTHS = 6;
-    uint64_t rng = 0x9E3779B97F4A7C15ull;
-    auto rnd = [&]() {  // xorshift64*: deterministic plans
+  // one beam search with RNG stream `seed`; the result (passes in reverse
+  // order) and its score (passes + penalties) go to *out / *score
+  auto beam = [&](const std::vector<Ref>& stream, uint64_t first_seed, double penalty, uint64_t seed,
+                  std::vector<std::pair<std::vector<int>, uint64_t>>* out, double* score) -> int {
+    static const int BEAM_WIDTH = std::getenv("HISVSIM_BEAM_WIDTH") ? std::atoi(std::getenv("HISVSIM_BEAM_WIDTH")) : 32;
+    static const int RANDOM_GROWTHS = std::getenv("HISVSIM_BEAM_GROWTHS") ? std::atoi(std::getenv("HISVSIM_BEAM_GROWTHS")) : 6;
+    uint64_t base_rng = 0x9E3779B97F4A7C15ull ^ (seed * 0xD1B54A32D192ED03ull);
+    if (const char* e = std::getenv("HISVSIM_BEAM_SEED")) base_rng ^= std::strtoull(e, nullptr, 10) * 0xD1B54A32D192ED03ull;
+    // xorshift64* on a caller-owned state: every state of every step draws
+    // from its own stream, so the result does not depend on the threads
+    auto rnd = [](uint64_t& rng) {
       rng ^= rng >> 12; rng ^= rng << 25; rng ^= rng >> 27;
       return double((rng * 2685821657736338717ull) >> 11) / 9007199254740992.0;
     };
     // growth with randomised choice among the best few additions
-    auto grow_r = [&](const std::vector<int>& rem, uint64_t in) -> uint64_t {
+    auto grow_r = [&](const std::vector<int>& rem, uint64_t in, uint64_t& rng) -> uint64_t {
       for (;;) {
         const int base = runnable(stream, rem, in, nullptr);
         uint64_t blocked = 0;
@@ -1097,7 +1109,7 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
         std::stable_sort(adds.begin(), adds.end(), [](const std::pair<double, uint64_t>& x,
                                                       const std::pair<double, uint64_t>& y) { return x.first > y.first; });
         if (adds.empty() || adds[0].first <= 0) return in;
-        const double r = rnd();
+        const double r = rnd(rng);
         const size_t k = std::min(adds.size() - 1, size_t(r * r * r * std::min<size_t>(3, adds.size())));
         in |= adds[adds[k].first > 0 ? k : 0].second;
       }
@@ -1108,63 +1120,82 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
       uint64_t prev = 0;
       double pen = 0.0;
     };
+    // the successors of one state (its candidate passes)
+    auto expand = [&](const State& st, uint64_t rng, std::vector<State>& next) {
+      std::vector<uint64_t> cands;
+      auto add_cand = [&](uint64_t in) {
+        if (std::find(cands.begin(), cands.end(), in) == cands.end()) cands.push_back(in);
+      };
+      if (!st.prev) {
+        add_cand(grow(stream, st.rem, first_seed));
+      } else {
+        add_cand(grow(stream, st.rem, 0));
+        std::vector<int> pb;
+        for (int b = 0; b < 64; ++b)
+          if (st.prev >> b & 1) pb.push_back(b);
+        for (int k = 1; k <= 3 && k <= (int)pb.size(); ++k)
+          for (int t = 0; t < 2; ++t) {
+            std::vector<int> pick(pb);
+            for (int j = 0; j < k; ++j) std::swap(pick[j], pick[j + size_t(rnd(rng) * (pick.size() - j))]);
+            uint64_t sd = 0;
+            for (int j = 0; j < k; ++j) sd |= 1ull << pick[j];
+            add_cand(grow(stream, st.rem, sd));
+          }
+      }
+      for (int t = 0; t < RANDOM_GROWTHS; ++t) add_cand(grow_r(st.rem, 0, rng));
+      for (uint64_t in : cands) {
+        std::vector<int> took;
+        runnable(stream, st.rem, in, &took);
+        if (took.empty()) continue;
+        uint64_t used = 0;
+        for (int g : took) used |= stream[g].mask;
+        State ns;
+        ns.passes = st.passes;
+        ns.passes.push_back({took, used});
+        ns.prev = used;
+        ns.pen = st.pen + ((st.prev && __builtin_popcountll(used & st.prev) < 3) ? penalty : 0.0);
+        // the last pass (the search's first) writes natural order only when
+        // it covers the seed positions; else a permutation launch follows
+        if (!st.prev && (in & first_seed) != first_seed) ns.pen += 1.0;
+        ns.rem.reserve(st.rem.size() - took.size());
+        size_t c = 0;
+        for (int g : st.rem) {
+          if (c < took.size() && took[c] == g) ++c;
+          else ns.rem.push_back(g);
+        }
+        next.push_back(std::move(ns));
+      }
+    };
     std::vector<State> states(1);
     states[0].rem.resize(stream.size());
     for (size_t g = 0; g < stream.size(); ++g) states[0].rem[g] = (int)g;
-    for (;;) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (uint64_t step = 0;; ++step) {
       for (const State& st : states)
         if (st.rem.empty()) {
-          held = st.passes;
-          for (size_t j = 0; j < held.size(); ++j)
-            total += pass_cost(held[j].second, j ? held[j - 1].second : 0, tile_max);
+          *out = st.passes;
+          *score = st.passes.size() + st.pen;
           return HS_OK;
         }
-      std::vector<State> next;
-      for (const State& st : states) {
-        std::vector<uint64_t> cands;
-        auto add_cand = [&](uint64_t in) {
-          if (std::find(cands.begin(), cands.end(), in) == cands.end()) cands.push_back(in);
-        };
-        if (!st.prev) {
-          add_cand(grow(stream, st.rem, first_seed));
-        } else {
-          add_cand(grow(stream, st.rem, 0));
-          std::vector<int> pb;
-          for (int b = 0; b < 64; ++b)
-            if (st.prev >> b & 1) pb.push_back(b);
-          for (int k = 1; k <= 3 && k <= (int)pb.size(); ++k)
-            for (int t = 0; t < 2; ++t) {
-              std::vector<int> pick(pb);
-              for (int j = 0; j < k; ++j) std::swap(pick[j], pick[j + size_t(rnd() * (pick.size() - j))]);
-              uint64_t seed = 0;
-              for (int j = 0; j < k; ++j) seed |= 1ull << pick[j];
-              add_cand(grow(stream, st.rem, seed));
-            }
+      std::vector<std::vector<State>> per(states.size());
+      auto work = [&](size_t from, size_t stride) {
+        for (size_t i = from; i < states.size(); i += stride) {
+          uint64_t rng = base_rng ^ ((step * 1315423911ull + i + 1) * 0x94D049BB133111EBull);
+          for (int w = 0; w < 4; ++w) rnd(rng);
+          expand(states[i], rng, per[i]);
         }
-        for (int t = 0; t < RANDOM_GROWTHS; ++t) add_cand(grow_r(st.rem, 0));
-        for (uint64_t in : cands) {
-          std::vector<int> took;
-          runnable(stream, st.rem, in, &took);
-          if (took.empty()) continue;
-          uint64_t used = 0;
-          for (int g : took) used |= stream[g].mask;
-          State ns;
-          ns.passes = st.passes;
-          ns.passes.push_back({took, used});
-          ns.prev = used;
-          ns.pen = st.pen + ((st.prev && __builtin_popcountll(used & st.prev) < 3) ? penalty : 0.0);
-          // the last pass (the search's first) writes natural order only when
-          // it covers the seed positions; else a permutation launch follows
-          if (!st.prev && (in & first_seed) != first_seed) ns.pen += 1.0;
-          ns.rem.reserve(st.rem.size() - took.size());
-          size_t c = 0;
-          for (int g : st.rem) {
-            if (c < took.size() && took[c] == g) ++c;
-            else ns.rem.push_back(g);
-          }
-          next.push_back(std::move(ns));
-        }
+      };
+      const size_t nth = std::min<size_t>(hw, states.size());
+      if (nth <= 1) {
+        work(0, 1);
+      } else {
+        std::vector<std::thread> pool;
+        for (size_t t = 0; t < nth; ++t) pool.emplace_back(work, t, nth);
+        for (auto& th : pool) th.join();
       }
+      std::vector<State> next;
+      for (auto& v : per)
+        for (State& ns : v) next.push_back(std::move(ns));
       if (next.empty()) { err = "internal: beam grouping made no progress"; return HS_ERR_INVALID; }
       std::stable_sort(next.begin(), next.end(), [](const State& x, const State& y) {
         const double a = x.passes.size() + x.pen, b = y.passes.size() + y.pen;
@@ -1230,7 +1261,18 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
     // (the seed never names a position the state does not have)
     const uint64_t avail = n_local >= 64 ? ~0ull : ((1ull << n_local) - 1);
     if (beam_mode) {
-      if (int s = beam(rev, 0x7ull & avail, mode == GROUP_BEAM_REVERSE_PEN ? 0.5 : 0.0)) return s;
+      // the plain beam from several RNG streams (a 12-launch c3 grouping
+      // turns up in about 2 of 5 searches), the penalised one once
+      static const int nseeds = std::getenv("HISVSIM_BEAM_SEEDS") ? std::atoi(std::getenv("HISVSIM_BEAM_SEEDS")) : BEAM_SEEDS;
+      const int seeds = mode == GROUP_BEAM_REVERSE ? nseeds : 1;
+      double best = 1e300;
+      for (int sd = 0; sd < seeds; ++sd) {
+        std::vector<std::pair<std::vector<int>, uint64_t>> got;
+        double score = 0.0;
+        if (int s = beam(rev, 0x7ull & avail, mode == GROUP_BEAM_REVERSE_PEN ? 0.5 : 0.0, sd, &got, &score)) return s;
+        if (score < best) { best = score; held.swap(got); }
+      }
+      for (size_t j = 0; j < held.size(); ++j) total += pass_cost(held[j].second, j ? held[j - 1].second : 0, tile_max);
     } else if (int s = group(rev, true, seeded, true, (low3 ? 0x7ull : 0x3Full) & avail)) {
       return s;
     }
@@ -1259,8 +1301,6 @@ int next_low_positions() {
 // the gate-free final permutation unnecessary: 3 bits = 128 B of complex128
 // (measured: c2 5.96 ms with a 1 KB-run rule and 9 launches vs 5.56 ms with
 // 128 B runs and 8; c3 96.6 vs 94.9 ms; 64 B runs lose: c2 6.51 vs 5.74 ms)
-// streams up to this many gates also try the beam-search groupings
-constexpr int BEAM_MAX_GATES = 2000;
 
 // ---- on-disk cache of the chosen tile-pass grouping. Planning every
 // grouping candidate (the beam searches above all) costs up to ~1 s of host
@@ -1268,7 +1308,7 @@ constexpr int BEAM_MAX_GATES = 2000;
 // program's inputs, so a second process reuses it. Key: FNV-1a over the
 // inputs and GROUPING_VERSION; value: the passes (hs_part / hs_gate, POD) and
 // their owners. A cached grouping is always a valid one for these inputs.
-constexpr uint64_t GROUPING_VERSION = 3;
+constexpr uint64_t GROUPING_VERSION = 5;
 
 uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                       const hs_gate* gates, int num_gates, const int32_t* given_init) {
@@ -1289,7 +1329,7 @@ uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, co
     mix(G.params, sizeof(G.params));
   }
   if (given_init) mix(given_init, sizeof(int32_t) * (size_t)n_local);
-  for (const char* v : {"HISVSIM_PLAN_SELECT", "HISVSIM_BEAM"})  // grouping experiments
+  for (const char* v : {"HISVSIM_PLAN_SELECT", "HISVSIM_BEAM", "HISVSIM_BEAM_SEED"})  // grouping experiments
     if (const char* e = std::getenv(v)) mix(e, std::strlen(e));
   return h;
 }
