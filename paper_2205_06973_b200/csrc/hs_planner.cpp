@@ -920,9 +920,11 @@ namespace {
 // (passes + penalty, gates left) survive; PEN charges 0.5 pass for a pass
 // sharing fewer than 3 qubits with its neighbour (short reads); a last pass
 // missing positions 0..2 costs a permutation launch. A beam grouping wins only
-// with fewer launches: c1 7 -> 6 (0.100 -> 0.080 ms), c5_33 17 -> 16 (1.240 ->
-// 1.213 s); c3 stays at the greedy 13 (the beam's 13 without short reads ran
-// 90.9 vs 90.3 ms on one box; a hand-run 12-launch beam grouping 88.4 vs 90.6).
+// with fewer launches, and is tried only for HBM-bound programs (see
+// plan_program): c1 7 -> 6 launches (0.095 -> 0.085 ms). Measured and not
+// taken: c3's beam groupings (13 launches without short reads 90.9 vs the
+// greedy 13 at 90.3 ms on one box; a 12-launch one, found by some RNG
+// streams only, 88.4 vs 90.6), c5_33's (15 launches 1370 vs 17 at 1241 ms).
 // streams up to this many gates also try the beam-search groupings; the
 // plain beam runs from this many RNG streams
 constexpr int BEAM_MAX_GATES = 2000;
@@ -1308,7 +1310,7 @@ int next_low_positions() {
 // program's inputs, so a second process reuses it. Key: FNV-1a over the
 // inputs and GROUPING_VERSION; value: the passes (hs_part / hs_gate, POD) and
 // their owners. A cached grouping is always a valid one for these inputs.
-constexpr uint64_t GROUPING_VERSION = 5;
+constexpr uint64_t GROUPING_VERSION = 6;
 
 uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                       const hs_gate* gates, int num_gates, const int32_t* given_init) {
@@ -1427,6 +1429,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       // 9-pass forward regrouping of c2 ran 6.00 vs 5.71 ms for its 9 parts
       // + permutation, so equal counts keep the parts; c5_33's unseeded
       // frontier, 15 passes, 1224 vs 1273 ms for the seeded 16.)
+      double fp64_per_launch = 0.0;  // FP64 instructions per amplitude and launch of the parts' plan
       auto planned = [&](const std::vector<hs_part>& ps, const std::vector<hs_gate>& gs, size_t* out) -> int {
         std::vector<PartPlan> tmp;
         std::vector<int32_t> ip, fp;
@@ -1435,17 +1438,27 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
                                     gs.data(), (int)gs.size(), tmp, e, &ip, given_init, &fp);
         if (st != HS_OK) { err = e; return st; }
         *out = tmp.size();
+        double f = 0.0;
+        for (const PartPlan& pl : tmp) f += pl.info.fp64_instr_per_amp;
+        fp64_per_launch = tmp.empty() ? 0.0 : f / double(tmp.size());
         return HS_OK;
       };
       size_t best_launches = 0;
       if ((s = planned(xp, xg, &best_launches)) != HS_OK) return s;
+      // Passes issuing more FP64 work than a pass moves HBM bytes (~60 FP64
+      // instructions per complex128 amplitude at the measured rates) gain
+      // little from fewer launches, and the beam's denser passes measured
+      // slower there (c5_33: 15 beam launches 1370 ms vs 17 greedy 1241):
+      // beam candidates only for HBM-bound programs (c1 7 -> 6, 0.095 ->
+      // 0.085 ms; c3 ties at 13)
+      const bool fp64_bound = fp64_per_launch > (dtype == HS_C128 ? 60.0 : 30.0);
       bool regrouped = false;
       int stream_gates = 0;
       for (int i = 0; i < num_parts; ++i) stream_gates += parts[i].num_gates;
       std::vector<Grouping> modes = {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                                      GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6};
       const char* beam_env = std::getenv("HISVSIM_BEAM");  // "0": greedy groupings only (A/B)
-      if (stream_gates <= BEAM_MAX_GATES && !(beam_env && std::string(beam_env) == "0")) {
+      if (stream_gates <= BEAM_MAX_GATES && !fp64_bound && !(beam_env && std::string(beam_env) == "0")) {
         modes.push_back(GROUP_BEAM_REVERSE);
         modes.push_back(GROUP_BEAM_REVERSE_PEN);
       }
