@@ -739,7 +739,16 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         for (int k = 0; ok && k < RB; ++k) ok &= last->rpos[k] != want[r];
         if (ok) residues |= 1u << (want[r] % hot);
       }
-      ok &= residues == (1u << hot) - 1;
+      // all residues distinct: conflict-free loads in the last phase. With
+      // HISVSIM_DIRECT_2WAY=1 two distinct residues (2-way conflicts in the
+      // last phase's loads, +1 tile of wavefronts) still go direct, saving the
+      // store's shared-memory round trip (2 tiles of wavefronts)
+      static const int two_way = [] {  // 0: distinct residues only; 1: two distinct; 2: any
+        const char* e = std::getenv("HISVSIM_DIRECT_2WAY");
+        return e ? std::atoi(e) : 0;
+      }();
+      ok &= residues == (1u << hot) - 1 || (two_way >= 1 && hot == 3 && __builtin_popcount(residues) == 2) ||
+            (two_way >= 2 && hot == 3);
       if (ok) {
         std::vector<int> order(want.begin(), want.end());
         for (int m = 0; m < T - RB; ++m)
