@@ -804,11 +804,17 @@ def test_bench_two_ranks_share_one_gpu(tmp_path):
     import sys
     from pathlib import Path
 
+    import socket
+
     root = Path(__file__).resolve().parent.parent
     env = dict(os.environ, HISVSIM_BENCH_ONE_DEVICE="1", HISVSIM_BENCH_BACKEND="gloo",
                HISVSIM_CACHE_DIR=str(tmp_path / "cubins"))
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29531", str(root / "bench.py"), "--gpus", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"), "--gpus", "2",
            "--config", "c2", "--steps", "3", "--warmup", "3"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
