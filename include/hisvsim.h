@@ -190,6 +190,20 @@ int hs_program_final_layout(hs_program* prog, int32_t* phys);
 int hs_program_bind_scratch(hs_program* prog, void* scratch, size_t bytes);
 /* empty unless HS_PLAN_JIT compilation failed (the interpreter then runs) */
 const char* hs_program_jit_error(hs_program* prog);
+/* Fuse a layout switch into launch `launch` of a compiled ping-pong program
+ * (one process per GPU, peer memory): instead of writing its tile to this
+ * rank's state, the launch writes it to the state buffer of the rank that
+ * owns it after the switch - out_ptrs[k] (a device pointer, e.g. an IPC
+ * mapping of that rank's state) for the tiles whose bits at the outgoing
+ * qubits' positions seg_pos[] (ascending, outside the launch's tile) spell k -
+ * at the same offset with those bits replaced by my_slot. This is the
+ * in-place switch of hs_group_switch without the pack and pull passes: the
+ * transfer rides on the pass's stores. The launch must be out of place and
+ * write the state (out_buf 0); every rank's previous launch must be complete
+ * before any rank runs it (it overwrites peers' state buffers). num_seg_bits
+ * = 0 with out_ptrs NULL restores the plain launch. Recompiles the launch. */
+int hs_program_fuse_switch(hs_program* prog, int launch, int num_seg_bits, const int32_t* seg_pos,
+                           const uint64_t* out_ptrs, int32_t my_slot);
 /* process-wide counts of compiled-part kernels loaded from the on-disk cubin
  * cache ($HISVSIM_CACHE_DIR, default ~/.cache/hisvsim; "off" disables) and
  * compiled with NVRTC (in-process cache hits count as neither) */

@@ -32,7 +32,7 @@ EXPORTS = (
     "hs_program_num_parts", "hs_program_num_launches", "hs_program_part_info", "hs_program_initial_layout",
     "hs_program_final_layout",
     "hs_program_bind_scratch",
-    "hs_program_jit_error", "hs_jit_cache_stats",
+    "hs_program_jit_error", "hs_jit_cache_stats", "hs_program_fuse_switch",
     "hs_program_dump",
     "hs_program_run", "hs_program_run_graph", "hs_plan_part", "hs_plan_program", "hs_plan_program_layouts", "hs_jit_source", "hs_structure_2x2", "hs_dagp_merge", "hs_part_apply",
     "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
@@ -104,6 +104,8 @@ def _declare(lib) -> None:
         "hs_program_num_launches": (I, [P]),
         "hs_program_jit_error": (ctypes.c_char_p, [P]),
         "hs_jit_cache_stats": (I, [ctypes.POINTER(I), ctypes.POINTER(I)]),
+        "hs_program_fuse_switch": (I, [P, I, I, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_uint64),
+                                       ctypes.c_int32]),
         "hs_program_initial_layout": (I, [P, ctypes.POINTER(ctypes.c_int32)]),
         "hs_program_final_layout": (I, [P, ctypes.POINTER(ctypes.c_int32)]),
         "hs_program_bind_scratch": (I, [P, P, ctypes.c_size_t]),

@@ -334,6 +334,50 @@ int hs_program_initial_layout(hs_program* prog, int32_t* phys) {
 
 const char* hs_program_jit_error(hs_program* prog) { return prog ? prog->jit_error.c_str() : ""; }
 
+int hs_program_fuse_switch(hs_program* prog, int launch, int num_seg_bits, const int32_t* seg_pos,
+                           const uint64_t* out_ptrs, int32_t my_slot) {
+  if (!prog) return fail(HS_ERR_INVALID, "program is NULL");
+  if (launch < 0 || launch >= (int)prog->plans.size()) return fail(HS_ERR_INVALID, "launch index out of range");
+  PartPlan& pl = prog->plans[launch];
+  if (num_seg_bits == 0 && !out_ptrs) {  // clear
+    if (!pl.fuse.on) return HS_OK;
+    pl.fuse = FuseSwitch();
+  } else {
+    if (!pl.jit) return fail(HS_ERR_UNSUPPORTED, "a fused switch needs a compiled launch (HS_PLAN_JIT)");
+    if (!pl.launch.oop || pl.launch.out_buf != 0 || pl.launch.cluster_log)
+      return fail(HS_ERR_UNSUPPORTED, "a fused switch needs an out-of-place launch that writes the state");
+    if (num_seg_bits < 1 || num_seg_bits > 3 || !seg_pos || !out_ptrs)
+      return fail(HS_ERR_INVALID, "a fused switch moves 1..3 qubits");
+    FuseSwitch f;
+    f.on = 1;
+    f.c = num_seg_bits;
+    for (int b = 0; b < num_seg_bits; ++b) {
+      f.pa[b] = seg_pos[b];
+      if (seg_pos[b] < 0 || seg_pos[b] >= prog->n_local || (b && seg_pos[b] <= seg_pos[b - 1]))
+        return fail(HS_ERR_INVALID, "segment positions must be ascending positions of the shard");
+      for (int r = 0; r < pl.launch.T; ++r)
+        if (pl.launch.opos[r] == seg_pos[b])
+          return fail(HS_ERR_UNSUPPORTED, "a segment position is a tile bit of the launch");
+    }
+    for (int k = 0; k < (1 << num_seg_bits); ++k) {
+      if (!out_ptrs[k]) return fail(HS_ERR_INVALID, "NULL destination");
+      f.out_ptr[k] = out_ptrs[k];
+    }
+    if (my_slot < 0 || my_slot >= (1 << num_seg_bits)) return fail(HS_ERR_INVALID, "slot outside the segments");
+    f.slot = my_slot;
+    pl.fuse = f;
+  }
+  std::string err;
+  HS_CUDA(cudaSetDevice(prog->eng->device), "cudaSetDevice");
+  if (int s = jit_recompile(pl, prog->dtype, prog->n_local, prog->eng->device, prog->eng->smem_optin, err))
+    return fail(s, err);
+  if (prog->graph) {  // the captured graph holds the old kernel
+    cudaGraphExecDestroy(prog->graph);
+    prog->graph = nullptr;
+  }
+  return HS_OK;
+}
+
 int hs_jit_cache_stats(int* disk_hits, int* compiles) {
   jit_cache_stats(disk_hits, compiles);
   return HS_OK;

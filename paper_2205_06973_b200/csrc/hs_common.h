@@ -67,11 +67,28 @@ struct PartLaunch {
 };
 static_assert(sizeof(PartLaunch) == 144, "PartLaunch layout");
 
+// A layout switch fused into an out-of-place launch (one process per GPU,
+// peer memory): the launch writes each tile straight into the state buffer of
+// the rank that owns it after the switch. The switch's outgoing qubits sit on
+// output positions pa[] outside the tile, so a whole tile has one owner:
+// segment k = the tile's bits at pa -> rank dst[k], written at the same offset
+// with the pa bits replaced by this rank's slot (its incoming qubits' values).
+struct FuseSwitch {
+  int on = 0;
+  int c = 0;                 // outgoing qubits (segment bits)
+  int pa[3] = {0, 0, 0};     // their output positions, ascending
+  uint64_t out_ptr[8] = {};  // per segment k: the owner's state buffer (mapped)
+  int slot = 0;              // this rank's slot bits
+};
+
 struct PartPlan {
   PartLaunch launch;
   std::vector<Instr> prog;
   hs_part_info info;
   void* jit = nullptr;  // cudaKernel_t of the compiled part (HS_PLAN_JIT), else null
+  double carry_in[2] = {1.0, 0.0};  // the program's pending scalar when this launch starts (jit)
+  bool last = false;                // the program's last launch (applies the scalar)
+  FuseSwitch fuse;
 };
 
 // Compile every plan to a straight-line kernel (hs_jit.cpp); on failure all
@@ -79,6 +96,8 @@ struct PartPlan {
 int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, int device, int smem_optin,
                         std::string& err);
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local);
+// recompile one launch of a compiled program (e.g. after setting pl.fuse)
+int jit_recompile(PartPlan& pl, int dtype, int n_local, int device, int smem_optin, std::string& err);
 void jit_cache_stats(int* disk_hits, int* compiles);
 int jit_teams();
 // on-disk cache directory ($HISVSIM_CACHE_DIR, default ~/.cache/hisvsim; empty = off)

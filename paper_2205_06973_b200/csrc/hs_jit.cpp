@@ -797,7 +797,29 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   // registers, so its refill (tile i + 3) overlaps the last phase's gates
   emit_program(g, pl, cl > 0 ? "TEAM_CSYNC();" : "TEAM_SYNC();", fp64_per_amp, "TEAM_SYNC();",
                direct ? "TEAM_SYNC(); issue(i + 3);" : nullptr);
-  if (oop) o << "    const unsigned long long obase = out_base(tt);\n";
+  const FuseSwitch& fz = pl.fuse;
+  if (oop && !fz.on) o << "    const unsigned long long obase = out_base(tt);\n";
+  if (oop && fz.on) {
+    // fused layout switch: the tile's owner after the switch is picked by its
+    // bits at the outgoing qubits' positions (free positions: one owner per
+    // tile); it is written there, those bits replaced by this rank's slot
+    uint64_t pam = 0, slotbits = 0;
+    for (int b = 0; b < fz.c; ++b) {
+      pam |= 1ull << fz.pa[b];
+      if (fz.slot >> b & 1) slotbits |= 1ull << fz.pa[b];
+    }
+    o << "    const unsigned long long obase_raw = out_base(tt);\n";
+    o << "    unsigned seg_k = 0u;\n";
+    for (int b = 0; b < fz.c; ++b)
+      o << "    seg_k |= (unsigned)((obase_raw >> " << fz.pa[b] << ") & 1ull) << " << b << ";\n";
+    o << "    const unsigned long long obase = (obase_raw & ~" << pam << "ull) | " << slotbits << "ull;\n";
+    o << "    C* const out_dst = reinterpret_cast<C*>(";
+    for (int k = 0; k < (1 << fz.c); ++k)
+      o << (k + 1 < (1 << fz.c) ? "seg_k == " + std::to_string(k) + "u ? " : "") << "0x" << std::hex << fz.out_ptr[k]
+        << std::dec << "ull" << (k + 1 < (1 << fz.c) ? " : " : "");
+    o << ");\n";
+  }
+  const char* out_name = fz.on ? "out_dst" : "psi_out";
   if (direct) {
     // store slot bit r sits at output position pos[r]; lanes 0..2 carry slot
     // bits 0..2, so each warp instruction writes whole 128 B lines
@@ -811,21 +833,21 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       for (int k = 0; k < RB; ++k)
         if (i >> k & 1) off |= 1ull << pos[pl.launch.fin_rpos[k]];
       if (env_on("HISVSIM_STORE_CS", "1"))
-      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; __stcs(&" << (oop ? "psi_out" : "psi")
+      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; __stcs(&" << (oop ? out_name : "psi")
         << "[dbase | " << off << "ull], v); }\n";
     else
-      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; " << (oop ? "psi_out" : "psi") << "[dbase | "
+      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; " << (oop ? out_name : "psi") << "[dbase | "
         << off << "ull] = v; }\n";
     }
     o << "  }\n}\n";
   } else {
     for (int j = 0; j < g.nreg; ++j) {
       const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
+      const std::string dst = oop ? std::string(out_name) + "[obase | " : std::string("psi[base | ");
       if (env_on("HISVSIM_STORE_CS", "1"))
-        o << "    __stcs(&" << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull], sm[sw_tid ^ " << sx
-          << "u]);\n";
+        o << "    __stcs(&" << dst << ohi_of(j) << "ull], sm[sw_tid ^ " << sx << "u]);\n";
       else
-        o << "    " << (oop ? "psi_out[obase | " : "psi[base | ") << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
+        o << "    " << dst << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
     }
     o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
     o << "    issue(i + 3);\n";
@@ -978,7 +1000,12 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
   // the structured-gate scalars multiply into one global factor, applied by
   // the last launch (runs of a program's launches must be complete, in order)
   double scale[2] = {1.0, 0.0};
-  for (size_t i = 0; i < n; ++i) srcs[i] = jit_source(plans[i], dtype, n_local, &fp64[i], scale, i + 1 == n);
+  for (size_t i = 0; i < n; ++i) {
+    plans[i].carry_in[0] = scale[0];
+    plans[i].carry_in[1] = scale[1];
+    plans[i].last = i + 1 == n;
+    srcs[i] = jit_source(plans[i], dtype, n_local, &fp64[i], scale, i + 1 == n);
+  }
   std::vector<int> status(n, HS_OK);
   std::vector<std::string> errs(n);
   unsigned hw = std::thread::hardware_concurrency();
@@ -1003,6 +1030,19 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
 }
 
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local) { return jit_source(pl, dtype, n_local); }
+
+int jit_recompile(PartPlan& pl, int dtype, int n_local, int device, int smem_optin, std::string& err) {
+  double scale[2] = {pl.carry_in[0], pl.carry_in[1]};
+  double fp64 = 0.0;
+  const std::string src = jit_source(pl, dtype, n_local, &fp64, scale, pl.last);
+  cudaSetDevice(device);
+  void* k = nullptr;
+  const int s = compile_one(src, &k, err);
+  if (s != HS_OK) return s;
+  cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  pl.jit = k;
+  return HS_OK;
+}
 
 std::string hs_cache_dir() { return cache_dir(); }
 

@@ -224,7 +224,7 @@ class ShardedRun:
     def __init__(self, circuit, partition, num_rank_bits: int, group=None, device=None, ops=None,
                  dtype="complex128", program=True, chunk_bytes: int = SWITCH_CHUNK_BYTES, basis_start: bool = True,
                  loopback: bool = False, policy: str = "lookahead", transport: str = "nccl",
-                 staging_bytes: int | None = None):
+                 staging_bytes: int | None = None, fuse_switches: bool = True):
         """``loopback``: all ranks live in this process on one device
         (``run_loopback``); no process group is used. ``policy``: layout
         schedule (``dist.plan_layouts``): "lookahead" (default: fewest remap
@@ -296,6 +296,12 @@ class ShardedRun:
         self.transport = "nccl"
         self.transport_note = None
         self._peer = None
+        # p2p: switches fused into the last pass of the segment before them
+        # (hs_program_fuse_switch), set up on the first run with a shard
+        self.fuse_switches = fuse_switches
+        self._fused = {}        # switch index a -> True when segment a-1's last launch performs it
+        self._fused_for = None  # data_ptr of the shard the fused launches write
+        self._state_maps = []   # peers' shard storages mapped through CUDA IPC (kept alive)
         if transport != "nccl" and not loopback and self.world > 1 and self.switch_at:
             amp = 16 if str(dtype) in ("complex128", "c128", "torch.complex128") else 8
             shard = amp << self.n_local
@@ -329,7 +335,8 @@ class ShardedRun:
 
     def comm_summary(self) -> dict:
         return {"switches": self.stats.num_switches, "bytes_remote_total": self.stats.total_bytes,
-                "remote_fraction_of_state": self.stats.total_bytes / float((1 << self.n) * 16)}
+                "remote_fraction_of_state": self.stats.total_bytes / float((1 << self.n) * 16),
+                "fused_switches": len(self._fused)}
 
     @staticmethod
     def switch_plan(old: RankLayout, new: RankLayout, phys=None):
@@ -475,6 +482,59 @@ class ShardedRun:
         dist.barrier(self.group)  # nobody packs into a staging buffer a peer still reads
         return shard
 
+    def _setup_fused(self, shard) -> None:
+        """p2p transport: map every rank's shard (CUDA IPC through torch's
+        storage sharing) and fuse each switch into the last launch of the
+        segment before it when that launch is out of place, writes the state
+        and keeps the outgoing qubits off its tile (hs_program_fuse_switch);
+        the others stay separate switches. Collective."""
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        if self._fused_for == shard.data_ptr():
+            return
+        storage = shard.untyped_storage()
+        info = storage._share_cuda_()
+        mine = (info, shard.storage_offset() * shard.element_size())
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, mine, group=self.group)
+        ptrs, maps = [], []
+        for r, (inf, off) in enumerate(gathered):
+            if r == self.rank:
+                ptrs.append(shard.data_ptr())
+                continue
+            st = torch.UntypedStorage._new_shared_cuda(*inf)
+            maps.append(st)
+            ptrs.append(st.data_ptr() + off)
+        self._state_maps = maps
+        lib = _native.load()
+        self._fused = {}
+        R = self.world
+        for si in range(len(self.segments) - 1):
+            a = self.segments[si + 1][0]
+            pr = self.programs[si]
+            if a not in self.switch_at or pr is None:
+                continue
+            pa, c, dst, slot = group_switch_args(self, si + 1)
+            last = pr.num_launches - 1
+            ok = 1 <= c <= 3
+            if ok:
+                outs = (ctypes.c_uint64 * (1 << c))(*[ptrs[dst[(self.rank << c) | k]] for k in range(1 << c)])
+                sp = (ctypes.c_int32 * c)(*pa)
+                ok = lib.hs_program_fuse_switch(pr._h, last, c, sp, outs, slot[self.rank]) == 0
+            else:
+                lib.hs_program_fuse_switch(pr._h, last, 0, None, None, 0)
+            # every rank fuses this switch or none does
+            flags = [None] * R
+            dist.all_gather_object(flags, bool(ok), group=self.group)
+            if all(flags):
+                self._fused[a] = True
+            elif ok:
+                lib.hs_program_fuse_switch(pr._h, last, 0, None, None, 0)
+        self._fused_for = shard.data_ptr()
+
     def run(self, shard, events=None, run_part=None, with_timing: bool = False):
         """All parts in order on this rank's shard (switches included);
         returns the final shard in natural order of the last layout.
@@ -489,9 +549,14 @@ class ShardedRun:
                 ev.record()
                 events.append((kind, ev))
 
+        fused = run_part is None and self.transport == "p2p" and self.fuse_switches and self.programs
+        if fused:
+            self._setup_fused(shard)
         sw_marks = []
         for si, (a, b) in enumerate(self.segments):
-            if a in self.switch_at:
+            if a in self.switch_at and fused and self._fused.get(a):
+                mark("switch")  # done by the previous segment's last launch
+            elif a in self.switch_at:
                 old, new, _ = self.switch_at[a]
                 phys = self.seg_phys_out[si - 1] if run_part is None and self.programs else None
                 if with_timing:
@@ -512,7 +577,29 @@ class ShardedRun:
                         run_part(shard, self.exes[j])
             elif self.programs[si] is not None:
                 self._share_scratch(shard)
-                self.programs[si].run(shard)
+                nxt = self.segments[si + 1][0] if si + 1 < len(self.segments) else None
+                if fused and self._fused.get(nxt):
+                    import torch.distributed as dist
+
+                    pr = self.programs[si]
+                    pr.run(shard, 0, pr.num_launches - 1)
+                    # the last launch overwrites peers' shards: every rank must
+                    # be past its own reads of them
+                    stream = torch.cuda.current_stream(shard.device)
+                    stream.synchronize()
+                    dist.barrier(self.group)
+                    if with_timing:
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                    pr.run(shard, pr.num_launches - 1, 1)
+                    stream.synchronize()
+                    dist.barrier(self.group)  # every tile has landed before the next segment reads
+                    if with_timing:
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e1.record()
+                        sw_marks.append((e0, e1))
+                else:
+                    self.programs[si].run(shard)
             mark("parts")
         if sw_marks:
             sw_marks[-1][1].synchronize()

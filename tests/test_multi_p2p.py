@@ -27,7 +27,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, name, limit, policy, staging, out):
+def _worker(rank, world, port, name, limit, policy, staging, out, fuse=False):
     import sys
     from pathlib import Path
 
@@ -46,7 +46,7 @@ def _worker(rank, world, port, name, limit, policy, staging, out):
         c = configs.build(name)
         part = partition_dfs(build_dag(c), limit)
         run = ShardedRun(c, part, world.bit_length() - 1, device="cuda:0", policy=policy, transport="p2p",
-                         staging_bytes=staging)
+                         staging_bytes=staging, fuse_switches=fuse)
         assert run.transport == "p2p" and run.switch_at
         shard = allocate(run.n_local, device="cuda:0")
         if rank == 0:
@@ -55,15 +55,31 @@ def _worker(rank, world, port, name, limit, policy, staging, out):
             shard.zero_()
         shard = run.run(shard, with_timing=True)
         torch.cuda.synchronize()
-        out[rank] = (shard_positions(run.layouts[-1], rank), shard.cpu().numpy(), list(run.stats.switch_time_s))
+        # a second run on the same buffers (fused launches stay bound to them)
+        if rank == 0:
+            init_basis(shard, 0)
+        else:
+            shard.zero_()
+        shard = run.run(shard, with_timing=True)
+        torch.cuda.synchronize()
+        out[rank] = (shard_positions(run.layouts[-1], rank), shard.cpu().numpy(), list(run.stats.switch_time_s),
+                     len(run._fused))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,name,policy,staging", [(2, "c3@22", "lookahead", 1 << 20),
-                                                       (2, "c2@21", "reference", 4096),
-                                                       (4, "c3@22", "reference", 1 << 18)])
-def test_p2p_switch_two_processes_one_gpu(world, name, policy, staging):
+@pytest.mark.parametrize("world,name,policy,staging,fuse", [(2, "c3@22", "lookahead", 1 << 20, False),
+                                                            (2, "c2@21", "reference", 4096, False),
+                                                            (4, "c3@22", "reference", 1 << 18, False),
+                                                            (2, "c3@25", "lookahead", 1 << 20, True),
+                                                            (2, "c2@25", "reference", 1 << 20, True),
+                                                            (4, "c3@26", "lookahead", 1 << 20, True)])
+def test_p2p_switch_two_processes_one_gpu(world, name, policy, staging, fuse):
+    """... and with ``fuse``: shards of >= 23 local qubits run ping-pong
+    segment programs, and a switch whose outgoing qubits stay off the
+    preceding segment's last tile is fused into that launch
+    (hs_program_fuse_switch: the tiles go straight into the owners' shards
+    through the IPC mappings, no pack / pull passes)."""
     from oracle import c_oracle
     from paper_2205_06973_b200 import build_dag, configs, partition_dfs
 
@@ -71,7 +87,8 @@ def test_p2p_switch_two_processes_one_gpu(world, name, policy, staging):
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, 10, policy, staging, out)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, 10, policy, staging, out, fuse))
+             for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
@@ -82,7 +99,9 @@ def test_p2p_switch_two_processes_one_gpu(world, name, policy, staging):
     ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
     full = np.zeros(1 << c.num_qubits, dtype=np.complex128)
     for r in range(world):
-        pos, amp, times = out[r]
+        pos, amp, times, nfused = out[r]
         full[pos] = amp
         assert times and min(times) > 0
     assert float(np.max(np.abs(full - ref))) < 1e-10
+    if fuse:
+        print(f"{name} over {world}: {out[0][3]} fused switch(es)")
