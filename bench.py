@@ -157,12 +157,29 @@ def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup):
     c_oracle.lib()
     threads = c_oracle.threads()
     n = circuit.num_qubits
+    slots = [c_oracle.part_slots(circuit, p.gate_indices, p.qubits) for p in part.parts]
+    # a state that does not fit the host (36 qubits = 1 TiB) is sampled on a
+    # host-sized one: each part keeps its gates, width and the order of its
+    # positions, compressed onto the lowest qubits that fit (the sample only
+    # sets the lowest free bits of a fixing anyway); said in `sample`
+    host = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    n_host = n
+    while (16 << n_host) > 0.4 * host and n_host > 1 + max(len(pos) for pos, _, _ in slots):
+        n_host -= 1
+    if n_host < n:
+        squeezed = []
+        for pos, ops, sl in slots:
+            top = n_host - len(pos)  # keep positions below `top`, move the rest just below n_host
+            high = [q for q in pos if q >= top]
+            remap = {q: (q if q < top else top + high.index(q)) for q in pos}
+            squeezed.append((tuple(sorted(remap[q] for q in pos)), ops, sl))
+        slots = squeezed
+        n = n_host
     # calibrate: fixings per part so that one step takes ~target seconds
     target = args.cpu_step_seconds
     psi = np.empty(1 << n, dtype=np.complex128)
     psi.fill(0)  # fault the pages in before timing anything
     psi[0] = 1.0
-    slots = [c_oracle.part_slots(circuit, p.gate_indices, p.qubits) for p in part.parts]
     def make_plan(frac):
         return [(pos, ops, sl, max(1, min(1 << (n - len(pos)), int((1 << (n - len(pos))) * frac))))
                 for pos, ops, sl in slots]
@@ -199,7 +216,10 @@ def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup):
     dt = time.perf_counter() - t0
     value = nbytes / dt / 1e9
     sample_amps = sum(k << len(pos) for pos, _, _, k in plan)
-    sample = (f"{config_label(args)}: each step runs every one of the {len(plan)} parts over "
+    sample = (("" if n == circuit.num_qubits else
+               f"state squeezed to {n} of {circuit.num_qubits} qubits to fit the host (parts' positions "
+               f"compressed onto the lowest qubits); ") +
+              f"{config_label(args)}: each step runs every one of the {len(plan)} parts over "
               f"{sample_amps / (1 << n) / len(plan):.4%} of its fixings ({sample_amps} amplitude updates "
               f"per step, fixings 0..k-1 of each part) with {threads} threads; GB/s = 2 x 16 B x "
               f"amplitudes / time, the same algorithmic count as the GPU arm")
