@@ -194,9 +194,9 @@ const char* hs_program_jit_error(hs_program* prog);
  * (one process per GPU, peer memory): instead of writing its tile to this
  * rank's state, the launch writes it to the state buffer of the rank that
  * owns it after the switch - out_ptrs[k] (a device pointer, e.g. an IPC
- * mapping of that rank's state) for the tiles whose bits at the outgoing
- * qubits' positions seg_pos[] (ascending, outside the launch's tile) spell k -
- * at the same offset with those bits replaced by my_slot. This is the
+ * mapping of that rank's state) for the amplitudes whose output index's bits
+ * at the outgoing qubits' positions seg_pos[] (ascending) spell k - at the
+ * same index with those bits replaced by my_slot. This is the
  * in-place switch of hs_group_switch without the pack and pull passes: the
  * transfer rides on the pass's stores. The launch must be out of place and
  * write the state (out_buf 0); every rank's previous launch must be complete

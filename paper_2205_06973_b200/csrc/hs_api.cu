@@ -355,9 +355,6 @@ int hs_program_fuse_switch(hs_program* prog, int launch, int num_seg_bits, const
       f.pa[b] = seg_pos[b];
       if (seg_pos[b] < 0 || seg_pos[b] >= prog->n_local || (b && seg_pos[b] <= seg_pos[b - 1]))
         return fail(HS_ERR_INVALID, "segment positions must be ascending positions of the shard");
-      for (int r = 0; r < pl.launch.T; ++r)
-        if (pl.launch.opos[r] == seg_pos[b])
-          return fail(HS_ERR_UNSUPPORTED, "a segment position is a tile bit of the launch");
     }
     for (int k = 0; k < (1 << num_seg_bits); ++k) {
       if (!out_ptrs[k]) return fail(HS_ERR_INVALID, "NULL destination");

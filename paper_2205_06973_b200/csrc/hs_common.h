@@ -68,11 +68,11 @@ struct PartLaunch {
 static_assert(sizeof(PartLaunch) == 144, "PartLaunch layout");
 
 // A layout switch fused into an out-of-place launch (one process per GPU,
-// peer memory): the launch writes each tile straight into the state buffer of
-// the rank that owns it after the switch. The switch's outgoing qubits sit on
-// output positions pa[] outside the tile, so a whole tile has one owner:
-// segment k = the tile's bits at pa -> rank dst[k], written at the same offset
-// with the pa bits replaced by this rank's slot (its incoming qubits' values).
+// peer memory): the launch writes every amplitude straight into the state
+// buffer of the rank that owns it after the switch: segment k = the output
+// index's bits at the outgoing qubits' positions pa[] -> out_ptr[k], at the
+// same index with the pa bits replaced by this rank's slot (its incoming
+// qubits' values).
 struct FuseSwitch {
   int on = 0;
   int c = 0;                 // outgoing qubits (segment bits)

@@ -798,28 +798,30 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   emit_program(g, pl, cl > 0 ? "TEAM_CSYNC();" : "TEAM_SYNC();", fp64_per_amp, "TEAM_SYNC();",
                direct ? "TEAM_SYNC(); issue(i + 3);" : nullptr);
   const FuseSwitch& fz = pl.fuse;
-  if (oop && !fz.on) o << "    const unsigned long long obase = out_base(tt);\n";
+  if (oop) o << "    const unsigned long long obase = out_base(tt);\n";
+  // fused layout switch: every amplitude goes to the rank that owns it after
+  // the switch - the one picked by its output index's bits at the outgoing
+  // qubits' positions (per tile when those are free bits, per register or
+  // lane when they are tile bits) - at the same index with those bits
+  // replaced by this rank's slot (FSTORE)
   if (oop && fz.on) {
-    // fused layout switch: the tile's owner after the switch is picked by its
-    // bits at the outgoing qubits' positions (free positions: one owner per
-    // tile); it is written there, those bits replaced by this rank's slot
     uint64_t pam = 0, slotbits = 0;
     for (int b = 0; b < fz.c; ++b) {
       pam |= 1ull << fz.pa[b];
       if (fz.slot >> b & 1) slotbits |= 1ull << fz.pa[b];
     }
-    o << "    const unsigned long long obase_raw = out_base(tt);\n";
-    o << "    unsigned seg_k = 0u;\n";
-    for (int b = 0; b < fz.c; ++b)
-      o << "    seg_k |= (unsigned)((obase_raw >> " << fz.pa[b] << ") & 1ull) << " << b << ";\n";
-    o << "    const unsigned long long obase = (obase_raw & ~" << pam << "ull) | " << slotbits << "ull;\n";
-    o << "    C* const out_dst = reinterpret_cast<C*>(";
+    std::ostringstream sel;
+    sel << "unsigned k_ = 0u;";
+    for (int b = 0; b < fz.c; ++b) sel << " k_ |= (unsigned)((x_ >> " << fz.pa[b] << ") & 1ull) << " << b << ";";
+    std::ostringstream ptr;
     for (int k = 0; k < (1 << fz.c); ++k)
-      o << (k + 1 < (1 << fz.c) ? "seg_k == " + std::to_string(k) + "u ? " : "") << "0x" << std::hex << fz.out_ptr[k]
-        << std::dec << "ull" << (k + 1 < (1 << fz.c) ? " : " : "");
-    o << ");\n";
+      ptr << (k + 1 < (1 << fz.c) ? "k_ == " + std::to_string(k) + "u ? " : "") << "0x" << std::hex << fz.out_ptr[k]
+          << std::dec << "ull" << (k + 1 < (1 << fz.c) ? " : " : "");
+    o << "#define FSTORE(X, V) do { const unsigned long long x_ = (X); " << sel.str()
+      << " reinterpret_cast<C*>(" << ptr.str() << ")[(x_ & ~" << pam << "ull) | " << slotbits
+      << "ull] = (V); } while (0)\n";
   }
-  const char* out_name = fz.on ? "out_dst" : "psi_out";
+  const bool fstore = oop && fz.on;
   if (direct) {
     // store slot bit r sits at output position pos[r]; lanes 0..2 carry slot
     // bits 0..2, so each warp instruction writes whole 128 B lines
@@ -832,19 +834,23 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       uint64_t off = 0;
       for (int k = 0; k < RB; ++k)
         if (i >> k & 1) off |= 1ull << pos[pl.launch.fin_rpos[k]];
-      if (env_on("HISVSIM_STORE_CS", "1"))
-      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; __stcs(&" << (oop ? out_name : "psi")
+      if (fstore)
+      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; FSTORE(dbase | " << off << "ull, v); }\n";
+    else if (env_on("HISVSIM_STORE_CS", "1"))
+      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; __stcs(&" << (oop ? "psi_out" : "psi")
         << "[dbase | " << off << "ull], v); }\n";
     else
-      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; " << (oop ? out_name : "psi") << "[dbase | "
+      o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; " << (oop ? "psi_out" : "psi") << "[dbase | "
         << off << "ull] = v; }\n";
     }
     o << "  }\n}\n";
   } else {
     for (int j = 0; j < g.nreg; ++j) {
       const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
-      const std::string dst = oop ? std::string(out_name) + "[obase | " : std::string("psi[base | ");
-      if (env_on("HISVSIM_STORE_CS", "1"))
+      const std::string dst = oop ? std::string("psi_out[obase | ") : std::string("psi[base | ");
+      if (fstore)
+        o << "    FSTORE(obase | " << ohi_of(j) << "ull, sm[sw_tid ^ " << sx << "u]);\n";
+      else if (env_on("HISVSIM_STORE_CS", "1"))
         o << "    __stcs(&" << dst << ohi_of(j) << "ull], sm[sw_tid ^ " << sx << "u]);\n";
       else
         o << "    " << dst << ohi_of(j) << "ull] = sm[sw_tid ^ " << sx << "u];\n";
