@@ -576,11 +576,23 @@ def gpu_arm(args, circuit, part, rank, world):
     if dist:
         sw = [sum(c) / len(c) for c in zip(*switch_list)] if switch_list and switch_list[0] else []
         sw_ms = sum(sw)
+        # switches fused into the previous segment's last launch move their
+        # bytes inside that launch (counted in parts time): the NVLink rate is
+        # over the separate switches only
+        order = sorted(run.switch_at)
+        fused = [a in getattr(run, "_fused", {}) for a in order]
+        sep_bytes = sum(st.bytes_remote for st, f in zip(run.stats.switches, fused) if not f)
+        sep_ms = sum(t for t, f in zip(sw, fused) if not f)
         comm = dict(run.comm_summary(), transport=run.transport, transport_note=run.transport_note,
-                    switch_ms_per_step=sw_ms, per_switch_ms=[round(x, 4) for x in sw],
+                    switch_ms_per_step=sw_ms, per_switch_ms=[round(x, 4) for x in sw], fused=fused,
                     parts_ms_per_step=seg_ms / n_marked,
-                    nvlink_gbs_per_rank=(run.stats.total_bytes / world / (sw_ms / 1e3) / 1e9 if sw_ms > 0 else None),
-                    nvlink_note="bytes each rank sends over all switches (closed-form CommStats / ranks) / switch time")
+                    nvlink_gbs_per_rank=(sep_bytes / world / (sep_ms / 1e3) / 1e9 if sep_ms > 0 and sep_bytes else None),
+                    nvlink_note="bytes each rank sends over the separate (unfused) switches (closed-form CommStats / "
+                                "ranks) / their time; fused switches ride on the preceding pass's stores")
+    if dist:
+        for r_ in (run, locals().get("run_e2e")):
+            if r_ is not None:
+                r_.release()
     return {
         "ms_step": ms_step, "value": value, "moved": moved, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
         "launch_ms": [sum(c) / len(c) for c in zip(*launch_ms)] if launch_ms else [],

@@ -535,6 +535,23 @@ class ShardedRun:
                 lib.hs_program_fuse_switch(pr._h, last, 0, None, None, 0)
         self._fused_for = shard.data_ptr()
 
+    def release(self) -> None:
+        """Drop the fused launches' peer mappings (collective: every rank
+        unmaps its peers' shards before any producer goes away)."""
+        import torch
+        import torch.distributed as dist
+
+        if not self._state_maps and not self._fused:
+            return
+        lib = _native.load()
+        for si in range(len(self.segments) - 1):
+            if self._fused.get(self.segments[si + 1][0]) and self.programs[si] is not None:
+                pr = self.programs[si]
+                lib.hs_program_fuse_switch(pr._h, pr.num_launches - 1, 0, None, None, 0)
+        torch.cuda.synchronize()
+        self._state_maps, self._fused, self._fused_for = [], {}, None
+        dist.barrier(self.group)
+
     def run(self, shard, events=None, run_part=None, with_timing: bool = False):
         """All parts in order on this rank's shard (switches included);
         returns the final shard in natural order of the last layout.

@@ -64,6 +64,7 @@ def _worker(rank, world, port, name, limit, policy, staging, out, fuse=False):
         torch.cuda.synchronize()
         out[rank] = (shard_positions(run.layouts[-1], rank), shard.cpu().numpy(), list(run.stats.switch_time_s),
                      len(run._fused))
+        run.release()
     finally:
         dist.destroy_process_group()
 
