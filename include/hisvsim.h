@@ -336,6 +336,9 @@ int hs_group_switch(hs_group* group, void* const* shards, int n_local, int dtype
  * from a peer's staging. Buffers to export come from hs_device_alloc (a
  * whole allocation: the mapped pointer is its base). */
 int hs_device_alloc(size_t bytes, void** device_ptr);
+/* let kernels on the current device read / write peer_device's memory
+ * (NVLink / NVSwitch); a no-op for the current device itself */
+int hs_enable_peer_access(int peer_device);
 int hs_device_free(void* device_ptr);
 int hs_ipc_get_handle(const void* device_ptr, void* handle_out);
 int hs_ipc_open_handle(const void* handle, void** device_ptr);

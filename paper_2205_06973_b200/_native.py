@@ -38,7 +38,7 @@ EXPORTS = (
     "hs_state_init_basis", "hs_bit_permute", "hs_fp64_peak", "hs_max_abs_diff",
     "hs_pack_segments", "hs_unpack_segments", "hs_pack_segments_range", "hs_unpack_segments_range",
     "hs_unpack_segments_range_from", "hs_group_create", "hs_group_destroy", "hs_group_switch",
-    "hs_ipc_get_handle", "hs_ipc_open_handle", "hs_ipc_close", "hs_device_alloc", "hs_device_free",
+    "hs_ipc_get_handle", "hs_ipc_open_handle", "hs_ipc_close", "hs_device_alloc", "hs_device_free", "hs_enable_peer_access",
 )
 
 
@@ -148,6 +148,7 @@ def _declare(lib) -> None:
         "hs_ipc_close": (I, [P]),
         "hs_device_alloc": (I, [ctypes.c_size_t, ctypes.POINTER(P)]),
         "hs_device_free": (I, [P]),
+        "hs_enable_peer_access": (I, [I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -833,6 +833,19 @@ int hs_group_switch(hs_group* g, void* const* shards, int n_local, int dtype, co
   return HS_OK;
 }
 
+int hs_enable_peer_access(int peer_device) {
+  int dev = 0, ok = 0;
+  HS_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  if (peer_device == dev) return HS_OK;
+  HS_CUDA(cudaDeviceCanAccessPeer(&ok, dev, peer_device), "cudaDeviceCanAccessPeer");
+  if (!ok) return fail(HS_ERR_UNSUPPORTED, "device " + std::to_string(dev) + " has no peer access to device " +
+                                               std::to_string(peer_device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+  else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return HS_OK;
+}
+
 int hs_device_alloc(size_t bytes, void** device_ptr) {
   if (!device_ptr) return fail(HS_ERR_INVALID, "NULL argument");
   *device_ptr = nullptr;

@@ -160,6 +160,11 @@ class PeerStaging:
             torch.cuda.set_device(torch.device(device))
         handles = []
         try:
+            # kernels here read the peers' staging and write their shards
+            devs = [None] * self.world
+            dist.all_gather_object(devs, torch.cuda.current_device(), group=group)
+            for d in sorted(set(devs)):
+                _native.check(lib.hs_enable_peer_access(int(d)))
             for _ in range(2):
                 ptr = ctypes.c_void_p()
                 _native.check(lib.hs_device_alloc(self.bytes, ctypes.byref(ptr)))
