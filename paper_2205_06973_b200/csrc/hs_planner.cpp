@@ -1467,7 +1467,8 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       std::vector<Grouping> modes = {GROUP_ACROSS, GROUP_FRONTIER, GROUP_FRONTIER_SEEDED, GROUP_REVERSE_LOW3,
                                      GROUP_REVERSE_LOW6, GROUP_REVERSE_PLAIN_LOW3, GROUP_REVERSE_PLAIN_LOW6};
       const char* beam_env = std::getenv("HISVSIM_BEAM");  // "0": greedy groupings only (A/B)
-      if (stream_gates <= BEAM_MAX_GATES && !fp64_bound && !(beam_env && std::string(beam_env) == "0")) {
+      const bool beam_forced = beam_env && std::string(beam_env) == "1";
+      if (stream_gates <= BEAM_MAX_GATES && (!fp64_bound || beam_forced) && !(beam_env && std::string(beam_env) == "0")) {
         modes.push_back(GROUP_BEAM_REVERSE);
         modes.push_back(GROUP_BEAM_REVERSE_PEN);
       }
