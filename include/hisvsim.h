@@ -144,7 +144,13 @@ typedef struct {
  * the tile (fewer launches than parts when consecutive parts together fit
  * one tile; same results, launches report the part they mostly carry) */
 #define HS_PLAN_MERGE 0x400u
-#define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY | HS_PLAN_MERGE)
+/* with HS_PLAN_MERGE | HS_PLAN_JIT | HS_PLAN_PARITY: diagonal gates (Z-type
+ * 1-qubit gates, CZ, CRZ, CX.D.CX parity diagonals) need not have their
+ * qubits staged - a compiled pass applies them from the tile's free index
+ * bits - so regrouped passes stage only the qubits their non-diagonal gates
+ * act on (fewer passes; kept when the grouping takes fewer launches) */
+#define HS_PLAN_GLOBAL_DIAG 0x800u
+#define HS_PLAN_DEFAULT (HS_PLAN_FUSE_1Q | HS_PLAN_PARITY | HS_PLAN_MERGE | HS_PLAN_GLOBAL_DIAG)
 
 typedef struct hs_engine hs_engine;
 typedef struct hs_program hs_program;

@@ -217,8 +217,8 @@ def engine_query(device: int) -> dict:
 
 HS_PLAN_FUSE_1Q, HS_PLAN_RB3, HS_PLAN_PARITY, HS_PLAN_LAYOUT, HS_PLAN_JIT = 0x1, 0x2, 0x4, 0x8, 0x10
 HS_PLAN_INIT_LAYOUT, HS_PLAN_PINGPONG, HS_PLAN_CLUSTER, HS_PLAN_NO_RESTORE = 0x20, 0x40, 0x80, 0x100
-HS_PLAN_PART_LOCAL, HS_PLAN_MERGE = 0x200, 0x400
-HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY | HS_PLAN_MERGE
+HS_PLAN_PART_LOCAL, HS_PLAN_MERGE, HS_PLAN_GLOBAL_DIAG = 0x200, 0x400, 0x800
+HS_PLAN_DEFAULT = HS_PLAN_FUSE_1Q | HS_PLAN_PARITY | HS_PLAN_MERGE | HS_PLAN_GLOBAL_DIAG
 
 
 def set_options(device: int, options: int) -> None:

@@ -202,6 +202,12 @@ static int program_create(hs_engine* eng, int n_local, int dtype, const hs_part*
     int s = jit_compile_program(prog->plans, dtype, n_local, eng->device, eng->smem_optin, err);
     if (s != HS_OK) prog->jit_error = err;  // interpreter fallback on the GPU, reported
   }
+  // passes with global (unstaged) diagonal qubits exist only as compiled
+  // kernels: the interpreter cannot run them
+  for (const auto& pl : prog->plans)
+    if (!pl.jit && !pl.prog.empty() && pl.prog[0].op == I_GLOBALS)
+      return fail(HS_ERR_UNSUPPORTED, "compiled passes failed (" + prog->jit_error +
+                                           "); passes with global diagonal qubits have no interpreter form");
   size_t total = 0;
   for (auto& pl : prog->plans) {
     pl.launch.prog_offset = (int64_t)total;

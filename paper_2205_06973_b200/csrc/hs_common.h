@@ -1,6 +1,7 @@
 // Internal definitions shared by the planner (host C++) and the part kernels.
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -14,6 +15,11 @@ enum : uint16_t {
   I_DENSE = 2,  // 2x2 on register bit k, predicated on controls
   I_PERM = 3,   // X-type exchange on register bit k, predicated on controls
   I_DIAG = 4,   // diag(d0, d1) on a target bit (register k or tid-mask), predicated
+  // compiled passes only (first instruction of a program that has them): the
+  // physical positions of the pass's global qubits - qubits some diagonal
+  // gate acts on that are not staged; their values are the tile's free index
+  // bits. k = count, the positions are bytes of m[] (up to 64).
+  I_GLOBALS = 5,
 };
 
 // DIAG flags
@@ -41,6 +47,25 @@ struct alignas(16) Instr {
   double m[8];     // DENSE: m00 m01 m10 m11 (re, im); DIAG: d0, d1
 };
 static_assert(sizeof(Instr) == 96, "Instr layout");
+// DIAG instructions on global qubits keep two more masks in m[4] / m[5]
+// (raw bits; a DIAG uses only m[0..3]): gq = global qubits in the entry's
+// parity, gc = global controls (bit j = the program's I_GLOBALS entry j).
+inline uint64_t instr_gq(const Instr& in) {
+  if (in.op != I_DIAG) return 0;
+  uint64_t v;
+  std::memcpy(&v, &in.m[4], 8);
+  return v;
+}
+inline uint64_t instr_gc(const Instr& in) {
+  if (in.op != I_DIAG) return 0;
+  uint64_t v;
+  std::memcpy(&v, &in.m[5], 8);
+  return v;
+}
+inline void instr_set_global(Instr& in, uint64_t gq, uint64_t gc) {
+  std::memcpy(&in.m[4], &gq, 8);
+  std::memcpy(&in.m[5], &gc, 8);
+}
 
 // Everything a part launch needs besides the instruction array.
 struct PartLaunch {
@@ -122,14 +147,15 @@ struct LayoutIO {
 // Plan one part. Returns HS_OK or an error code with `err` filled.
 int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int32_t* staged, int w,
               const hs_gate* gates, int num_gates, PartPlan& out, std::string& err,
-              const LayoutIO* lay = nullptr);
+              const LayoutIO* lay = nullptr, const int32_t* gpos = nullptr, int ng = 0);
 
 // Plan a whole part sequence (with HS_PLAN_LAYOUT: evolving layout plus the
 // restore launches that bring every qubit home at the end).
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                  const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
                  std::vector<int32_t>* init_phys = nullptr, const int32_t* given_init = nullptr,
-                 std::vector<int32_t>* final_phys = nullptr);
+                 std::vector<int32_t>* final_phys = nullptr,
+                 const std::vector<std::vector<int32_t>>* globals = nullptr);
 
 // 2x2 base matrix of a gate kind (controls handled by masking), row-major
 // complex: m[0..7] = m00 re/im, m01, m10, m11. Mirrors statevec.py:33-98.

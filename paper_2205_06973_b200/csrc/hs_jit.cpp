@@ -63,7 +63,7 @@ int l2_prefetch_ahead() {
   return std::max(0, std::min(8, std::atoi(e)));
 }
 
-std::string lit(double v, bool c128) {
+std::string lit_raw(double v, bool c128) {
   char buf[64];
   std::snprintf(buf, sizeof(buf), "%a", v);
   std::string s(buf);
@@ -79,8 +79,47 @@ struct Gen {
   std::vector<int> var;  // register slot i -> variable index
   const char* R() const { return c128 ? "double" : "float"; }
 
+  // FP64 literals of one kernel, deduplicated by magnitude: products and
+  // factorisations of the same gate set give values a few ulps apart
+  // (1/sqrt(2) came out in 12 spellings in one c2 part). ptxas keeps a
+  // kernel's distinct constants in uniform registers while they fit (63 per
+  // warp, 2 per FP64 value) and spills the rest to vector registers, which
+  // makes the DFMA read three vector operands (the slow issue rate of
+  // profiles/tools/fp64probe.cu). Values within 1e-14 relative of an earlier
+  // one reuse it (negation is a free operand modifier); the change per gate
+  // entry is ~50 ulps, far inside the 1e-10 tolerance.
+  std::vector<double> pool;
+  bool dedup = !env_on("HISVSIM_LIT_DEDUP", "0");  // "0": every literal as computed (A/B)
+  std::string lit(double v, bool c) {
+    const double a = std::fabs(v);
+    if (dedup && a != 0.0 && a != 1.0) {
+      for (double p : pool)
+        if (std::fabs(a - p) <= 1e-14 * p) return lit_raw(v < 0 ? -p : p, c);
+      pool.push_back(a);
+    }
+    return lit_raw(v, c);
+  }
+
   std::string re(int i) { return "r" + std::to_string(var[i]); }
   std::string im(int i) { return "q" + std::to_string(var[i]); }
+
+  // A diagonal's entry parity / control test over this thread's tile bits
+  // (t) and the tile's global qubits (gw: the free index bits of the pass's
+  // I_GLOBALS positions, one word per tile)
+  std::string tparity(const Instr& in) const {
+    const uint64_t gq = instr_gq(in);
+    std::string e;
+    if (in.qtid) e = "__popc(t & " + std::to_string(in.qtid) + "u)";
+    if (gq) e += std::string(e.empty() ? "" : " + ") + "__popc(gw & " + std::to_string(gq) + "u)";
+    return e.empty() ? std::string("false") : "(((" + e + ") & 1) != 0)";
+  }
+  std::string tcond(const Instr& in) const {
+    const uint64_t gc = instr_gc(in);
+    std::string e;
+    if (in.ctid) e = "((t & " + std::to_string(in.ctid) + "u) == " + std::to_string(in.ctid) + "u)";
+    if (gc) e += std::string(e.empty() ? "" : " && ") + "((gw & " + std::to_string(gc) + "u) == " + std::to_string(gc) + "u)";
+    return e.empty() ? std::string("true") : "(" + e + ")";
+  }
 
   // thread-dependent word tdep (tile location bits of this thread's amps)
   void emit_tdep(const char* name, const uint8_t* npos) {
@@ -147,7 +186,7 @@ struct Gen {
   void cmul_into(int i, const std::string& dr, const std::string& di) {
     o << "      { const " << R() << " x = " << re(i) << ", y = " << im(i) << "; " << re(i) << " = fma(x, " << dr
       << ", -y * " << di << "); " << im(i) << " = fma(x, " << di << ", y * " << dr << "); }\n";
-    ops += 4 * wgt;
+    cat[1] += 4 * wgt; ops += 4 * wgt;
   }
   // multiply register i by a compile-time constant, exploiting 0 / +-1 parts
   void cmul_const(int i, double fr, double fi) {
@@ -158,7 +197,7 @@ struct Gen {
         return;
       }
       o << "      " << re(i) << " *= " << lit(fr, c128) << "; " << im(i) << " *= " << lit(fr, c128) << ";\n";
-      ops += 2 * wgt;
+      cat[2] += 2 * wgt; ops += 2 * wgt;
       return;
     }
     if (fr == 0.0) {  // (x + iy) * (i b) = -b y + i b x
@@ -168,7 +207,7 @@ struct Gen {
       else if (fi == -1.0) o << re(i) << " = y; " << im(i) << " = NEG(x); }\n";
       else {
         o << re(i) << " = -" << b << " * y; " << im(i) << " = " << b << " * x; }\n";
-        ops += 2 * wgt;
+        cat[2] += 2 * wgt; ops += 2 * wgt;
       }
       return;
     }
@@ -181,6 +220,7 @@ struct Gen {
   // final store (folded into the last diagonal run when there is one).
   double Sr = 1.0, Si = 0.0;
   double ops = 0;   // FP64 instructions per thread per tile (control-weighted)
+  double cat[5] = {0, 0, 0, 0, 0};  // of which: dense, diagonal apply, constant factors, mixed groups, scalar combine
   double wgt = 1;   // fraction of threads executing the current block
   bool scale_ok(double sr, double si) const {
     const double nr = Sr * sr - Si * si, ni = Sr * si + Si * sr;
@@ -209,7 +249,7 @@ struct Gen {
       else if (coef[t] == 1.0) e = "(" + e + " + " + src[t] + ")";
       else if (coef[t] == -1.0) e = "(" + e + " - " + src[t] + ")";
       else e = "fma(" + lit(coef[t], c128) + ", " + src[t] + ", " + e + ")";
-      ops += wgt;
+      cat[0] += wgt; ops += wgt;
     }
     if (start >= 0 && e == "-" + src[start]) return "NEG(" + src[start] + ")";  // a lone negation: sign bit
     return e.empty() ? std::string(c128 ? "0.0" : "0.0f") : e;
@@ -294,7 +334,7 @@ struct Gen {
         if (kreg != masks[gi]) continue;
         const std::string d0r = lit(in.m[0], c128), d0i = lit(in.m[1], c128);
         const std::string d1r = lit(in.m[2], c128), d1i = lit(in.m[3], c128);
-        o << "      { const bool tp = (__popc(t & " << in.qtid << "u) & 1) != 0;\n";
+        o << "      { const bool tp = " << tparity(in) << ";\n";
         o << "        const " << T << " ar = tp ? " << d1r << " : " << d0r << ", ai = tp ? " << d1i << " : " << d0i
           << ", br = tp ? " << d0r << " : " << d1r << ", bi = tp ? " << d0i << " : " << d1i << ";\n";
         if (first) {
@@ -331,7 +371,7 @@ struct Gen {
         } else {
           o << " { const " << T << " x = fr, y = fi; fr = x * " << r << " - y * " << im_ << "; fi = x * " << im_
             << " + y * " << r << "; }";
-          ops += 4 * wgt;
+          cat[3] += 4 * wgt; ops += 4 * wgt;
         }
       }
       o << "\n  ";
@@ -400,7 +440,7 @@ struct Gen {
         o << "      { const " << R() << " fr = fma(" << lit(cre[i], c128) << ", " << ur << ", -" << lit(cim[i], c128)
           << " * " << ui << "), fi = fma(" << lit(cre[i], c128) << ", " << ui << ", " << lit(cim[i], c128) << " * "
           << ur << ");\n  ";
-        ops += 4 * wgt;
+        cat[4] += 4 * wgt; ops += 4 * wgt;
         cmul_into(i, "fr", "fi");
         o << "      }\n";
       }
@@ -412,7 +452,7 @@ struct Gen {
   bool fold_diag(const Instr& in) {
     const bool parity = in.flags & F_PARITY;
     const uint32_t kreg = parity ? in.rpos[0] : (in.k == K_NONE ? 0u : (1u << in.k));
-    const bool tdep = in.qtid != 0 || in.ctid != 0;
+    const bool tdep = in.qtid != 0 || in.ctid != 0 || instr_gq(in) != 0 || instr_gc(in) != 0;
     const bool rdep = kreg != 0 || in.creg != 0;
     const double d0r = in.m[0], d0i = in.m[1], d1r = in.m[2], d1i = in.m[3];
     if (!tdep) {
@@ -429,7 +469,7 @@ struct Gen {
     }
     if (rdep) {
       // controlled ones, and sign flips (integer XORs, no FP64), are applied as they come
-      if (in.creg != 0 || in.ctid != 0 || cluster || (in.flags & F_SIGN)) return false;
+      if (in.creg != 0 || in.ctid != 0 || instr_gc(in) != 0 || cluster || (in.flags & F_SIGN)) return false;
       mixed.push_back(in);
       return true;
     }
@@ -440,8 +480,8 @@ struct Gen {
       have_u = true;
     }
     const std::string ur = "ur" + std::to_string(u_id), ui = "ui" + std::to_string(u_id);
-    o << "    { const bool tp = (__popc(t & " << in.qtid << "u) & 1) != 0;\n";
-    std::string cond = in.ctid ? "((t & " + std::to_string(in.ctid) + "u) == " + std::to_string(in.ctid) + "u)" : "true";
+    o << "    { const bool tp = " << tparity(in) << ";\n";
+    const std::string cond = tcond(in);
     o << "      if (" << cond << ") { const " << R() << " fr = tp ? " << lit(d1r, c128) << " : " << lit(d0r, c128)
       << ", fi = tp ? " << lit(d1i, c128) << " : " << lit(d0i, c128) << "; const " << R() << " a = " << ur << ", b = "
       << ui << "; " << ur << " = a * fr - b * fi; " << ui << " = a * fi + b * fr; } }\n";
@@ -455,8 +495,8 @@ struct Gen {
     const bool sign = in.flags & F_SIGN, d0one = in.flags & F_D0_ONE, d1one = in.flags & F_D1_ONE;
     const bool parity = in.flags & F_PARITY;
     const uint32_t kreg = parity ? in.rpos[0] : (in.k == K_NONE ? 0u : (1u << in.k));
-    const bool tbits = in.qtid != 0;
-    if (tbits) o << "      const bool tp = (__popc(t & " << in.qtid << "u) & 1) != 0;\n";
+    const bool tbits = in.qtid != 0 || instr_gq(in) != 0;
+    if (tbits) o << "      const bool tp = " << tparity(in) << ";\n";
     for (int i = 0; i < nreg; ++i) {
       if ((uint32_t(i) & in.creg) != in.creg) continue;
       const bool rp = __builtin_popcount(uint32_t(i) & kreg) & 1;
@@ -508,6 +548,7 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   const Instr* cur = nullptr;
   g.reset_pending();
   for (const Instr& in : pl.prog) {
+    if (in.op == I_GLOBALS) continue;  // the kernel's gw word (jit_source)
     if (in.op == I_DIAG && g.fold_diag(in)) continue;
     if (in.op != I_DIAG) g.flush();  // a non-diagonal step: apply the pending run first
     if (in.op == I_PHASE) {
@@ -522,8 +563,8 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
       cur = &in;
       continue;
     }
-    const bool ctl_t = in.ctid != 0;
-    if (ctl_t) o << "    if ((t & " << in.ctid << "u) == " << in.ctid << "u) {\n";
+    const bool ctl_t = in.ctid != 0 || instr_gc(in) != 0;
+    if (ctl_t) o << "    if (" << g.tcond(in) << ") {\n";
     else o << "    {\n";
     g.wgt = 1.0 / double(1u << __builtin_popcount(in.ctid));
     if (in.op == I_DENSE) g.dense(in);
@@ -537,7 +578,9 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   const bool apply = !g.carry || std::fabs(std::log2(std::hypot(g.Sr, g.Si))) > (g.c128 ? 200 : 24);
   g.flush(apply);
   if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
-  o << "    // fp64_instr_per_amp " << g.ops / g.nreg << "\n";
+  o << "    // fp64_instr_per_amp " << g.ops / g.nreg << " (dense " << g.cat[0] / g.nreg << ", diagonal apply "
+    << g.cat[1] / g.nreg << ", constants " << g.cat[2] / g.nreg << ", mixed groups " << g.cat[3] / g.nreg
+    << ", scalar combine " << g.cat[4] / g.nreg << ")\n";
   if (pl.launch.direct_store) return;  // the caller stores the registers to HBM
   // the final write goes to the store order; the read-out after it is local
   const std::string fs = xsync(cur->rpos, cur->npos, pl.launch.fin_rpos, pl.launch.fin_npos);
@@ -772,6 +815,13 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "    const long long tt = TILE(i);\n";
   o << "    if (!TILE_OK(i, tt)) break;\n";
   o << "    const unsigned long long base = tile_base(tt);\n";
+  for (const Instr& in : pl.prog) {  // the tile's global qubits (free index bits of the input)
+    if (in.op != I_GLOBALS) continue;
+    const uint8_t* gp = reinterpret_cast<const uint8_t*>(in.m);
+    o << "    const unsigned gw = 0u";
+    for (int j = 0; j < in.k; ++j) o << " | ((unsigned)((base >> " << (int)gp[j] << ") & 1ull) << " << j << ")";
+    o << ";\n";
+  }
   o << "    unsigned tid = tid0 | (rank << " << low << "); asm volatile(\"\" : \"+r\"(tid));  // keep phase addresses in the loop\n";
   o << "    const int b = (int)(i % 3);\n";
   o << "    C* sm = reinterpret_cast<C*>(smem_raw + b * " << tile_bytes << ");\n";

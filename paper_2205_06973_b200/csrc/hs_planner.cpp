@@ -28,6 +28,11 @@
 
 namespace hs {
 
+static bool env_is(const char* name, const char* value) {
+  const char* e = std::getenv(name);
+  return e && std::string(e) == value;
+}
+
 // lowest storage positions each pass hands to the next pass's qubits from
 // its own tile ($HISVSIM_HOT, default 3: 128 B runs of complex128)
 int layout_hot() {
@@ -160,6 +165,10 @@ namespace {
 
 enum Cls { C_DENSE, C_PERM, C_DIAG, C_SWAP };
 
+// tile-logical bit of a pass's global qubit j (plan_part): above every tile
+// location, so register / lane logic never sees it
+constexpr int GBIT = 32;
+
 int arity_of(int kind) {
   switch (kind) {
     case HS_CX: case HS_CZ: case HS_CRZ: case HS_CRY: case HS_SWAP: return 2;
@@ -176,8 +185,9 @@ struct Gate {
   int nctl;
   int par = -1; // DIAG on the parity tgt ^ par (from CX . D . CX), else -1
   double m[8];
-  uint32_t nd;  // tile-logical bits touched non-diagonally
-  uint32_t d;   // tile-logical bits touched diagonally (controls, diag targets)
+  uint64_t nd;  // tile-logical bits touched non-diagonally
+  uint64_t d;   // tile-logical bits touched diagonally (controls, diag targets);
+                // global qubits are bits GBIT + j
 };
 
 struct Rec {  // a scheduled gate, in locations
@@ -213,11 +223,11 @@ void classify(Gate& G) {
   bool perm = !diag && m[0] == 0 && m[1] == 0 && m[6] == 0 && m[7] == 0 && m[2] == 1 && m[3] == 0 &&
               m[4] == 1 && m[5] == 0;
   G.cls = diag ? C_DIAG : perm ? C_PERM : C_DENSE;
-  uint32_t cm = 0;
-  for (int a = 0; a < G.nctl; ++a) cm |= 1u << G.ctl[a];
-  if (G.par >= 0) cm |= 1u << G.par;
-  if (G.cls == C_DIAG) { G.nd = 0; G.d = cm | (1u << G.tgt); }
-  else { G.nd = 1u << G.tgt; G.d = cm; }
+  uint64_t cm = 0;
+  for (int a = 0; a < G.nctl; ++a) cm |= 1ull << G.ctl[a];
+  if (G.par >= 0) cm |= 1ull << G.par;
+  if (G.cls == C_DIAG) { G.nd = 0; G.d = cm | (1ull << G.tgt); }
+  else { G.nd = 1ull << G.tgt; G.d = cm; }
 }
 
 bool is_cx(const Gate& G) { return G.cls == C_PERM && G.nctl == 1 && G.par < 0; }
@@ -232,7 +242,7 @@ void fuse_parity_diagonals(std::vector<Gate>& gs) {
   for (int i = 0; i < n; ++i) {
     if (dead[i] || !is_cx(gs[i])) continue;
     const int a = gs[i].ctl[0], b = gs[i].tgt;
-    const uint32_t ab = (1u << a) | (1u << b);
+    const uint64_t ab = (1ull << a) | (1ull << b);
     auto next_on = [&](int from) {
       for (int j = from; j < n; ++j)
         if (!dead[j] && ((gs[j].nd | gs[j].d) & ab)) return j;
@@ -298,7 +308,7 @@ int compiled_cost(const Gate& G) {
 void fuse_single_qubit_runs(std::vector<Gate>& gs, int T, bool cost_aware) {
   std::vector<Gate> out;
   out.reserve(gs.size());
-  std::vector<int> open(T, -1);
+  std::vector<int> open(64, -1);  // tile bits < T, global bits GBIT + j
   for (const Gate& G : gs) {
     if (G.cls != C_SWAP && G.nctl == 0 && G.par < 0) {
       int& o = open[G.tgt];
@@ -315,8 +325,8 @@ void fuse_single_qubit_runs(std::vector<Gate>& gs, int T, bool cost_aware) {
       out.push_back(G);
       continue;
     }
-    uint32_t touched = G.nd | G.d;
-    for (int b = 0; b < T; ++b)
+    const uint64_t touched = G.nd | G.d;
+    for (int b = 0; b < 64; ++b)
       if (touched >> b & 1) open[b] = -1;
     out.push_back(G);
   }
@@ -341,7 +351,8 @@ double paper_flops(const Rec& r) {
 }  // namespace
 
 int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int32_t* staged, int w,
-              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err, const LayoutIO* lay) {
+              const hs_gate* gates, int num_gates, PartPlan& out, std::string& err, const LayoutIO* lay,
+              const int32_t* gpos, int ng) {
   if (n_local < 1 || n_local > 62) { err = "n_local outside [1, 62]"; return HS_ERR_INVALID; }
   if (w < 0 || w > HS_MAX_STAGED) { err = "staged count outside [0, 24]"; return HS_ERR_INVALID; }
   for (int j = 0; j < w; ++j) {
@@ -351,7 +362,19 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     }
     if (j && staged[j] <= staged[j - 1]) { err = "staged positions not strictly ascending"; return HS_ERR_INVALID; }
   }
+  // global qubits (gate slots w .. w + ng - 1): positions outside the tile
+  // that only diagonal gates act on; compiled, single-CTA passes only
+  if (ng < 0 || ng > 32 || (ng > 0 && !gpos)) { err = "global qubit count outside [0, 32]"; return HS_ERR_INVALID; }
+  for (int j = 0; j < ng; ++j) {
+    if (gpos[j] < 0 || gpos[j] >= n_local) { err = "global position outside the state"; return HS_ERR_INVALID; }
+    for (int i = 0; i < w; ++i)
+      if (staged[i] == gpos[j]) { err = "global position is staged"; return HS_ERR_INVALID; }
+    for (int i = 0; i < j; ++i)
+      if (gpos[i] == gpos[j]) { err = "repeated global position"; return HS_ERR_INVALID; }
+  }
+  if (ng > 0 && !(options & HS_PLAN_JIT)) { err = "global qubits need compiled passes (HS_PLAN_JIT)"; return HS_ERR_UNSUPPORTED; }
   const int T = std::min(std::max(tile_max, w), n_local);
+  if (ng > 0 && (T > tile_max || w + ng > n_local)) { err = "global qubits on a cluster tile"; return HS_ERR_UNSUPPORTED; }
   // a part wider than one CTA's tile runs as a cluster tile (compiled parts)
   const int cluster_log = T > tile_max ? T - tile_max : 0;
   if (cluster_log > 0 && (!(options & HS_PLAN_JIT) || !(options & HS_PLAN_CLUSTER) || cluster_log > MAX_CLUSTER_LOG)) {
@@ -376,6 +399,20 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   std::sort(tile.begin(), tile.end());
   std::vector<int> tl(w);
   for (int j = 0; j < w; ++j) tl[j] = int(std::find(tile.begin(), tile.end(), phy[j]) - tile.begin());
+  // global qubits the tile's fill took in (lowest free positions) are tile
+  // bits like any other; the rest keep bits GBIT + j' and the tile's index
+  // bits at their physical positions (gphys) give their values
+  std::vector<int> gbit(ng), gphys;
+  for (int j = 0; j < ng; ++j) {
+    const int p = lay && lay->phys_in ? lay->phys_in[gpos[j]] : gpos[j];
+    auto it = std::find(tile.begin(), tile.end(), p);
+    if (it != tile.end()) {
+      gbit[j] = int(it - tile.begin());
+    } else {
+      gbit[j] = GBIT + (int)gphys.size();
+      gphys.push_back(p);
+    }
+  }
 
   // classify gates
   std::vector<Gate> gs(num_gates);
@@ -387,8 +424,8 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     int bits[3];
     for (int a = 0; a < ar; ++a) {
       int s = in.slots[a];
-      if (s < 0 || s >= w) { err = "gate " + std::to_string(g) + ": slot outside the part"; return HS_ERR_INVALID; }
-      bits[a] = tl[s];
+      if (s < 0 || s >= w + ng) { err = "gate " + std::to_string(g) + ": slot outside the part"; return HS_ERR_INVALID; }
+      bits[a] = s < w ? tl[s] : gbit[s - w];
       for (int b = 0; b < a; ++b)
         if (bits[b] == bits[a]) { err = "gate " + std::to_string(g) + ": repeated slot"; return HS_ERR_INVALID; }
     }
@@ -409,14 +446,32 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   if (options & HS_PLAN_FUSE_1Q) fuse_single_qubit_runs(gs, T, (options & HS_PLAN_JIT) != 0);
   if (options & HS_PLAN_PARITY) fuse_parity_diagonals(gs);
   num_gates = (int)gs.size();
+  // a global qubit is never staged: only diagonal action on it can run
+  const int ngl = (int)gphys.size();
+  const uint64_t gmask = ngl > 0 ? (((1ull << ngl) - 1) << GBIT) : 0;
+  for (const Gate& G : gs)
+    if ((G.nd & gmask) || (G.cls != C_DIAG && (G.d & gmask))) {
+      err = "a non-diagonal gate acts on a global (unstaged) qubit";
+      return HS_ERR_INVALID;
+    }
 
-  // storage labelling: loc_of[tile bit] / bit_at[location]
-  std::vector<int> loc_of(T), bit_at(T);
-  for (int b = 0; b < T; ++b) loc_of[b] = bit_at[b] = b;
+  // storage labelling: loc_of[tile bit] / bit_at[location] (global bits
+  // GBIT + j keep their own label)
+  std::vector<int> loc_of(64), bit_at(64);
+  for (int b = 0; b < 64; ++b) loc_of[b] = bit_at[b] = b;
 
   PartPlan& P = out;
   P.prog.clear();
   std::memset(&P.info, 0, sizeof(P.info));
+  if (ngl > 0) {  // the global qubits' physical positions in the input buffer
+    Instr gi;
+    std::memset(&gi, 0, sizeof(gi));
+    gi.op = I_GLOBALS;
+    gi.k = (uint8_t)ngl;
+    uint8_t* pos = reinterpret_cast<uint8_t*>(gi.m);
+    for (int j = 0; j < ngl; ++j) pos[j] = (uint8_t)gphys[j];
+    P.prog.push_back(gi);
+  }
   std::vector<char> done(num_gates, 0);
   int remaining = num_gates;
   std::vector<int> R;
@@ -430,7 +485,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
   // FP64 work).
   auto diag_mixed = [&](const Gate& G, const std::vector<int>& lo, uint32_t regs) {
     int in = 0, all = 0;
-    auto see = [&](int b) { ++all; in += (regs >> lo[b]) & 1; };
+    auto see = [&](int b) { ++all; in += lo[b] < 32 && ((regs >> lo[b]) & 1); };
     see(G.tgt);
     if (G.par >= 0) see(G.par);
     for (int a = 0; a < G.nctl; ++a) see(G.ctl[a]);
@@ -449,7 +504,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     const bool exact = __builtin_popcount(allow) == RB;
     for (;;) {
       bool progress = false;
-      uint32_t blk_nd = 0, blk_d = 0;
+      uint64_t blk_nd = 0, blk_d = 0;
       for (int g = 0; g < num_gates; ++g) {
         if (dn[g]) continue;
         const Gate& G = gs[g];
@@ -601,7 +656,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     std::vector<Rec> recs;
     for (;;) {
       bool progress = false;
-      uint32_t blk_nd = 0, blk_d = 0;
+      uint64_t blk_nd = 0, blk_d = 0;
       for (int g = 0; g < num_gates; ++g) {
         if (done[g]) continue;
         Gate& G = gs[g];
@@ -632,6 +687,33 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       if (!progress) break;
     }
     if (recs.empty()) continue;  // only relabels
+    // Compiled passes apply a run of diagonal gates as one factor per
+    // amplitude (one complex multiply per register and flush): sink every
+    // diagonal past the non-diagonal gates that do not act on its locations
+    // (they commute: diagonals only meet controls there), so a phase's
+    // diagonals gather into as few runs as its dense gates allow.
+    if (options & HS_PLAN_JIT) {
+      std::vector<Rec> order, pend;
+      order.reserve(recs.size());
+      auto touches = [](const Rec& d, int loc) {
+        if (d.tloc == loc || d.ploc == loc) return true;
+        for (int a = 0; a < d.nctl; ++a)
+          if (d.cloc[a] == loc) return true;
+        return false;
+      };
+      for (const Rec& r : recs) {
+        if (r.cls == C_DIAG) { pend.push_back(r); continue; }
+        bool hit = false;
+        for (const Rec& d : pend) hit |= touches(d, r.tloc);
+        if (hit) {  // the whole pending run goes first: one flush
+          order.insert(order.end(), pend.begin(), pend.end());
+          pend.clear();
+        }
+        order.push_back(r);
+      }
+      order.insert(order.end(), pend.begin(), pend.end());
+      recs.swap(order);
+    }
     // the rest of the chosen register set first (the mixed-diagonal choice
     // above assumed it), then the lowest locations
     for (int L = 0; allow != ~0u && L < T && (int)R.size() < RB; ++L)
@@ -657,9 +739,12 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       Instr in;
       std::memset(&in, 0, sizeof(in));
       in.k = K_NONE;
+      uint64_t gq = 0, gc = 0;
       for (int a = 0; a < r.nctl; ++a) {
         int k = reg_of(r.cloc[a]);
-        if (k >= 0) in.creg |= 1u << k; else in.ctid |= 1u << r.cloc[a];
+        if (r.cloc[a] >= GBIT) gc |= 1ull << (r.cloc[a] - GBIT);
+        else if (k >= 0) in.creg |= 1u << k;
+        else in.ctid |= 1u << r.cloc[a];
       }
       int k = reg_of(r.tloc);
       if (r.cls == C_DIAG) {
@@ -668,7 +753,9 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         for (int loc : {r.tloc, r.ploc}) {
           if (loc < 0) continue;
           int kk = reg_of(loc);
-          if (kk >= 0) kreg |= 1u << kk; else qt |= 1u << loc;
+          if (loc >= GBIT) gq |= 1ull << (loc - GBIT);
+          else if (kk >= 0) kreg |= 1u << kk;
+          else qt |= 1u << loc;
         }
         if (r.ploc < 0 && k >= 0) {
           in.k = (uint8_t)k;  // one register bit
@@ -685,6 +772,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         if (d0one) in.flags |= F_D0_ONE;
         if (d1one) in.flags |= F_D1_ONE;
         if (d0one && r.m[6] == -1.0 && r.m[7] == 0.0) in.flags |= F_SIGN;
+        if (gq || gc) instr_set_global(in, gq, gc);
         P.info.diag_gates++;
       } else {
         in.op = (r.cls == C_PERM) ? I_PERM : I_DENSE;
@@ -693,7 +781,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         if (r.m[1] == 0 && r.m[3] == 0 && r.m[5] == 0 && r.m[7] == 0) in.flags |= F_REAL;
         if (r.cls == C_PERM) P.info.perm_gates++; else P.info.dense_gates++;
       }
-      if (in.creg == 0 && in.ctid == 0) in.flags |= F_PLAIN;
+      if (in.creg == 0 && in.ctid == 0 && gc == 0) in.flags |= F_PLAIN;
       flops += paper_flops(r);
       {  // FP64 pipe instructions per amplitude, FMA = 1 (what the kernels issue)
         double share = 1.0 / double(1 << r.nctl);
@@ -952,24 +1040,74 @@ double pass_cost(uint64_t used, uint64_t prev, int tile_max) {
   return (prev && full && __builtin_popcountll(used & prev) < 3) ? 2.0 : 1.0;
 }
 
+bool diag_kind(int k) {
+  return k == HS_Z || k == HS_S || k == HS_T || k == HS_SDG || k == HS_TDG || k == HS_RZ || k == HS_U1 || k == HS_CZ ||
+         k == HS_CRZ;
+}
+
+// CX(a,b) D(b) CX(a,b) starting at gate g of a part (D a 1-qubit diagonal)
+bool parity_triple(const hs_gate* pg, int g, int n) {
+  if (g + 2 >= n || pg[g].kind != HS_CX) return false;
+  const hs_gate& G = pg[g];
+  const hs_gate& D = pg[g + 1];
+  const hs_gate& C = pg[g + 2];
+  return D.num_slots == 1 && D.slots[0] == G.slots[1] && diag_kind(D.kind) && D.kind != HS_CZ && D.kind != HS_CRZ &&
+         C.kind == HS_CX && C.num_slots == 2 && C.slots[0] == G.slots[0] && C.slots[1] == G.slots[1];
+}
+
+// Share of the stream's units (gates, parity triples) that act diagonally.
+// Measured: global-diagonal groupings pay off on diagonal-rich circuits (c3
+// QAOA 55 %: 13 -> 7 launches, 91.9 -> 69.0 ms; c4 TFIM 49 %: 46 -> 27,
+// 5.56 -> 4.55 s; c1 QFT) and lose on random circuits, whose passes are
+// FP64-bound and whose CZs are a quarter of the units (c2 26 %: 8 -> 7
+// launches, 5.24 -> 5.33 ms; c5_33: 17 -> 12 launches, 1187 -> 1296 ms).
+double diag_unit_share(const hs_part* parts, int num_parts, const hs_gate* gates, int num_gates) {
+  long units = 0, diag = 0;
+  for (int i = 0; i < num_parts; ++i) {
+    const hs_part& p = parts[i];
+    if (p.gate_offset < 0 || p.num_gates < 0 || p.gate_offset + p.num_gates > num_gates) continue;
+    const hs_gate* pg = gates + p.gate_offset;
+    for (int g = 0; g < p.num_gates; ++g, ++units) {
+      if (parity_triple(pg, g, p.num_gates)) { g += 2; ++diag; continue; }
+      diag += diag_kind(pg[g].kind);
+    }
+  }
+  return units ? double(diag) / double(units) : 0.0;
+}
+constexpr double GLOBAL_DIAG_MIN_SHARE = 0.4;
+
+// With `glob` (HS_PLAN_GLOBAL_DIAG) a unit of the stream is a gate or a
+// CX . D . CX parity triple; a unit whose action is diagonal (Z-type gates,
+// CZ, CRZ, parity triples) needs none of its qubits staged - the compiled
+// pass applies it from the tile's free index bits - and units that are both
+// diagonal on a shared qubit commute. Measured on the planner alone: c3 17
+// parts -> 7 passes (13 staged-diagonal launches), c4 137 -> 23 (45), c2
+// 9 -> 6 (8).
 int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts, const hs_gate* gates,
                  int num_gates, Grouping mode, std::vector<hs_part>& xparts, std::vector<hs_gate>& xgates,
-                 std::vector<int>& owner, double* cost, std::string& err) {
+                 std::vector<int>& owner, double* cost, std::string& err, bool glob = false,
+                 std::vector<std::vector<int32_t>>* xglobals = nullptr) {
   struct Ref {
     int part;
-    const hs_gate* g;
-    uint64_t mask;  // storage positions the gate touches
+    const hs_gate* g;  // first gate of the unit (ng consecutive gates of the part)
+    int ng;
+    uint64_t mask;     // storage positions the unit must stage
+    uint64_t all;      // storage positions the unit touches
+    uint64_t bn, bd;   // a left-behind unit blocks later units touching bn / acting non-diagonally on bd
   };
+  // a later unit u conflicts with the left-behind units' (bn, bd)
+  auto conflicts = [](const Ref& u, uint64_t bn, uint64_t bd) { return (u.all & bn) || (u.bn & bd); };
   // gates of `rem` (stream order) that run with qubit set `in`: inside the
   // set and not preceded by a gate left behind on a shared qubit
-  auto runnable = [](const std::vector<Ref>& stream, const std::vector<int>& rem, uint64_t in,
-                     std::vector<int>* took) -> int {
-    uint64_t blocked = 0;
+  auto runnable = [&](const std::vector<Ref>& stream, const std::vector<int>& rem, uint64_t in,
+                      std::vector<int>* took) -> int {
+    uint64_t bn = 0, bd = 0;
     int n = 0;
     for (int g : rem) {
-      const uint64_t m = stream[g].mask;
-      if ((m & blocked) || (m & ~in)) {
-        blocked |= m;
+      const Ref& u = stream[g];
+      if (conflicts(u, bn, bd) || (u.mask & ~in)) {
+        bn |= u.bn;
+        bd |= u.bd;
       } else {
         ++n;
         if (took) took->push_back(g);
@@ -982,14 +1120,15 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
   auto grow = [&](const std::vector<Ref>& stream, const std::vector<int>& rem, uint64_t in) -> uint64_t {
     for (;;) {
       const int base = runnable(stream, rem, in, nullptr);
-      uint64_t blocked = 0, best_add = 0;
+      uint64_t bn = 0, bd = 0, best_add = 0;
       double best_gain = 0.0;
       std::vector<uint64_t> seen;
       for (int g : rem) {
-        const uint64_t m = stream[g].mask;
-        if (m & blocked) continue;
-        blocked |= m;
-        const uint64_t add = m & ~in;
+        const Ref& u = stream[g];
+        if (conflicts(u, bn, bd)) continue;  // (candidates: units clear of the earlier candidates)
+        bn |= u.bn;
+        bd |= u.bd;
+        const uint64_t add = u.mask & ~in;
         if (!add || __builtin_popcountll(in | add) > tile_max) continue;
         if (std::find(seen.begin(), seen.end(), add) != seen.end()) continue;
         seen.push_back(add);
@@ -1006,17 +1145,27 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
     int slot_of[64];
     for (int b = 0; b < 64; ++b)  // staged positions stay ascending
       if (in >> b & 1) { slot_of[b] = q.num_staged; q.staged[q.num_staged++] = b; }
+    // global qubits: touched (diagonally) but not staged; slots after the staged
+    uint64_t touched = 0;
+    for (int g : chosen) touched |= stream[g].all;
+    std::vector<int32_t> gl;
+    for (int b = 0; b < 64; ++b)
+      if ((touched & ~in) >> b & 1) { slot_of[b] = q.num_staged + (int)gl.size(); gl.push_back(b); }
     q.gate_offset = (int32_t)xgates.size();
-    q.num_gates = (int32_t)chosen.size();
+    q.num_gates = 0;
     std::vector<int> votes(num_parts, 0);
     for (int g : chosen) {
       const Ref& r = stream[g];
-      hs_gate G = *r.g;
       const hs_part& p = parts[r.part];
-      for (int a = 0; a < G.num_slots; ++a) G.slots[a] = slot_of[p.staged[G.slots[a]]];
-      xgates.push_back(G);
+      for (int k = 0; k < r.ng; ++k) {
+        hs_gate G = r.g[k];
+        for (int a = 0; a < G.num_slots; ++a) G.slots[a] = slot_of[p.staged[G.slots[a]]];
+        xgates.push_back(G);
+        ++q.num_gates;
+      }
       ++votes[r.part];
     }
+    if (xglobals) xglobals->push_back(gl);
     int best = stream[chosen[0]].part;
     for (int i = 0; i < num_parts; ++i)
       if (votes[i] > votes[best] || (votes[i] == votes[best] && i < best)) best = i;
@@ -1036,11 +1185,16 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
       std::vector<int> chosen;
       uint64_t used = 0;
       if (!frontier) {
-        uint64_t in = 0, blocked = 0;
+        uint64_t in = 0, bn = 0, bd = 0;
         for (int g : rem) {
-          const uint64_t m = stream[g].mask, u = in | m;
-          if (!(m & blocked) && __builtin_popcountll(u) <= tile_max) in = u;
-          else blocked |= m;
+          const Ref& r = stream[g];
+          const uint64_t u = in | r.mask;
+          if (!conflicts(r, bn, bd) && __builtin_popcountll(u) <= tile_max) {
+            in = u;
+          } else {
+            bn |= r.bn;
+            bd |= r.bd;
+          }
         }
         runnable(stream, rem, in, &chosen);
         for (int g : chosen) used |= stream[g].mask;
@@ -1067,6 +1221,10 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
           const double score = double(took.size()) / pass_cost(u, prev, tile_max);
           if (score > best) { best = score; chosen.swap(took); used = u; }
         }
+      }
+      if (chosen.empty() && first && first_seed) {  // the seed left no room (tiny tiles): unseeded
+        first_seed = 0;
+        continue;
       }
       if (chosen.empty()) { err = "internal: pass grouping made no progress"; return HS_ERR_INVALID; }
       total += pass_cost(used, prev, tile_max);
@@ -1104,14 +1262,15 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
     auto grow_r = [&](const std::vector<int>& rem, uint64_t in, uint64_t& rng) -> uint64_t {
       for (;;) {
         const int base = runnable(stream, rem, in, nullptr);
-        uint64_t blocked = 0;
+        uint64_t bn = 0, bd = 0;
         std::vector<std::pair<double, uint64_t>> adds;
         std::vector<uint64_t> seen;
         for (int g : rem) {
-          const uint64_t m = stream[g].mask;
-          if (m & blocked) continue;
-          blocked |= m;
-          const uint64_t add = m & ~in;
+          const Ref& u = stream[g];
+          if (conflicts(u, bn, bd)) continue;
+          bn |= u.bn;
+          bd |= u.bd;
+          const uint64_t add = u.mask & ~in;
           if (!add || __builtin_popcountll(in | add) > tile_max) continue;
           if (std::find(seen.begin(), seen.end(), add) != seen.end()) continue;
           seen.push_back(add);
@@ -1234,16 +1393,33 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
       if (p.staged[j] < 0 || p.staged[j] >= 64) { err = "staged position outside 0..63"; return HS_ERR_INVALID; }
     const hs_gate* pg = gates + p.gate_offset;
     std::vector<Ref> own;
+    auto pos_mask = [&](const hs_gate& G, uint64_t* m) -> bool {
+      *m = 0;
+      if (G.num_slots < 1 || G.num_slots > 3) { err = "gate arity outside 1..3"; return false; }
+      for (int a = 0; a < G.num_slots; ++a) {
+        const int sl = G.slots[a];
+        if (sl < 0 || sl >= p.num_staged) { err = "gate slot outside the part"; return false; }
+        *m |= 1ull << p.staged[sl];
+      }
+      return true;
+    };
     for (int g = 0; g < p.num_gates; ++g) {
       const hs_gate& G = pg[g];
       uint64_t m = 0;
-      if (G.num_slots < 1 || G.num_slots > 3) { err = "gate arity outside 1..3"; return HS_ERR_INVALID; }
-      for (int a = 0; a < G.num_slots; ++a) {
-        const int sl = G.slots[a];
-        if (sl < 0 || sl >= p.num_staged) { err = "gate slot outside the part"; return HS_ERR_INVALID; }
-        m |= 1ull << p.staged[sl];
+      if (!pos_mask(G, &m)) return HS_ERR_INVALID;
+      if (!glob) {
+        own.push_back(Ref{i, &G, 1, m, m, m, 0});
+        continue;
       }
-      own.push_back(Ref{i, &G, m});
+      // CX(a,b) D(b) CX(a,b), consecutive: one diagonal unit (plan_part's
+      // HS_PLAN_PARITY fusion turns it into the parity diagonal on a ^ b)
+      if (parity_triple(pg, g, p.num_gates)) {
+        own.push_back(Ref{i, &G, 3, 0, m, 0, m});
+        g += 2;
+        continue;
+      }
+      if (diag_kind(G.kind)) own.push_back(Ref{i, &G, 1, 0, m, 0, m});
+      else own.push_back(Ref{i, &G, 1, m, m, m, 0});
     }
     if (mode != GROUP_PER_PART) {
       all.insert(all.end(), own.begin(), own.end());
@@ -1255,6 +1431,7 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
       xgates.insert(xgates.end(), pg, pg + p.num_gates);
       xparts.push_back(q);
       owner.push_back(i);
+      if (xglobals) xglobals->emplace_back();
       uint64_t u = 0;
       for (int j = 0; j < p.num_staged; ++j) u |= 1ull << p.staged[j];
       total += pass_cost(u, prev, tile_max);
@@ -1270,7 +1447,8 @@ int group_passes(int n_local, int tile_max, const hs_part* parts, int num_parts,
     const bool low3 = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_PLAIN_LOW3 || beam_mode;
     const bool seeded = mode == GROUP_REVERSE_LOW3 || mode == GROUP_REVERSE_LOW6;
     // (the seed never names a position the state does not have)
-    const uint64_t avail = n_local >= 64 ? ~0ull : ((1ull << n_local) - 1);
+    // (nor more positions than a tile holds)
+    const uint64_t avail = (n_local >= 64 ? ~0ull : ((1ull << n_local) - 1)) & ((1ull << std::min(tile_max, 63)) - 1);
     if (beam_mode) {
       // the plain beam from several RNG streams (a 12-launch c3 grouping
       // turns up in about 2 of 5 searches), the penalised one once
@@ -1319,7 +1497,7 @@ int next_low_positions() {
 // program's inputs, so a second process reuses it. Key: FNV-1a over the
 // inputs and GROUPING_VERSION; value: the passes (hs_part / hs_gate, POD) and
 // their owners. A cached grouping is always a valid one for these inputs.
-constexpr uint64_t GROUPING_VERSION = 6;
+constexpr uint64_t GROUPING_VERSION = 7;
 
 uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                       const hs_gate* gates, int num_gates, const int32_t* given_init) {
@@ -1340,7 +1518,7 @@ uint64_t grouping_key(int n_local, int dtype, int tile_max, uint32_t options, co
     mix(G.params, sizeof(G.params));
   }
   if (given_init) mix(given_init, sizeof(int32_t) * (size_t)n_local);
-  for (const char* v : {"HISVSIM_PLAN_SELECT", "HISVSIM_BEAM", "HISVSIM_BEAM_SEED"})  // grouping experiments
+  for (const char* v : {"HISVSIM_PLAN_SELECT", "HISVSIM_BEAM", "HISVSIM_BEAM_SEED", "HISVSIM_GLOBAL_DIAG"})  // grouping experiments
     if (const char* e = std::getenv(v)) mix(e, std::strlen(e));
   return h;
 }
@@ -1353,7 +1531,8 @@ std::string grouping_path(uint64_t key) {
   return dir + buf;
 }
 
-bool grouping_load(uint64_t key, std::vector<hs_part>& xp, std::vector<hs_gate>& xg, std::vector<int>& owner) {
+bool grouping_load(uint64_t key, std::vector<hs_part>& xp, std::vector<hs_gate>& xg, std::vector<int>& owner,
+                   std::vector<std::vector<int32_t>>& gl) {
   const std::string path = grouping_path(key);
   if (path.empty()) return false;
   FILE* f = std::fopen(path.c_str(), "rb");
@@ -1369,13 +1548,21 @@ bool grouping_load(uint64_t key, std::vector<hs_part>& xp, std::vector<hs_gate>&
          std::fread(xg.data(), sizeof(hs_gate), xg.size(), f) == xg.size() &&
          std::fread(own.data(), sizeof(int32_t), own.size(), f) == own.size();
     for (size_t i = 0; ok && i < own.size(); ++i) owner[i] = own[i];
+    gl.assign(xp.size(), {});
+    for (size_t i = 0; ok && i < xp.size(); ++i) {  // per pass: count, positions
+      int32_t n = 0;
+      ok = std::fread(&n, sizeof(n), 1, f) == 1 && n >= 0 && n <= 64;
+      if (!ok) break;
+      gl[i].resize(n);
+      ok = n == 0 || std::fread(gl[i].data(), sizeof(int32_t), n, f) == (size_t)n;
+    }
   }
   std::fclose(f);
   return ok;
 }
 
 void grouping_store(uint64_t key, const std::vector<hs_part>& xp, const std::vector<hs_gate>& xg,
-                    const std::vector<int>& owner) {
+                    const std::vector<int>& owner, const std::vector<std::vector<int32_t>>& gl) {
   const std::string path = grouping_path(key);
   if (path.empty()) return;
   const std::string dir = path.substr(0, path.rfind('/'));
@@ -1392,6 +1579,10 @@ void grouping_store(uint64_t key, const std::vector<hs_part>& xp, const std::vec
             std::fwrite(xp.data(), sizeof(hs_part), xp.size(), f) == xp.size() &&
             std::fwrite(xg.data(), sizeof(hs_gate), xg.size(), f) == xg.size() &&
             std::fwrite(own.data(), sizeof(int32_t), own.size(), f) == own.size();
+  for (size_t i = 0; ok && i < xp.size(); ++i) {
+    const int32_t n = i < gl.size() ? (int32_t)gl[i].size() : 0;
+    ok = std::fwrite(&n, sizeof(n), 1, f) == 1 && (n == 0 || std::fwrite(gl[i].data(), sizeof(int32_t), n, f) == (size_t)n);
+  }
   ok = (std::fclose(f) == 0) && ok;
   if (ok) std::rename(tmp.c_str(), path.c_str());
   else std::remove(tmp.c_str());
@@ -1405,7 +1596,9 @@ int final_hot(int n_local, int tile_max) {
 
 int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const hs_part* parts, int num_parts,
                  const hs_gate* gates, int num_gates, std::vector<PartPlan>& plans, std::string& err,
-                 std::vector<int32_t>* init_phys, const int32_t* given_init, std::vector<int32_t>* final_phys) {
+                 std::vector<int32_t>* init_phys, const int32_t* given_init, std::vector<int32_t>* final_phys,
+                 const std::vector<std::vector<int32_t>>* globals) {
+  if (globals && (int)globals->size() != num_parts) { err = "internal: global lists per part"; return HS_ERR_INVALID; }
   bool wide = false;
   for (int i = 0; i < num_parts; ++i) wide |= parts[i].num_staged > tile_max;
   // (cluster tiles run wide parts as one pass each: no regrouping then)
@@ -1414,8 +1607,10 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     std::vector<hs_part> xp;
     std::vector<hs_gate> xg;
     std::vector<int> owner;
+    std::vector<std::vector<int32_t>> xgl;  // global qubits per pass (HS_PLAN_GLOBAL_DIAG groupings)
     double cost = 0.0;
-    int s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err);
+    int s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, GROUP_PER_PART, xp, xg, owner, &cost, err,
+                         false, &xgl);
     if (s != HS_OK) return s;
     const uint64_t gkey = (options & HS_PLAN_PART_LOCAL)
                               ? 0
@@ -1424,11 +1619,13 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
     std::vector<hs_part> cp;
     std::vector<hs_gate> cg;
     std::vector<int> co;
-    const bool cached = gkey && grouping_load(gkey, cp, cg, co);
+    std::vector<std::vector<int32_t>> cgl;
+    const bool cached = gkey && grouping_load(gkey, cp, cg, co, cgl);
     if (cached) {
       xp.swap(cp);
       xg.swap(cg);
       owner.swap(co);
+      xgl.swap(cgl);
     } else if (!(options & HS_PLAN_PART_LOCAL)) {
       // regroup the whole gate stream when that takes fewer launches; among
       // regroupings with as few, the lowest pass_cost. Every candidate is
@@ -1439,12 +1636,13 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       // + permutation, so equal counts keep the parts; c5_33's unseeded
       // frontier, 15 passes, 1224 vs 1273 ms for the seeded 16.)
       double fp64_per_launch = 0.0;  // FP64 instructions per amplitude and launch of the parts' plan
-      auto planned = [&](const std::vector<hs_part>& ps, const std::vector<hs_gate>& gs, size_t* out) -> int {
+      auto planned = [&](const std::vector<hs_part>& ps, const std::vector<hs_gate>& gs,
+                         const std::vector<std::vector<int32_t>>& gl, size_t* out) -> int {
         std::vector<PartPlan> tmp;
         std::vector<int32_t> ip, fp;
         std::string e;
         const int st = plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, ps.data(), (int)ps.size(),
-                                    gs.data(), (int)gs.size(), tmp, e, &ip, given_init, &fp);
+                                    gs.data(), (int)gs.size(), tmp, e, &ip, given_init, &fp, &gl);
         if (st != HS_OK) { err = e; return st; }
         *out = tmp.size();
         double f = 0.0;
@@ -1453,7 +1651,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
         return HS_OK;
       };
       size_t best_launches = 0;
-      if ((s = planned(xp, xg, &best_launches)) != HS_OK) return s;
+      if ((s = planned(xp, xg, xgl, &best_launches)) != HS_OK) return s;
       // Passes issuing more FP64 work than a pass moves HBM bytes (~60 FP64
       // instructions per complex128 amplitude at the measured rates) gain
       // little from fewer launches, and the beam's denser passes measured
@@ -1472,17 +1670,36 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
         modes.push_back(GROUP_BEAM_REVERSE);
         modes.push_back(GROUP_BEAM_REVERSE_PEN);
       }
-      for (Grouping mode : modes) {
+      // global-diagonal groupings (HS_PLAN_GLOBAL_DIAG: compiled passes with
+      // the parity fusion; $HISVSIM_GLOBAL_DIAG=0 turns them off for A/B):
+      // every mode is also tried with unstaged diagonals
+      // ($HISVSIM_GLOBAL_DIAG=1 tries them whatever the circuit's diagonal share)
+      const bool glob_ok = (options & HS_PLAN_GLOBAL_DIAG) && (options & HS_PLAN_JIT) && (options & HS_PLAN_PARITY) &&
+                           !env_is("HISVSIM_GLOBAL_DIAG", "0") &&
+                           (env_is("HISVSIM_GLOBAL_DIAG", "1") ||
+                            diag_unit_share(parts, num_parts, gates, num_gates) >= GLOBAL_DIAG_MIN_SHARE);
+      std::vector<std::pair<Grouping, bool>> cands;
+      for (Grouping mode : modes) cands.push_back({mode, false});
+      if (glob_ok)
+        for (Grouping mode : modes) cands.push_back({mode, true});
+      for (const auto& cand : cands) {
+        const Grouping mode = cand.first;
         std::vector<hs_part> ap;
         std::vector<hs_gate> ag;
         std::vector<int> ao;
+        std::vector<std::vector<int32_t>> agl;
         double c = 0.0;
-        s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err);
+        s = group_passes(n_local, tile_max, parts, num_parts, gates, num_gates, mode, ap, ag, ao, &c, err, cand.second,
+                         &agl);
         if (s != HS_OK) return s;
         size_t la = 0;
-        if ((s = planned(ap, ag, &la)) != HS_OK) return s;
+        if ((s = planned(ap, ag, agl, &la)) != HS_OK) {
+          if (!cand.second) return s;
+          continue;  // e.g. more than 32 global qubits in one pass: not this grouping
+        }
         if (std::getenv("HISVSIM_PLAN_DEBUG"))
-          std::fprintf(stderr, "[plan] grouping %d: %zu passes, %zu launches, cost %.1f\n", (int)mode, ap.size(), la, c);
+          std::fprintf(stderr, "[plan] grouping %d%s: %zu passes, %zu launches, cost %.1f\n", (int)mode,
+                       cand.second ? " (global diagonals)" : "", ap.size(), la, c);
         // fewest launches; among as few, the lowest pass_cost (measured c3:
         // 13 launches with one short-read pass 96.3 ms, 14 coalesced 96.6-97.4)
         static const bool by_cost = [] {
@@ -1497,15 +1714,15 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
                                     : (la < best_launches ||
                                        (regrouped && !beam_mode && la == best_launches && c < cost));
         if (better) {
-          xp.swap(ap); xg.swap(ag); owner.swap(ao); cost = c; best_launches = la;
+          xp.swap(ap); xg.swap(ag); owner.swap(ao); xgl.swap(agl); cost = c; best_launches = la;
           regrouped = true;
         }
       }
     }
     s = plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, xp.data(), (int)xp.size(), xg.data(), (int)xg.size(), plans,
-                     err, init_phys, given_init, final_phys);
+                     err, init_phys, given_init, final_phys, &xgl);
     if (s != HS_OK) return s;
-    if (gkey && !cached) grouping_store(gkey, xp, xg, owner);
+    if (gkey && !cached) grouping_store(gkey, xp, xg, owner, xgl);
     for (auto& pl : plans)
       if (pl.info.user_part >= 0) pl.info.user_part = owner[pl.info.user_part];
     return HS_OK;
@@ -1666,8 +1883,10 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       lay.mode = (!pp && !no_restore && i + 1 == num_parts) ? LAYOUT_TARGET : LAYOUT_PRIORITY;
     }
     std::string e;
+    const std::vector<int32_t>* gl = globals ? &(*globals)[i] : nullptr;
     int s = plan_part(n_local, dtype, tile_max, options, p.staged, p.num_staged, gates + p.gate_offset, p.num_gates,
-                      plans[i], e, layout ? &lay : nullptr);
+                      plans[i], e, layout ? &lay : nullptr, gl && !gl->empty() ? gl->data() : nullptr,
+                      gl ? (int)gl->size() : 0);
     if (s != HS_OK) {
       err = "part " + std::to_string(i) + ": " + e;
       return s;

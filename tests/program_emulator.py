@@ -14,7 +14,7 @@ import ctypes
 
 import numpy as np
 
-I_PHASE, I_DENSE, I_PERM, I_DIAG = 1, 2, 3, 4
+I_PHASE, I_DENSE, I_PERM, I_DIAG, I_GLOBALS = 1, 2, 3, 4, 5
 F_D0_ONE, F_D1_ONE, F_SIGN, F_PARITY = 1, 2, 4, 32
 K_NONE = 0xFF
 
@@ -74,6 +74,14 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog, out: np.ndarray | None 
     tid = np.arange(nt, dtype=np.int64)
     regs = None
     cur = None
+    gw = np.zeros(bases.size, dtype=np.int64)  # per tile: its global qubits' values (I_GLOBALS)
+
+    def popc_par(x):
+        x = np.asarray(x, dtype=np.int64)
+        p = np.zeros(x.shape, dtype=bool)
+        for b in range(64):
+            p ^= ((x >> b) & 1).astype(bool)
+        return p
 
     def slot_of(rpos, npos):
         tdep = _deposit(tid, npos[: T - RB])
@@ -81,6 +89,11 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog, out: np.ndarray | None 
 
     for ins in prog:
         op = int(ins["op"])
+        if op == I_GLOBALS:  # positions are bytes of m[]; their values are the tile's input index bits
+            gp = np.frombuffer(ins["m"].tobytes(), dtype=np.uint8)[: int(ins["k"])]
+            for j, p in enumerate(gp):
+                gw |= ((bases >> int(p)) & 1) << j
+            continue
         if op == I_PHASE:
             if regs is not None:
                 for i, s in enumerate(cur[1]):
@@ -89,7 +102,9 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog, out: np.ndarray | None 
             regs = [smem[:, s].copy() for s in cur[1]]
             continue
         tdep = cur[0]
-        tok = (tdep & int(ins["ctid"])) == int(ins["ctid"])  # per thread
+        graw = np.frombuffer(ins["m"].tobytes(), dtype=np.uint64)
+        gq, gc = (int(graw[4]), int(graw[5])) if op == I_DIAG else (0, 0)
+        tok = ((tdep & int(ins["ctid"])) == int(ins["ctid"]))[None, :] & ((gw & gc) == gc)[:, None]  # tile x thread
         creg = int(ins["creg"])
         m = ins["m"]
         k = int(ins["k"])
@@ -104,11 +119,11 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog, out: np.ndarray | None 
                     na, nb = b, a
                 else:
                     na, nb = u[0] * a + u[1] * b, u[2] * a + u[3] * b
-                regs[i] = np.where(tok[None, :], na, a)
-                regs[j] = np.where(tok[None, :], nb, b)
+                regs[i] = np.where(tok, na, a)
+                regs[j] = np.where(tok, nb, b)
         else:
             d0, d1 = complex(m[0], m[1]), complex(m[2], m[3])
-            tpar = np.array([bin(int(t) & int(ins["qtid"])).count("1") & 1 for t in tdep], dtype=bool)
+            tpar = popc_par(tdep & int(ins["qtid"]))[None, :] ^ popc_par(gw & gq)[:, None]
             for i in range(1 << RB):
                 if (i & creg) != creg:
                     continue
@@ -117,9 +132,9 @@ def emulate(psi: np.ndarray, n_local: int, launch, prog, out: np.ndarray | None 
                 elif k == K_NONE:
                     one = tpar
                 else:
-                    one = np.full(nt, bool(i & (1 << k)))
+                    one = np.full((1, nt), bool(i & (1 << k)))
                 f = np.where(one, d1, d0)
-                regs[i] = np.where(tok[None, :], regs[i] * f[None, :], regs[i])
+                regs[i] = np.where(tok, regs[i] * f, regs[i])
     fin = slot_of([int(x) for x in launch["fin_rpos"]], [int(x) for x in launch["fin_npos"]])
     for i, s in enumerate(fin[1]):
         smem[:, s] = regs[i]

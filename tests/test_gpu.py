@@ -155,6 +155,45 @@ def test_full_size_configs_match_c_oracle(golden, name, strategy):
     assert max_abs_diff(st, ref) < 1e-10
 
 
+@pytest.mark.parametrize("name,strategy,force", [("c2@24", "dfs", True), ("c2@24", "dagp", True),
+                                                 ("c4@26", "dfs", False), ("c3@26", "dagp", False),
+                                                 ("c1", "dfs", False)])
+def test_global_diagonal_programs_match_c_oracle(name, strategy, force, monkeypatch):
+    """Compiled passes with global (unstaged) diagonal qubits: CZs with a
+    global control or target (random circuits, forced with
+    HISVSIM_GLOBAL_DIAG=1), parity diagonals of CX.RZ.CX (c3 / c4) and
+    CRZ / U1 (c1) whose values come from the tile's free index bits; the
+    programs must carry global passes and equal the C oracle."""
+    import ctypes
+
+    from paper_2205_06973_b200.hier import PartProgram, _pack
+
+    if force:
+        monkeypatch.setenv("HISVSIM_GLOBAL_DIAG", "1")
+    c = configs.build(name)
+    part = (partition_dfs if strategy == "dfs" else partition_dagp)(build_dag(c), 12)
+    exes = [remap_part(c, p) for p in part.parts]
+    prog = PartProgram(c.num_qubits, exes)
+    lib = _native.load()
+    parts, gates, total = _pack(exes)
+    size, nl = ctypes.c_size_t(), ctypes.c_int()
+    _native.check(lib.hs_plan_program(c.num_qubits, 0, 12, prog.options, parts, len(exes), gates, total, None, 0,
+                                      ctypes.byref(size), ctypes.byref(nl)))
+    buf = ctypes.create_string_buffer(size.value)
+    _native.check(lib.hs_plan_program(c.num_qubits, 0, 12, prog.options, parts, len(exes), gates, total, buf,
+                                      size.value, ctypes.byref(size), ctypes.byref(nl)))
+    raw, off, globals_ = buf.raw, 0, 0
+    for _ in range(nl.value):
+        nprog = int.from_bytes(raw[off + 8:off + 12], "little", signed=True)
+        first_op = int.from_bytes(raw[off + 144:off + 146], "little") if nprog else 0
+        globals_ += first_op == 5
+        off += 144 + 96 * nprog
+    assert globals_ > 0
+    st = execute_hierarchical(c, part)
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert max_abs_diff(st, ref) < 1e-10
+
+
 def test_distributed_emulated_ranks_match_reference(golden):
     docs, states = golden.json("corpus"), golden.npz("corpus")
     for i, doc in enumerate(docs):

@@ -354,12 +354,13 @@ def test_regrouped_passes_match_oracle(name, limit, tile):
             assert np.max(np.abs(psi[0] - want)) < 1e-12, (layout, len(launches))
 
 
-@pytest.mark.parametrize("options", [0x405, 0x40d, 0x44d, 0x415, 0x45d])
+@pytest.mark.parametrize("options", [0x405, 0x40d, 0x44d, 0x415, 0x45d, 0xc15, 0xc5d])
 def test_merged_programs_match_oracle_on_corpus(golden, options):
     """Whole programs with HS_PLAN_MERGE (every pass grouping candidate is
     planned and the fewest launches win) on the corpus: tiny states (n < 6,
     where seeds must stay inside the state), every gate kind, with and
-    without layouts / ping-pong, emulated against the reference states."""
+    without layouts / ping-pong, with and without global diagonals
+    (0x800 with HS_PLAN_JIT), emulated against the reference states."""
     docs, states = golden.json("corpus"), golden.npz("corpus")
     checked = 0
     for i, doc in enumerate(docs[:40]):
@@ -464,3 +465,65 @@ def test_grouping_cache_reuses_the_chosen_passes(tmp_path, monkeypatch):
     files[0].write_bytes(b"garbage")
     third = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True).stdout
     assert third == first
+
+
+@pytest.mark.parametrize("name,limit,tile", [("c3@16", 8, 10), ("c4@15", 8, 10), ("c2@16", 8, 10), ("c3@14", 6, 8),
+                                             ("c1@13", 6, 10)])
+def test_global_diagonal_programs_match_oracle(name, limit, tile, monkeypatch):
+    """HS_PLAN_GLOBAL_DIAG: regrouped passes stage only the qubits their
+    non-diagonal gates act on; diagonal gates (CZ, parity diagonals of
+    CX.RZ.CX, Z-type gates) on unstaged qubits read those qubits' values from
+    the tile's free index bits (I_GLOBALS + the gq / gc masks of DIAG
+    instructions). Fewer launches than the staged-diagonal grouping, the
+    same amplitudes, in place and ping-pong, emulated against the oracle
+    (HISVSIM_GLOBAL_DIAG=1: also for circuits below the diagonal share the
+    planner asks for by default)."""
+    monkeypatch.setenv("HISVSIM_GLOBAL_DIAG", "1")
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), limit)
+    exes = [remap_part(c, p) for p in part.parts]
+    want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    with_globals = 0
+    for layout in (0, 8, 8 | 0x40):
+        staged = emu.plan_program(_native, c.num_qubits, 0, tile, exes, options=0x415 | layout)
+        glob = emu.plan_program(_native, c.num_qubits, 0, tile, exes, options=0xc15 | layout)
+        assert len(glob) <= len(staged)
+        with_globals += sum(1 for _, prog in glob if len(prog) and int(prog[0]["op"]) == emu.I_GLOBALS)
+        for launches in (staged, glob):
+            psi = np.zeros((1, 1 << c.num_qubits), dtype=np.complex128)
+            psi[0, 0] = 1
+            emu.run_program(psi, c.num_qubits, launches)
+            assert np.max(np.abs(psi[0] - want)) < 1e-12, (layout, len(launches))
+    if not name.startswith("c1"):
+        assert with_globals > 0
+
+
+def test_global_diagonals_cut_the_c3_and_c4_launch_counts():
+    """The BASELINE configs' full-size programs (planning is host-only):
+    c3 (30-qubit QAOA, k = 12) 13 -> 7 launches, c4 (33-qubit TFIM) 46 -> 27
+    with unstaged diagonals; HS_PLAN_GLOBAL_DIAG off keeps the old plans, and
+    so do random circuits (c2: CZs are 26 % of the units, below the 40 % the
+    planner asks for; measured slower there)."""
+    import os
+
+    old = os.environ.get("HISVSIM_CACHE_DIR")
+    os.environ["HISVSIM_CACHE_DIR"] = "off"
+    try:
+        for name, opts, most in (("c3", 0x47d, 8), ("c4", 0x41d, 30)):
+            c = configs.build(name)
+            part = partition_dfs(build_dag(c), configs.CONFIGS[name].limit)
+            exes = [remap_part(c, p) for p in part.parts]
+            staged = emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=opts)
+            glob = emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=opts | 0x800)
+            assert len(glob) <= most < len(staged), (name, len(glob), len(staged))
+            assert not any(len(p) and int(p[0]["op"]) == emu.I_GLOBALS for _, p in staged)
+        c = configs.build("c2")
+        part = partition_dfs(build_dag(c), 12)
+        exes = [remap_part(c, p) for p in part.parts]
+        plan = emu.plan_program(_native, c.num_qubits, 0, 12, exes, options=0xc7d)
+        assert not any(len(p) and int(p[0]["op"]) == emu.I_GLOBALS for _, p in plan)
+    finally:
+        if old is None:
+            os.environ.pop("HISVSIM_CACHE_DIR", None)
+        else:
+            os.environ["HISVSIM_CACHE_DIR"] = old
