@@ -3,12 +3,13 @@
 One step = one full simulation of the BASELINE config circuit on a state
 already resident in HBM: every tile pass the planner made of the
 partition's parts (csrc/hs_planner.cpp group_passes), plus any gate-free
-layout launch. ``value`` = HBM bytes the step's launches move (each launch
+layout launch. ``value`` = the reference's work per circuit - every part of
+the partition updates every amplitude once (parts x 2^n amplitude updates,
+summed over ranks) - / time-to-solution: the same count on the reference
+arm, whatever number of launches the engine groups the parts into.
+``hbm_gbs_moved`` = HBM bytes the step's launches actually move (each launch
 reads and writes every amplitude of a rank's shard: 2 x 2^l x 16 B) / step
-time, summed over ranks, so it can never exceed the HBM peak; the metric's
-per-part-pass figure (parts x 2 x 2^l x 16 B / time, a time-to-solution in
-bandwidth units, comparable with the reference arm) is reported beside it
-as ``part_pass_equivalent_gbs``. ``ms_per_step`` is the circuit
+time, never above the HBM peak; ``roofline`` explains it per launch. ``ms_per_step`` is the circuit
 time-to-solution; partitioning and planning (host) are reported
 separately. ``e2e`` is the same metric through the public API with the
 initial state in pinned host memory and the final state read back every
@@ -41,7 +42,14 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "circuit time-to-solution and effective HBM GB/s per part-pass at 1/2/4/8 B200"
-UNIT = "GB/s"
+#: The reference's unit of work: one part updates every amplitude of the
+#: state once (its gather -> gates -> scatter pass, hier.py:220-244).
+#: value = parts x 2^n amplitude updates (all ranks) / time-to-solution; it
+#: counts the same work on both arms however the engine groups the parts
+#: into launches. HBM bytes the launches actually move are reported beside
+#: it (hbm_gbs_moved, never above the HBM peak) and in `roofline`.
+UNIT = "G part-amplitude updates/s"
+AMP_BYTES_PER_UPDATE = 32  # one read + one write of a complex128 amplitude
 
 
 def _peaks():
@@ -214,18 +222,19 @@ def cpu_arm(args, cfg, circuit, part, t_part, steps, warmup):
     for _ in range(steps):
         nbytes += step()
     dt = time.perf_counter() - t0
-    value = nbytes / dt / 1e9
+    gbs = nbytes / dt / 1e9
+    value = gbs / AMP_BYTES_PER_UPDATE  # G amplitude updates / s
     sample_amps = sum(k << len(pos) for pos, _, _, k in plan)
     sample = (("" if n == circuit.num_qubits else
                f"state squeezed to {n} of {circuit.num_qubits} qubits to fit the host (parts' positions "
                f"compressed onto the lowest qubits); ") +
               f"{config_label(args)}: each step runs every one of the {len(plan)} parts over "
               f"{sample_amps / (1 << n) / len(plan):.4%} of its fixings ({sample_amps} amplitude updates "
-              f"per step, fixings 0..k-1 of each part) with {threads} threads; GB/s = 2 x 16 B x "
-              f"amplitudes / time, the same algorithmic count as the GPU arm")
-    full_s = (len(plan) * (1 << n) * 32) / (value * 1e9)
+              f"per step, fixings 0..k-1 of each part) with {threads} threads; value = amplitude updates / "
+              f"time, the same count as the GPU arm (gbs = 2 x 16 B per update)")
+    full_s = (len(plan) * (1 << n)) / (value * 1e9)
     return {
-        "value": value, "threads": threads, "sample": sample, "ms_per_step": dt / steps * 1e3,
+        "value": value, "gbs": gbs, "threads": threads, "sample": sample, "ms_per_step": dt / steps * 1e3,
         "projected_time_to_solution_s": full_s,
     }
 
@@ -446,7 +455,9 @@ def gpu_arm(args, circuit, part, rank, world):
         total_ms = float(t.item())
     ms_step = total_ms / args.steps
     moved = world * num_launches * bytes_per_pass  # HBM bytes of all ranks' launches per step
-    value = moved / (ms_step / 1e3) / 1e9
+    hbm_gbs = moved / (ms_step / 1e3) / 1e9
+    part_amps = world * num_parts * (1 << n_local)  # the reference's work: every part updates every amplitude
+    value = part_amps / (ms_step / 1e3) / 1e9
 
     # the literal reference granularity: one pass per part (no merging or
     # regrouping of parts into tile passes), same layouts / JIT / graph
@@ -462,8 +473,8 @@ def gpu_arm(args, circuit, part, rank, world):
         lit_ms = _time_program(lit, state, args.steps, lambda b: launch(b, lit), stream)
         nl = lit.program.num_launches
         literal = {"ms_per_step": lit_ms, "launches_per_step": nl, "parts": num_parts,
-                   "value": nl * bytes_per_pass / (lit_ms / 1e3) / 1e9, "unit": UNIT,
-                   "part_pass_equivalent_gbs": num_parts * bytes_per_pass / (lit_ms / 1e3) / 1e9,
+                   "value": num_parts * (1 << n_local) / (lit_ms / 1e3) / 1e9, "unit": UNIT,
+                   "hbm_gbs_moved": nl * bytes_per_pass / (lit_ms / 1e3) / 1e9,
                    "options": hex(opts),
                    "note": "HS_PLAN_PART_LOCAL without HS_PLAN_MERGE: every launch carries one part's gates "
                            "(plus gate-free layout launches); the default regroups parts into tile passes"}
@@ -509,8 +520,8 @@ def gpu_arm(args, circuit, part, rank, world):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e_ms = float(t.item())
         nl_e2e = sum(pr.num_launches for pr in run_e2e.programs if pr is not None)
-        e2e = {"value": world * nl_e2e * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
-               "part_pass_equivalent_gbs": world * num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9,
+        e2e = {"value": world * num_parts * (1 << n_local) / (e_ms / 1e3) / 1e9, "unit": UNIT,
+               "hbm_gbs_moved": world * nl_e2e * bytes_per_pass / (e_ms / 1e3) / 1e9,
                "launches_per_step": nl_e2e, "ms_per_step": e_ms,
                "h2d_bytes_per_step": world * (1 << n_local) * 16, "d2h_bytes_per_step": world * (1 << n_local) * 16,
                "path": "public API ShardedRun.run per rank: shard uploaded from pinned host, every part and "
@@ -550,8 +561,8 @@ def gpu_arm(args, circuit, part, rank, world):
             e_ms = e0.elapsed_time(e1) / args.steps
             assert abs(float(host_out.abs().pow(2).sum()) - 1.0) < 1e-9
             nl_e2e = run_e2e.program.num_launches
-            e2e = {"value": nl_e2e * bytes_per_pass / (e_ms / 1e3) / 1e9, "unit": UNIT,
-                   "part_pass_equivalent_gbs": num_parts * bytes_per_pass / (e_ms / 1e3) / 1e9,
+            e2e = {"value": num_parts * (1 << n_local) / (e_ms / 1e3) / 1e9, "unit": UNIT,
+                   "hbm_gbs_moved": nl_e2e * bytes_per_pass / (e_ms / 1e3) / 1e9,
                    "launches_per_step": nl_e2e, "ms_per_step": e_ms, "h2d_bytes_per_step": shard_bytes,
                    "d2h_bytes_per_step": shard_bytes,
                    "path": "public API HierarchicalRun.run_stream: each step uploads an initial state from pinned "
@@ -594,7 +605,7 @@ def gpu_arm(args, circuit, part, rank, world):
             if r_ is not None:
                 r_.release()
     return {
-        "ms_step": ms_step, "value": value, "moved": moved, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
+        "ms_step": ms_step, "value": value, "hbm_gbs": hbm_gbs, "moved": moved, "durations_ms": durs, "bytes_per_pass": bytes_per_pass,
         "launch_ms": [sum(c) / len(c) for c in zip(*launch_ms)] if launch_ms else [],
         "num_parts": num_parts, "clocks": clk, "e2e": e2e, "info": info, "n_local": n_local,
         "num_launches": num_launches, "restore_ms_per_step": restore_ms / n_marked if n_marked else 0.0,
@@ -679,9 +690,10 @@ def main(argv=None):
                 "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator)",
                 "config": config, "impl": "reference",
                 "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
-                                 "sample": r["sample"], "numpy_port_c1_seconds": np_c1},
+                                 "sample": r["sample"], "numpy_port_c1_seconds": np_c1, "gbs": r["gbs"]},
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "part_pass_equivalent_gbs": r["value"],
+                "value_definition": "amplitude updates (2 x 16 B each) / time on the sampled fixings",
+                "hbm_gbs_moved": r["gbs"],
                 "projected_time_to_solution_s": r["projected_time_to_solution_s"],
                 "host_seconds": {"partition": round(t_part, 4)},
                 "note": "host CPU, rank 0 only: the C restatement of the reference's per-part gather/gates/scatter "
@@ -732,15 +744,18 @@ def main(argv=None):
         roofline["binding"] = {"what": "sum over launches of max(HBM bytes / peak, FP64 instructions / measured DFMA rate)",
                                "bound_ms_per_step": bind_ms, "measured_ms_per_step": g["ms_step"],
                                "frac": bind_ms / g["ms_step"]}
-    pp_equiv = world * g["num_parts"] * g["bytes_per_pass"] / (g["ms_step"] / 1e3) / 1e9
     line = {"metric": METRIC, "value": g["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": g["ms_step"], "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
             "config": config,
             "launch": ("per-kernel" if (args.no_graph or world > 1) else "one CUDA graph per step (PartProgram.run_graph)"),
             "plan_add": hex(args.plan_add),
-            "value_definition": "HBM bytes moved per step (launches x 2 x 2^l x 16 B, all ranks) / device step time",
-            "part_pass_equivalent_gbs": pp_equiv,
+            "value_definition": "reference work rate: parts x 2^n amplitude updates per circuit (every part of the "
+                                "reference partition updates every amplitude once; all ranks) / device time-to-solution "
+                                "of the circuit",
+            "hbm_gbs_moved": g["hbm_gbs"],
+            "hbm_gbs_moved_definition": "HBM bytes the launches move (launches x 2 x 2^l x 16 B, all ranks) / step time; "
+                                        "never above the HBM peak",
             "roofline": roofline, "clocks": g["clocks"],
             "gpu_launches": args.steps * g["num_launches"],
             "layout_restore_ms_per_step": g["restore_ms_per_step"],
@@ -760,7 +775,8 @@ def main(argv=None):
     if not args.no_cpu_baseline and world == 1:
         r = cpu_arm(args, cfg, circuit, part, t_part, 2, 1)
         line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "port",
-                                "sample": r["sample"], "numpy_port_c1_seconds": numpy_port_c1_seconds()}
+                                "sample": r["sample"], "numpy_port_c1_seconds": numpy_port_c1_seconds(),
+                                "gbs": r["gbs"]}
     print(json.dumps(line), flush=True)
     return 0
 
