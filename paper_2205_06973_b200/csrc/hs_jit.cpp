@@ -359,26 +359,43 @@ struct Gen {
           << "; " << i << " = x * " << ui << " + y * " << ur << "; }\n";
       }
     }
-    for (int i = 0; i < nreg; ++i) {
-      std::string fr, fi;
-      o << "      {";
-      for (size_t gi = 0; gi < masks.size(); ++gi) {
-        const int par = __builtin_popcount(uint32_t(i) & masks[gi]) & 1;
-        const std::string r = M + std::to_string(gi) + "r" + std::to_string(par);
-        const std::string im_ = M + std::to_string(gi) + "i" + std::to_string(par);
-        if (gi == 0) {
-          o << " " << T << " fr = " << r << ", fi = " << im_ << ";";
-        } else {
-          o << " { const " << T << " x = fr, y = fi; fr = x * " << r << " - y * " << im_ << "; fi = x * " << im_
-            << " + y * " << r << "; }";
-          cat[3] += 4 * wgt; ops += 4 * wgt;
+    // registers sharing a factor (the same group parities) back to back:
+    // the factor of a parity signature is built once per thread (G - 1
+    // complex multiplies per distinct signature, not per register)
+    std::vector<int> reg_order(nreg);
+    for (int i = 0; i < nreg; ++i) reg_order[i] = i;
+    auto signature = [&](int i) {
+      int sig = 0;
+      for (size_t gi = 0; gi < masks.size(); ++gi) sig |= (__builtin_popcount(uint32_t(i) & masks[gi]) & 1) << gi;
+      return sig;
+    };
+    std::stable_sort(reg_order.begin(), reg_order.end(), [&](int x, int y) { return signature(x) < signature(y); });
+    int cur_sig = -1;
+    for (int i : reg_order) {
+      const int sig = signature(i);
+      if (sig != cur_sig) {
+        if (cur_sig >= 0) o << "      }\n";
+        cur_sig = sig;
+        o << "      {";
+        for (size_t gi = 0; gi < masks.size(); ++gi) {
+          const int par = sig >> gi & 1;
+          const std::string r = M + std::to_string(gi) + "r" + std::to_string(par);
+          const std::string im_ = M + std::to_string(gi) + "i" + std::to_string(par);
+          if (gi == 0) {
+            o << " " << T << " fr = " << r << ", fi = " << im_ << ";";
+          } else {
+            o << " { const " << T << " x = fr, y = fi; fr = x * " << r << " - y * " << im_ << "; fi = x * " << im_
+              << " + y * " << r << "; }";
+            cat[3] += 4.0; ops += 4.0;  // per thread, not per amplitude
+          }
         }
+        o << "\n";
       }
-      o << "\n  ";
+      o << "  ";
       cmul_const(i, cre[i], cim[i]);
       cmul_into(i, "fr", "fi");
-      o << "      }\n";
     }
+    if (cur_sig >= 0) o << "      }\n";
     o << "    }\n";
   }
   // final: fold the part's scalar S into the run and apply it (no

@@ -618,6 +618,70 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     for (int g = 0; g < num_gates; ++g) c += !done[g] && gs[g].cls != C_DIAG && gs[g].cls != C_SWAP;
     return c;
   };
+  // one scheduled gate as a device instruction of the phase whose register
+  // locations are R_last
+  std::vector<int> R_last;
+  std::vector<Rec> carry;  // diagonals deferred to the next phase
+  auto to_instr = [&](const Rec& r) -> Instr {
+    auto reg_of = [&](int L) -> int {
+      for (int k = 0; k < (int)R_last.size(); ++k) if (R_last[k] == L) return k;
+      return -1;
+    };
+    Instr in;
+    std::memset(&in, 0, sizeof(in));
+    in.k = K_NONE;
+    uint64_t gq = 0, gc = 0;
+    for (int a = 0; a < r.nctl; ++a) {
+      int k = reg_of(r.cloc[a]);
+      if (r.cloc[a] >= GBIT) gc |= 1ull << (r.cloc[a] - GBIT);
+      else if (k >= 0) in.creg |= 1u << k;
+      else in.ctid |= 1u << r.cloc[a];
+    }
+    int k = reg_of(r.tloc);
+    if (r.cls == C_DIAG) {
+      in.op = I_DIAG;
+      uint32_t kreg = 0, qt = 0;
+      for (int loc : {r.tloc, r.ploc}) {
+        if (loc < 0) continue;
+        int kk = reg_of(loc);
+        if (loc >= GBIT) gq |= 1ull << (loc - GBIT);
+        else if (kk >= 0) kreg |= 1u << kk;
+        else qt |= 1u << loc;
+      }
+      if (r.ploc < 0 && k >= 0) {
+        in.k = (uint8_t)k;  // one register bit
+      } else if (kreg == 0) {
+        in.qtid = qt;       // parity of thread bits: uniform per thread
+      } else {
+        in.flags |= F_PARITY;
+        in.rpos[0] = (uint8_t)kreg;
+        in.qtid = qt;
+      }
+      in.m[0] = r.m[0]; in.m[1] = r.m[1]; in.m[2] = r.m[6]; in.m[3] = r.m[7];
+      bool d0one = r.m[0] == 1.0 && r.m[1] == 0.0;
+      bool d1one = r.m[6] == 1.0 && r.m[7] == 0.0;
+      if (d0one) in.flags |= F_D0_ONE;
+      if (d1one) in.flags |= F_D1_ONE;
+      if (d0one && r.m[6] == -1.0 && r.m[7] == 0.0) in.flags |= F_SIGN;
+      if (gq || gc) instr_set_global(in, gq, gc);
+      P.info.diag_gates++;
+    } else {
+      in.op = (r.cls == C_PERM) ? I_PERM : I_DENSE;
+      in.k = (uint8_t)k;  // target is a register bit by construction
+      std::memcpy(in.m, r.m, sizeof(in.m));
+      if (r.m[1] == 0 && r.m[3] == 0 && r.m[5] == 0 && r.m[7] == 0) in.flags |= F_REAL;
+      if (r.cls == C_PERM) P.info.perm_gates++; else P.info.dense_gates++;
+    }
+    if (in.creg == 0 && in.ctid == 0 && gc == 0) in.flags |= F_PLAIN;
+    flops += paper_flops(r);
+    {  // FP64 pipe instructions per amplitude, FMA = 1 (what the kernels issue)
+      double share = 1.0 / double(1 << r.nctl);
+      if (in.op == I_DENSE) fp64 += share * ((in.flags & F_REAL) ? 4.0 : 8.0);
+      if (in.op == I_DIAG && !(in.flags & F_SIGN))
+        fp64 += share * (((in.flags & (F_D0_ONE | F_D1_ONE)) && !(in.flags & F_PARITY)) ? 2.0 : 4.0);
+    }
+    return in;
+  };
   while (remaining > 0) {
     R.clear();
     // compiled parts pay a shared-memory exchange per phase: pick the
@@ -686,6 +750,12 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
       }
       if (!progress) break;
     }
+    // diagonals deferred by the previous phase come first (sinking below
+    // moves them past this phase's dense gates where they commute)
+    if (!carry.empty()) {
+      recs.insert(recs.begin(), carry.begin(), carry.end());
+      carry.clear();
+    }
     if (recs.empty()) continue;  // only relabels
     // Compiled passes apply a run of diagonal gates as one factor per
     // amplitude (one complex multiply per register and flush): sink every
@@ -693,26 +763,89 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     // (they commute: diagonals only meet controls there), so a phase's
     // diagonals gather into as few runs as its dense gates allow.
     if (options & HS_PLAN_JIT) {
-      std::vector<Rec> order, pend;
-      order.reserve(recs.size());
-      auto touches = [](const Rec& d, int loc) {
-        if (d.tloc == loc || d.ploc == loc) return true;
-        for (int a = 0; a < d.nctl; ++a)
-          if (d.cloc[a] == loc) return true;
-        return false;
-      };
-      for (const Rec& r : recs) {
-        if (r.cls == C_DIAG) { pend.push_back(r); continue; }
-        bool hit = false;
-        for (const Rec& d : pend) hit |= touches(d, r.tloc);
-        if (hit) {  // the whole pending run goes first: one flush
-          order.insert(order.end(), pend.begin(), pend.end());
-          pend.clear();
+      // list schedule: run every dense gate whose predecessors are done (a
+      // diagonal predecessor must have been applied, i.e. flushed); gather
+      // every diagonal whose dense predecessors ran into the pending run;
+      // flush the run only when no dense gate can go on without it
+      const int n = (int)recs.size();
+      std::vector<uint64_t> ndm(n), dm(n);
+      for (int i = 0; i < n; ++i) {
+        const Rec& r = recs[i];
+        uint64_t c = 0;
+        for (int a = 0; a < r.nctl; ++a) c |= 1ull << r.cloc[a];
+        if (r.cls == C_DIAG) {
+          ndm[i] = 0;
+          dm[i] = c | (1ull << r.tloc) | (r.ploc >= 0 ? 1ull << r.ploc : 0ull);
+        } else {
+          ndm[i] = 1ull << r.tloc;
+          dm[i] = c;
         }
-        order.push_back(r);
       }
-      order.insert(order.end(), pend.begin(), pend.end());
+      std::vector<std::vector<int>> preds(n);
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < j; ++i)
+          if ((ndm[i] & (ndm[j] | dm[j])) || (dm[i] & ndm[j])) preds[j].push_back(i);
+      enum { TODO, PENDING, DONE };
+      std::vector<int> state(n, TODO);
+      std::vector<Rec> order, pend_run;
+      std::vector<int> pend_idx;
+      order.reserve(n);
+      int left = n;
+      while (left > 0) {
+        for (bool progress = true; progress;) {
+          progress = false;
+          for (int j = 0; j < n; ++j) {
+            if (state[j] != TODO) continue;
+            bool ok = true;
+            for (int i : preds[j]) ok &= state[i] == DONE;
+            if (!ok) continue;
+            if (recs[j].cls == C_DIAG) {
+              state[j] = PENDING;
+              pend_idx.push_back(j);
+            } else {
+              state[j] = DONE;
+              order.push_back(recs[j]);
+              --left;
+            }
+            progress = true;
+          }
+        }
+        // nothing else can run without the pending run: flush it
+        bool todo = false;
+        for (int j = 0; j < n; ++j) todo |= state[j] == TODO;
+        if (!todo) break;
+        if (pend_idx.empty()) {
+          if (std::getenv("HISVSIM_SCHED_DEBUG")) {
+            for (int j = 0; j < n; ++j) {
+              std::fprintf(stderr, "rec %d cls %d tloc %d ploc %d nctl %d state %d preds:", j, (int)recs[j].cls, recs[j].tloc, recs[j].ploc, recs[j].nctl, state[j]);
+              for (int i : preds[j]) std::fprintf(stderr, " %d", i);
+              std::fprintf(stderr, "\n");
+            }
+          }
+          err = "internal: phase schedule stalled";
+          return HS_ERR_INVALID;
+        }
+        std::sort(pend_idx.begin(), pend_idx.end());
+        bool dense_left = false;
+        for (int j = 0; j < n; ++j) dense_left |= state[j] == TODO;
+        if (!dense_left) break;  // only the trailing run is pending
+        for (int j : pend_idx) {
+          state[j] = DONE;
+          order.push_back(recs[j]);
+          --left;
+        }
+        pend_idx.clear();
+      }
+      std::sort(pend_idx.begin(), pend_idx.end());
+      std::vector<Rec> pend;
+      for (int j : pend_idx) pend.push_back(recs[j]);
+      // the trailing run commutes with the shared-memory exchange: defer it
+      // to the next phase, where it joins that phase's first run (one flush
+      // instead of two; the next phase re-expresses it in its registers)
+      if (remaining > 0) carry.swap(pend);
+      else order.insert(order.end(), pend.begin(), pend.end());
       recs.swap(order);
+      if (recs.empty()) continue;  // all deferred
     }
     // the rest of the chosen register set first (the mixed-diagonal choice
     // above assumed it), then the lowest locations
@@ -731,66 +864,8 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     choose_npos(nonreg, dtype, ph.npos);
     P.prog.push_back(ph);
     ++phases;
-    auto reg_of = [&](int L) -> int {
-      for (int k = 0; k < RB; ++k) if (R[k] == L) return k;
-      return -1;
-    };
-    for (const Rec& r : recs) {
-      Instr in;
-      std::memset(&in, 0, sizeof(in));
-      in.k = K_NONE;
-      uint64_t gq = 0, gc = 0;
-      for (int a = 0; a < r.nctl; ++a) {
-        int k = reg_of(r.cloc[a]);
-        if (r.cloc[a] >= GBIT) gc |= 1ull << (r.cloc[a] - GBIT);
-        else if (k >= 0) in.creg |= 1u << k;
-        else in.ctid |= 1u << r.cloc[a];
-      }
-      int k = reg_of(r.tloc);
-      if (r.cls == C_DIAG) {
-        in.op = I_DIAG;
-        uint32_t kreg = 0, qt = 0;
-        for (int loc : {r.tloc, r.ploc}) {
-          if (loc < 0) continue;
-          int kk = reg_of(loc);
-          if (loc >= GBIT) gq |= 1ull << (loc - GBIT);
-          else if (kk >= 0) kreg |= 1u << kk;
-          else qt |= 1u << loc;
-        }
-        if (r.ploc < 0 && k >= 0) {
-          in.k = (uint8_t)k;  // one register bit
-        } else if (kreg == 0) {
-          in.qtid = qt;       // parity of thread bits: uniform per thread
-        } else {
-          in.flags |= F_PARITY;
-          in.rpos[0] = (uint8_t)kreg;
-          in.qtid = qt;
-        }
-        in.m[0] = r.m[0]; in.m[1] = r.m[1]; in.m[2] = r.m[6]; in.m[3] = r.m[7];
-        bool d0one = r.m[0] == 1.0 && r.m[1] == 0.0;
-        bool d1one = r.m[6] == 1.0 && r.m[7] == 0.0;
-        if (d0one) in.flags |= F_D0_ONE;
-        if (d1one) in.flags |= F_D1_ONE;
-        if (d0one && r.m[6] == -1.0 && r.m[7] == 0.0) in.flags |= F_SIGN;
-        if (gq || gc) instr_set_global(in, gq, gc);
-        P.info.diag_gates++;
-      } else {
-        in.op = (r.cls == C_PERM) ? I_PERM : I_DENSE;
-        in.k = (uint8_t)k;  // target is a register bit by construction
-        std::memcpy(in.m, r.m, sizeof(in.m));
-        if (r.m[1] == 0 && r.m[3] == 0 && r.m[5] == 0 && r.m[7] == 0) in.flags |= F_REAL;
-        if (r.cls == C_PERM) P.info.perm_gates++; else P.info.dense_gates++;
-      }
-      if (in.creg == 0 && in.ctid == 0 && gc == 0) in.flags |= F_PLAIN;
-      flops += paper_flops(r);
-      {  // FP64 pipe instructions per amplitude, FMA = 1 (what the kernels issue)
-        double share = 1.0 / double(1 << r.nctl);
-        if (in.op == I_DENSE) fp64 += share * ((in.flags & F_REAL) ? 4.0 : 8.0);
-        if (in.op == I_DIAG && !(in.flags & F_SIGN))
-          fp64 += share * (((in.flags & (F_D0_ONE | F_D1_ONE)) && !(in.flags & F_PARITY)) ? 2.0 : 4.0);
-      }
-      P.prog.push_back(in);
-    }
+    R_last = R;
+    for (const Rec& r : recs) P.prog.push_back(to_instr(r));
   }
   if (phases == 0) {  // no arithmetic at all (empty part or SWAPs only)
     Instr ph;
@@ -803,7 +878,13 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     choose_npos(nonreg, dtype, ph.npos);
     P.prog.push_back(ph);
     phases = 1;
+    R_last.clear();
+    for (int k = 0; k < RB; ++k) R_last.push_back(k);
   }
+  // diagonals still deferred (the phases after them only relabelled): the
+  // last phase applies them
+  for (const Rec& r : carry) P.prog.push_back(to_instr(r));
+  carry.clear();
   // final store: register k holds location R[k] of the last phase, which is
   // tile bit bit_at[R[k]]; it is written to tile position rho[bit_at[R[k]]]
   Instr* last = nullptr;
