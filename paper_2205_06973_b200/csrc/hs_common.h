@@ -121,6 +121,9 @@ struct PartPlan {
 int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, int device, int smem_optin,
                         std::string& err);
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local);
+// FP64 instructions per amplitude the compiled kernel of `pl` issues
+// (the generator's count; host only, no compilation)
+double jit_fp64_per_amp(const PartPlan& pl, int dtype, int n_local);
 // recompile one launch of a compiled program (e.g. after setting pl.fuse)
 int jit_recompile(PartPlan& pl, int dtype, int n_local, int device, int smem_optin, std::string& err);
 void jit_cache_stats(int* disk_hits, int* compiles);

@@ -1103,6 +1103,11 @@ int jit_compile_program(std::vector<PartPlan>& plans, int dtype, int n_local, in
 }
 
 std::string jit_source_for(const PartPlan& pl, int dtype, int n_local) { return jit_source(pl, dtype, n_local); }
+double jit_fp64_per_amp(const PartPlan& pl, int dtype, int n_local) {
+  double f = 0.0;
+  jit_source(pl, dtype, n_local, &f);
+  return f;
+}
 
 int jit_recompile(PartPlan& pl, int dtype, int n_local, int device, int smem_optin, std::string& err) {
   double scale[2] = {pl.carry_in[0], pl.carry_in[1]};

@@ -1778,9 +1778,21 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
           if (!cand.second) return s;
           continue;  // e.g. more than 32 global qubits in one pass: not this grouping
         }
-        if (std::getenv("HISVSIM_PLAN_DEBUG"))
-          std::fprintf(stderr, "[plan] grouping %d%s: %zu passes, %zu launches, cost %.1f\n", (int)mode,
+        if (std::getenv("HISVSIM_PLAN_DEBUG")) {
+          std::fprintf(stderr, "[plan] grouping %d%s: %zu passes, %zu launches, cost %.1f", (int)mode,
                        cand.second ? " (global diagonals)" : "", ap.size(), la, c);
+          if (options & HS_PLAN_JIT) {  // the generator's FP64 count per launch
+            std::vector<PartPlan> tmp;
+            std::vector<int32_t> ip, fp;
+            std::string e;
+            if (plan_program(n_local, dtype, tile_max, options & ~HS_PLAN_MERGE, ap.data(), (int)ap.size(), ag.data(),
+                             (int)ag.size(), tmp, e, &ip, given_init, &fp, &agl) == HS_OK) {
+              std::fprintf(stderr, ", fp64/amp:");
+              for (const PartPlan& pl : tmp) std::fprintf(stderr, " %.0f", jit_fp64_per_amp(pl, dtype, n_local));
+            }
+          }
+          std::fprintf(stderr, "\n");
+        }
         // fewest launches; among as few, the lowest pass_cost (measured c3:
         // 13 launches with one short-read pass 96.3 ms, 14 coalesced 96.6-97.4)
         static const bool by_cost = [] {
