@@ -145,6 +145,7 @@ struct LayoutIO {
   const int32_t* extra_first = nullptr;  // physical positions that fill the tile before the lowest free ones
   int num_extra_first = 0;
   int mode = LAYOUT_KEEP;
+  int hot = 0;  // PRIORITY: lowest positions for the soonest-staged qubits (0: the default)
 };
 
 // Plan one part. Returns HS_OK or an error code with `err` filled.

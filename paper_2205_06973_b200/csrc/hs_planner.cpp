@@ -34,10 +34,14 @@ static bool env_is(const char* name, const char* value) {
 }
 
 // lowest storage positions each pass hands to the next pass's qubits from
-// its own tile ($HISVSIM_HOT, default 3: 128 B runs of complex128)
-int layout_hot() {
+// its own tile ($HISVSIM_HOT; default 3 = 128 B runs of complex128, 6 = 1 KB
+// runs for programs with global-diagonal passes). Measured on one B200: c3
+// with global diagonals 64.6-65.0 ms at 3, 62.0-62.1 at 6, 62.0 at 7 / 8
+// (its memory-bound last passes 7.4 / 7.9 -> 6.0 / 6.1 ms); c2 (staged
+// diagonals) 5.11 at 3 vs 5.25 at 6; c1 equal.
+int layout_hot(bool global_plan = false) {
   const char* e = std::getenv("HISVSIM_HOT");
-  if (!e || !*e) return 3;
+  if (!e || !*e) return global_plan ? 6 : 3;
   return std::max(1, std::min(8, std::atoi(e)));
 }
 
@@ -564,7 +568,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
                        [&](int x, int y) { return lay->next_use[occ[x]] < lay->next_use[occ[y]]; });
       const int32_t never = 1 << 29;
       std::vector<char> taken(T, 0), placed(T, 0);
-      const int hot = std::min(layout_hot(), T);
+      const int hot = std::min(lay->hot > 0 ? lay->hot : layout_hot(), T);
       for (int r = 0; r < hot; ++r) {
         rho[order[r]] = r;
         taken[r] = placed[order[r]] = 1;
@@ -1871,7 +1875,9 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
   // runs) c2 5.42 vs 5.55 ms, c3 95.0 vs 95.4 ms, c1 equal (an earlier
   // planner measured the opposite: c3 126 vs 121 ms). The gate-free final
   // permutation stages at most 2 * hot qubits.
-  const int hot = std::min(layout_hot(), std::max(1, std::min(n_local, tile_max / 2)));
+  bool global_plan = false;  // a program with global-diagonal passes
+  for (int i = 0; globals && i < num_parts; ++i) global_plan |= !(*globals)[i].empty();
+  const int hot = std::min(layout_hot(global_plan), std::max(1, std::min(n_local, tile_max / 2)));
   const bool no_restore = (options & HS_PLAN_NO_RESTORE) != 0;
   // The last part's tile takes the lowest logical qubits it does not stage
   // as its extra bits; it writes natural order itself when those and its
@@ -1902,6 +1908,7 @@ int plan_program(int n_local, int dtype, int tile_max, uint32_t options, const h
       return HS_ERR_INVALID;
     }
     LayoutIO lay;
+    lay.hot = hot;
     std::vector<int32_t> next(phys);
     std::vector<int32_t> tgt(phys);
     const bool oop = pp && !(first_inplace && i == 0);
