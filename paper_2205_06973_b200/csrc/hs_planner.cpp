@@ -309,7 +309,7 @@ int compiled_cost(const Gate& G) {
 // gate joins the run only if the product is no more expensive than the two
 // factors apart. Gates on other bits commute with the run, so program order
 // of the remaining list is still a valid order of the part.
-void fuse_single_qubit_runs(std::vector<Gate>& gs, int T, bool cost_aware) {
+void fuse_single_qubit_runs(std::vector<Gate>& gs, bool cost_aware) {
   std::vector<Gate> out;
   out.reserve(gs.size());
   std::vector<int> open(64, -1);  // tile bits < T, global bits GBIT + j
@@ -447,7 +447,7 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
     classify(G);
   }
   const int input_gates = num_gates;
-  if (options & HS_PLAN_FUSE_1Q) fuse_single_qubit_runs(gs, T, (options & HS_PLAN_JIT) != 0);
+  if (options & HS_PLAN_FUSE_1Q) fuse_single_qubit_runs(gs, (options & HS_PLAN_JIT) != 0);
   if (options & HS_PLAN_PARITY) fuse_parity_diagonals(gs);
   num_gates = (int)gs.size();
   // a global qubit is never staged: only diagonal action on it can run
