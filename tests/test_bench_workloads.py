@@ -81,3 +81,27 @@ def test_c5_sizes_and_rejections():
         configs.bench_workload("c5", 16)
     with pytest.raises(ValueError):
         configs.bench_workload("c3", 3)
+
+
+def test_reference_arm_line_counts_the_same_work(tmp_path):
+    """`bench.py --impl reference` (the CPU restatement, no GPU) prints the
+    contract's JSON line in the engine arm's unit: amplitude updates of the
+    reference partition per second (2 x 16 B each), with the sampled bytes
+    beside it, so the driver's ratio compares the same work."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import bench
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--steps", "1", "--warmup", "1", "--cpu-step-seconds", "0.2"],
+                         capture_output=True, text=True, timeout=600, cwd=tmp_path)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == bench.UNIT
+    assert line["value"] > 0 and line["e2e"]["value"] == line["value"]
+    assert abs(line["hbm_gbs_moved"] - line["value"] * bench.AMP_BYTES_PER_UPDATE) < 1e-6 * line["hbm_gbs_moved"]
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
