@@ -943,7 +943,8 @@ std::map<std::string, void*> g_cache;  // source -> kernel handle
 // ~/.cache/hisvsim; "off" disables), keyed by a 64-bit FNV-1a hash of the
 // generated source, the NVRTC options and the NVRTC version; the entry also
 // stores the full source, compared on load, so a hash collision is a miss.
-const char* kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device"};
+// (line info: ncu maps the compiled passes' SASS back to the generated source)
+const char* kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-default-device", "--generate-line-info"};
 
 std::string cache_dir() {
   const char* d = std::getenv("HISVSIM_CACHE_DIR");
@@ -1045,7 +1046,7 @@ int nvrtc_compile(const std::string& src, std::vector<char>& cubin, std::string&
     err = "nvrtcCreateProgram failed";
     return HS_ERR_UNSUPPORTED;
   }
-  nvrtcResult r = nvrtcCompileProgram(prog, 3, kNvrtcOpts);
+  nvrtcResult r = nvrtcCompileProgram(prog, (int)(sizeof(kNvrtcOpts) / sizeof(kNvrtcOpts[0])), kNvrtcOpts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
