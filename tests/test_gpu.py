@@ -194,6 +194,17 @@ def test_global_diagonal_programs_match_c_oracle(name, strategy, force, monkeypa
     assert max_abs_diff(st, ref) < 1e-10
 
 
+@pytest.mark.parametrize("name", ["c4@24", "c3@24"])
+def test_global_diagonal_programs_complex64(name):
+    """complex64 compiled passes with global diagonals (the gw word and the
+    gq / gc masks in the float kernels) against the C oracle at 1e-4."""
+    c = configs.build(name)
+    part = partition_dfs(build_dag(c), 12)
+    st = execute_hierarchical(c, part, dtype="complex64")
+    ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+    assert max_abs_diff(st, ref) < 1e-4
+
+
 def test_distributed_emulated_ranks_match_reference(golden):
     docs, states = golden.json("corpus"), golden.npz("corpus")
     for i, doc in enumerate(docs):
