@@ -743,7 +743,12 @@ def main(argv=None):
     if world == 1:
         roofline["binding"] = {"what": "sum over launches of max(HBM bytes / peak, FP64 instructions / measured DFMA rate)",
                                "bound_ms_per_step": bind_ms, "measured_ms_per_step": g["ms_step"],
-                               "frac": bind_ms / g["ms_step"]}
+                               "frac": bind_ms / g["ms_step"],
+                               "fp64_instr_per_amp_per_launch": [round(i["fp64_instr_per_amp"], 1) for i in infos],
+                               "hbm_ms_per_launch_at_peak": g["bytes_per_pass"] / (peak * 1e9) * 1e3,
+                               "note": "a launch whose FP64 work takes longer than its HBM traffic at the measured rates "
+                                       "is bound by the FP64 pipe (DFMA; B200 has no FP64 tensor-core path worth using, "
+                                       "DESIGN 3.5): its HBM fraction is below 1 by construction"}
     line = {"metric": METRIC, "value": g["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": g["ms_step"], "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no dataset)",
