@@ -527,3 +527,49 @@ def test_global_diagonals_cut_the_c3_and_c4_launch_counts():
             os.environ.pop("HISVSIM_CACHE_DIR", None)
         else:
             os.environ["HISVSIM_CACHE_DIR"] = old
+
+
+def test_global_diagonal_edge_circuits(monkeypatch):
+    """Edge cases of unstaged diagonals, emulated against the oracle: a
+    circuit of diagonal gates only (passes that stage nothing), a graph
+    state (H on every qubit, CZ on every pair: CZs with both qubits global),
+    and controlled phases whose control or target is the only unstaged
+    qubit; tiles narrower than the state so globals are free bits."""
+    import random
+
+    from paper_2205_06973_b200.qasm import Circuit, GateKind, GateOp
+
+    monkeypatch.setenv("HISVSIM_GLOBAL_DIAG", "1")
+    rng = random.Random(7)
+    n = 13
+    diag_only = [GateOp(GateKind.H, (q,), ()) for q in (0, 5)]
+    for _ in range(120):
+        a, b = rng.sample(range(n), 2)
+        k = rng.choice([GateKind.Z, GateKind.S, GateKind.T, GateKind.RZ, GateKind.U1, GateKind.CZ, GateKind.CRZ])
+        if k in (GateKind.CZ, GateKind.CRZ):
+            diag_only.append(GateOp(k, (a, b), (rng.uniform(0, 3),) if k == GateKind.CRZ else ()))
+        else:
+            diag_only.append(GateOp(k, (a,), (rng.uniform(0, 3),) if k in (GateKind.RZ, GateKind.U1) else ()))
+    graph = [GateOp(GateKind.H, (q,), ()) for q in range(n)]
+    graph += [GateOp(GateKind.CZ, (a, b), ()) for a in range(n) for b in range(a + 1, n) if (a * 7 + b) % 3]
+    graph += [GateOp(GateKind.RX, (q,), (0.3 + q,)) for q in range(n)]
+    ctl = [GateOp(GateKind.H, (q,), ()) for q in range(n)]
+    for layer in range(3):
+        for q in range(n - 1):
+            ctl.append(GateOp(GateKind.CRZ, (q, n - 1 - q) if q != n - 1 - q else (q, 0), (0.1 * (q + layer + 1),)))
+        ctl += [GateOp(GateKind.RY, (q,), (0.2 * layer + 0.1,)) for q in range(0, n, 2)]
+    for ops in (diag_only, graph, ctl):
+        c = Circuit(n, tuple(ops))
+        with_globals = 0
+        for limit in (4, 6):
+            part = partition_dfs(build_dag(c), limit)
+            exes = [remap_part(c, p) for p in part.parts]
+            want = orc.execute_hierarchical(c, [(p.gate_indices, p.qubits) for p in part.parts])
+            for tile, opts in ((6, 0xc15), (8, 0xc1d), (8, 0xc5d)):
+                launches = emu.plan_program(_native, n, 0, tile, exes, options=opts)
+                psi = np.zeros((1, 1 << n), dtype=np.complex128)
+                psi[0, 0] = 1
+                emu.run_program(psi, n, launches)
+                assert np.max(np.abs(psi[0] - want)) < 1e-12, (limit, tile, hex(opts))
+                with_globals += sum(1 for _, p in launches if len(p) and int(p[0]["op"]) == emu.I_GLOBALS)
+        assert with_globals > 0
