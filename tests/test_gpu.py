@@ -194,6 +194,34 @@ def test_global_diagonal_programs_match_c_oracle(name, strategy, force, monkeypa
     assert max_abs_diff(st, ref) < 1e-10
 
 
+def test_global_diagonal_edge_circuits_on_gpu(monkeypatch):
+    """Compiled passes on 22 qubits for the emulated edge cases: a graph
+    state (CZs with both qubits unstaged) and a circuit of diagonal gates
+    only (passes that stage nothing), against the C oracle."""
+    import random
+
+    from paper_2205_06973_b200.qasm import Circuit
+
+    monkeypatch.setenv("HISVSIM_GLOBAL_DIAG", "1")
+    rng = random.Random(3)
+    n = 22
+    graph = [GateOp(GateKind.H, (q,), ()) for q in range(n)]
+    graph += [GateOp(GateKind.CZ, (a, b), ()) for a in range(n) for b in range(a + 1, n) if (a * 5 + b) % 4 == 0]
+    graph += [GateOp(GateKind.RX, (q,), (0.2 + 0.1 * q,)) for q in range(n)]
+    diag = [GateOp(GateKind.H, (q,), ()) for q in range(0, n, 3)]
+    for _ in range(200):
+        a, b = rng.sample(range(n), 2)
+        k = rng.choice([GateKind.T, GateKind.RZ, GateKind.CZ, GateKind.CRZ])
+        diag.append(GateOp(k, (a, b) if k in (GateKind.CZ, GateKind.CRZ) else (a,),
+                           (rng.uniform(0, 3),) if k in (GateKind.RZ, GateKind.CRZ) else ()))
+    for ops in (graph, diag):
+        c = Circuit(n, tuple(ops))
+        part = partition_dfs(build_dag(c), 10)
+        st = execute_hierarchical(c, part)
+        ref = c_oracle.execute_parts(c, [(p.gate_indices, p.qubits) for p in part.parts])
+        assert max_abs_diff(st, ref) < 1e-10
+
+
 @pytest.mark.parametrize("name", ["c4@24", "c3@24"])
 def test_global_diagonal_programs_complex64(name):
     """complex64 compiled passes with global diagonals (the gw word and the
