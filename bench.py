@@ -69,7 +69,8 @@ def _traffic_from_profiles(config: str, strategy: str):
             d = json.loads(f.read_text())
         except Exception:
             continue
-        if d.get("workload") == f"{config}/{strategy}" and d.get("dram_bytes_per_launch"):
+        v = d.get("dram_bytes_per_launch")
+        if d.get("workload") == f"{config}/{strategy}" and v and v == v:  # (v == v: not NaN)
             key = (int(d.get("capture_seq", 1 if "final" in f.name else 0)), f.name)
             if best is None or key > best[0]:
                 best = (key, float(d["dram_bytes_per_launch"]))
