@@ -369,13 +369,28 @@ struct Gen {
       for (size_t gi = 0; gi < masks.size(); ++gi) sig |= (__builtin_popcount(uint32_t(i) & masks[gi]) & 1) << gi;
       return sig;
     };
-    std::stable_sort(reg_order.begin(), reg_order.end(), [&](int x, int y) { return signature(x) < signature(y); });
+    // registers with the same signature and the same constant factor (the
+    // run's register-only diagonals) share one per-thread factor: the
+    // constant is folded into it once per thread, not multiplied into every
+    // register on its own
+    auto key_less = [&](int x, int y) {
+      if (signature(x) != signature(y)) return signature(x) < signature(y);
+      if (cre[x] != cre[y]) return cre[x] < cre[y];
+      return cim[x] < cim[y];
+    };
+    std::stable_sort(reg_order.begin(), reg_order.end(), key_less);
     int cur_sig = -1;
+    double cur_r = 0, cur_i = 0;
+    bool open_sig = false, open_const = false;
     for (int i : reg_order) {
       const int sig = signature(i);
-      if (sig != cur_sig) {
-        if (cur_sig >= 0) o << "      }\n";
+      const bool new_sig = sig != cur_sig;
+      const bool new_const = new_sig || cre[i] != cur_r || cim[i] != cur_i;
+      if (new_const && open_const) { o << "      }\n"; open_const = false; }
+      if (new_sig) {
+        if (open_sig) o << "      }\n";
         cur_sig = sig;
+        open_sig = true;
         o << "      {";
         for (size_t gi = 0; gi < masks.size(); ++gi) {
           const int par = sig >> gi & 1;
@@ -391,11 +406,25 @@ struct Gen {
         }
         o << "\n";
       }
+      if (new_const) {
+        cur_r = cre[i];
+        cur_i = cim[i];
+        open_const = true;
+        o << "      {";
+        if (cur_r == 1.0 && cur_i == 0.0) {
+          o << " const " << T << " gr = fr, gi = fi;\n";
+        } else {  // (fr + i fi) * constant, once per thread
+          const std::string cr = lit(cur_r, c128), ci = lit(cur_i, c128);
+          o << " const " << T << " gr = fr * " << cr << " - fi * " << ci << ", gi = fr * " << ci << " + fi * " << cr
+            << ";\n";
+          cat[4] += 4.0; ops += 4.0;  // per thread
+        }
+      }
       o << "  ";
-      cmul_const(i, cre[i], cim[i]);
-      cmul_into(i, "fr", "fi");
+      cmul_into(i, "gr", "gi");
     }
-    if (cur_sig >= 0) o << "      }\n";
+    if (open_const) o << "      }\n";
+    if (open_sig) o << "      }\n";
     o << "    }\n";
   }
   // final: fold the part's scalar S into the run and apply it (no
