@@ -430,7 +430,12 @@ struct Gen {
   // final: fold the part's scalar S into the run and apply it (no
   // normalisation); otherwise the most common factor of the run is pulled
   // out into S so the registers carrying it cost nothing
-  void flush(bool final = false) {
+  // keep_u: the instruction that forces the flush acts on register bits
+  // only (dense / X-type gates): a pending per-thread scalar alone commutes
+  // with it (it scales all of the thread's registers alike) and waits for
+  // the next flush, which applies it for free, or the phase's end
+  void flush(bool final = false, bool keep_u = false) {
+    if (keep_u && !final && have_u && !have_const && mixed.empty()) return;
     if (final && (Sr != 1.0 || Si != 0.0)) {
       for (int i = 0; i < nreg; ++i) {
         const double nr = cre[i] * Sr - cim[i] * Si, ni = cre[i] * Si + cim[i] * Sr;
@@ -473,23 +478,38 @@ struct Gen {
       return;
     }
     o << "    {\n";
-    for (int i = 0; i < nreg; ++i) {
-      const bool unit = cre[i] == 1.0 && cim[i] == 0.0;
-      if (!have_u) {
-        cmul_const(i, cre[i], cim[i]);
-        continue;
-      }
+    if (!have_u) {
+      for (int i = 0; i < nreg; ++i) cmul_const(i, cre[i], cim[i]);
+    } else {
+      // registers with the same constant share one per-thread factor
+      // (constant x scalar, once per thread per distinct constant)
       const std::string ur = "ur" + std::to_string(u_id), ui = "ui" + std::to_string(u_id);
-      if (unit) {
-        cmul_into(i, ur, ui);
-      } else {
-        o << "      { const " << R() << " fr = fma(" << lit(cre[i], c128) << ", " << ur << ", -" << lit(cim[i], c128)
-          << " * " << ui << "), fi = fma(" << lit(cre[i], c128) << ", " << ui << ", " << lit(cim[i], c128) << " * "
-          << ur << ");\n  ";
-        cat[4] += 4 * wgt; ops += 4 * wgt;
+      std::vector<int> order(nreg);
+      for (int i = 0; i < nreg; ++i) order[i] = i;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return cre[x] != cre[y] ? cre[x] < cre[y] : cim[x] < cim[y];
+      });
+      bool open = false;
+      double cr_ = 0, ci_ = 0;
+      for (int i : order) {
+        if (!open || cre[i] != cr_ || cim[i] != ci_) {
+          if (open) o << "      }\n";
+          open = true;
+          cr_ = cre[i];
+          ci_ = cim[i];
+          if (cr_ == 1.0 && ci_ == 0.0) {
+            o << "      { const " << R() << " fr = " << ur << ", fi = " << ui << ";\n";
+          } else {
+            o << "      { const " << R() << " fr = fma(" << lit(cr_, c128) << ", " << ur << ", -" << lit(ci_, c128)
+              << " * " << ui << "), fi = fma(" << lit(cr_, c128) << ", " << ui << ", " << lit(ci_, c128) << " * "
+              << ur << ");\n";
+            cat[4] += 4.0; ops += 4.0;  // per thread
+          }
+        }
+        o << "  ";
         cmul_into(i, "fr", "fi");
-        o << "      }\n";
       }
+      if (open) o << "      }\n";
     }
     o << "    }\n";
     reset_pending();
@@ -596,7 +616,7 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   for (const Instr& in : pl.prog) {
     if (in.op == I_GLOBALS) continue;  // the kernel's gw word (jit_source)
     if (in.op == I_DIAG && g.fold_diag(in)) continue;
-    if (in.op != I_DIAG) g.flush();  // a non-diagonal step: apply the pending run first
+    if (in.op != I_DIAG) g.flush(false, in.op == I_DENSE || in.op == I_PERM);  // apply the pending run first
     if (in.op == I_PHASE) {
       if (cur) {
         g.store_regs(cur->rpos, cur->npos);
