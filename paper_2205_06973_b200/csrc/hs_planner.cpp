@@ -819,13 +819,6 @@ int plan_part(int n_local, int dtype, int tile_max, uint32_t options, const int3
         for (int j = 0; j < n; ++j) todo |= state[j] == TODO;
         if (!todo) break;
         if (pend_idx.empty()) {
-          if (std::getenv("HISVSIM_SCHED_DEBUG")) {
-            for (int j = 0; j < n; ++j) {
-              std::fprintf(stderr, "rec %d cls %d tloc %d ploc %d nctl %d state %d preds:", j, (int)recs[j].cls, recs[j].tloc, recs[j].ploc, recs[j].nctl, state[j]);
-              for (int i : preds[j]) std::fprintf(stderr, " %d", i);
-              std::fprintf(stderr, "\n");
-            }
-          }
           err = "internal: phase schedule stalled";
           return HS_ERR_INVALID;
         }
