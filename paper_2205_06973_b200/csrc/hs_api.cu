@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <memory>
@@ -469,6 +470,18 @@ int hs_plan_program(int n_local, int dtype, int tile_bits, uint32_t options, con
   for (auto& pl : plans) need += sizeof(PartLaunch) + pl.prog.size() * sizeof(Instr);
   if (bytes) *bytes = need;
   if (num_launches) *num_launches = (int)plans.size();
+  if (const char* dir = std::getenv("HISVSIM_DUMP_SRC")) {
+    // debugging aid: the generated source of every compiled launch
+    for (size_t i = 0; i < plans.size(); ++i) {
+      if (!(options & HS_PLAN_JIT)) break;
+      std::string path = std::string(dir) + "/launch" + std::to_string(i) + ".cu";
+      if (FILE* f = std::fopen(path.c_str(), "w")) {
+        std::string src = jit_source_for(plans[i], dtype, n_local);
+        std::fwrite(src.data(), 1, src.size(), f);
+        std::fclose(f);
+      }
+    }
+  }
   if (!buf) return HS_OK;
   if (buf_bytes < need) return fail(HS_ERR_INVALID, "plan buffer too small");
   char* o = (char*)buf;
