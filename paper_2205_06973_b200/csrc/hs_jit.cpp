@@ -745,7 +745,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       << "  const unsigned par = (k >> 1) & 1u;\n  unsigned done = 0;\n"
       << "  while (!done) asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
          "selp.u32 %0, 1, 0, p; }\" : \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\");\n"
-      << "  ++k;\n}\n";
+      << "  ++k;\n" << (NT >= 32 ? "  __syncwarp();\n" : "") << "}\n";
     o << "#define TEAM_CSYNC() team_csync(tb_team, csync_k, bar_id, tid0)\n";
   }
   // teams per CTA ($HISVSIM_TEAMS): 2 (default) alternate tiles; 1 keeps two
@@ -902,6 +902,13 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   o << "      const unsigned mb = (unsigned)__cvta_generic_to_shared(&full[b]); const unsigned par = (unsigned)(k & 1);\n";
   o << "      unsigned done = 0;\n";
   o << "      while (!done) asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\" : \"=r\"(done) : \"r\"(mb), \"r\"(par) : \"memory\"); }\n";
+  // Reconverge the warp after the data-dependent wait loops: without it
+  // ptxas treats the rest of the tile as divergent code and keeps the gate
+  // constants in vector registers (three-vector-operand DFMAs at ~2/3 of the
+  // issue rate, profiles/tools/fp64reuse.cu) instead of uniform registers.
+  // A warp belongs to one team unless the teams share warp 0 (tiny tiles).
+  const bool reconverge = NT >= 32 && !env_on("HISVSIM_SYNCWARP", "0");  // "0": A/B without
+  if (reconverge) o << "    __syncwarp();\n";
   if (cl > 0) {  // the first phase reads other CTAs' slots: their loads must be in
     const Instr* first = nullptr;
     for (const Instr& in : pl.prog)
@@ -912,7 +919,7 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   // direct stores: the buffer is free once the last phase has loaded its
   // registers, so its refill (tile i + 3) overlaps the last phase's gates
   emit_program(g, pl, cl > 0 ? "TEAM_CSYNC();" : "TEAM_SYNC();", fp64_per_amp, "TEAM_SYNC();",
-               direct ? "TEAM_SYNC(); issue(i + 3);" : nullptr);
+               direct ? (reconverge ? "TEAM_SYNC(); issue(i + 3); __syncwarp();" : "TEAM_SYNC(); issue(i + 3);") : nullptr);
   const FuseSwitch& fz = pl.fuse;
   if (oop) o << "    const unsigned long long obase = out_base(tt);\n";
   // fused layout switch: every amplitude goes to the rank that owns it after

@@ -246,6 +246,44 @@ def test_compiled_part_sources_build_for_sm100a(tmp_path, name, dtype):
         assert "hs_jit_part" in res.stderr
 
 
+def test_compiled_parts_reconverge_after_tile_waits(tmp_path, monkeypatch):
+    """The tile's wait loops are followed by __syncwarp(): without it ptxas
+    compiles the rest of the tile as divergent code and keeps the gate
+    constants in vector registers, so most DFMAs read three vector operands
+    (~2/3 of the DFMA issue rate). With it, the constants sit in uniform
+    registers (checked in the SASS: fewer three-vector DFMAs, more UR ones)."""
+    import shutil
+    import subprocess
+
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    c = configs.build("c2@16")
+    p = partition_dfs(build_dag(c), 12).parts[0]
+
+    def sass_counts(src):
+        (tmp_path / "k.cu").write_text(src)
+        res = subprocess.run([nvcc, "-arch=sm_100a", "-cubin", "-o", str(tmp_path / "k.cubin"), str(tmp_path / "k.cu")],
+                             capture_output=True, text=True)
+        assert res.returncode == 0, res.stderr[-2000:]
+        sass = subprocess.run([cuobjdump, "-sass", str(tmp_path / "k.cubin")], capture_output=True, text=True).stdout
+        three = ur = 0
+        for m in re.finditer(r"\bDFMA\S*\s+([^;]*);", sass):
+            srcs = [a.strip() for a in m.group(1).split(",")][1:]
+            ur += any("UR" in a for a in srcs)
+            three += sum(bool(re.match(r"-?\|?R\d+", a)) for a in srcs) == 3
+        return three, ur
+
+    src = _jit_source(c, p)
+    wait = src.index("mbarrier.try_wait.parity.shared::cta.b64")
+    assert src[wait:].split("\n", 2)[1].strip() == "__syncwarp();"
+    three, ur = sass_counts(src)
+    monkeypatch.setenv("HISVSIM_SYNCWARP", "0")
+    src0 = _jit_source(c, p)
+    assert "__syncwarp();" not in src0
+    three0, ur0 = sass_counts(src0)
+    assert three < three0 and ur > ur0, (three, three0, ur, ur0)
+
+
 def _structure(m, allow_scale=True):
     import ctypes
 
