@@ -144,6 +144,50 @@ def test_scaled_configs_match_reference_samples(golden, name):
     assert abs(st.norm() - doc["norm"]) < 1e-10
 
 
+@pytest.mark.parametrize("name,fixture", [("c2@24", "configs_large"), ("c3@24", "configs_large"),
+                                          ("c4@22", "configs_large_c4")])
+def test_24_qubit_programs_match_the_reference_itself(golden, name, fixture):
+    """The compiled paths against the UNMODIFIED reference's own amplitudes
+    (no oracle in between) at the largest size the reference runs in minutes:
+    24-qubit c2 / c3 and 22-qubit c4 (tests/golden/make_golden_large.py ran hier.py:342-368
+    there; 4096 sampled amplitudes, the norm and a weighted checksum of every
+    |amp|^2). Checked: execute_hierarchical, the program bench.py times
+    (|0..0> in its own initial layout, ping-pong passes, one CUDA graph) and
+    the one-pass-per-part program."""
+    from paper_2205_06973_b200.statevec import StateVector, allocate
+
+    doc = golden.json(fixture)[name + ":sample"]
+    arr = golden.npz(fixture)
+    key = name.replace("@", "_")
+    c = configs.build(name)
+    n = c.num_qubits
+    assert (n, c.num_ops) == (doc["num_qubits"], doc["num_ops"])
+    part = partition_of(doc["partition"], "dfs", doc["limit"])
+    idx = torch.as_tensor(arr[key + "_idx"], device="cuda")
+    weights = (torch.arange(1 << n, device="cuda") % 7).to(torch.float64)
+
+    def check(data):
+        got = data[idx].cpu().numpy()
+        assert float(np.max(np.abs(got - arr[key + "_amp"]))) < 1e-10
+        p2 = data.real ** 2 + data.imag ** 2
+        assert abs(float(p2.sum().sqrt()) - doc["norm"]) < 1e-10
+        assert abs(float((p2 * weights).sum()) - doc["checksum_abs2_weighted"]) < 1e-9
+
+    check(execute_hierarchical(c, part).data)
+    buf = allocate(n)
+    timed = HierarchicalRun(c, part, basis_start=True)
+    assert all(timed.program.info(j)["compiled"] for j in range(timed.program.num_launches))
+    for _ in range(2):  # graph capture, then replay
+        timed.program.init_basis(buf, 0)
+        timed.program.run_graph(buf)
+        check(StateVector(n, buf).data)
+    literal = HierarchicalRun(c, part, basis_start=True, options=(timed.program.options & ~_native.HS_PLAN_MERGE)
+                              | _native.HS_PLAN_PART_LOCAL)
+    literal.program.init_basis(buf, 0)
+    literal.program.run_graph(buf)
+    check(StateVector(n, buf).data)
+
+
 @pytest.mark.parametrize("name,strategy", [("c2", "dfs"), ("c2", "dagp"), ("c3@26", "dfs")])
 def test_full_size_configs_match_c_oracle(golden, name, strategy):
     """26-qubit runs against the multi-threaded C oracle (same partition)."""

@@ -138,6 +138,23 @@ def test_c_oracle_matches_reference_samples(golden, name):
     _sample_check(golden, name, psi)
 
 
+@pytest.mark.parametrize("name,fixture", [("c2@24", "configs_large"), ("c3@24", "configs_large"),
+                                          ("c4@22", "configs_large_c4")])
+def test_c_oracle_matches_reference_samples_at_24_qubits(golden, name, fixture):
+    """The C oracle against the unmodified reference at 24 qubits
+    (tests/golden/make_golden_large.py): sampled amplitudes, norm, and the
+    weighted checksum over every |amp|^2."""
+    doc = golden.json(fixture)[name + ":sample"]
+    arr = golden.npz(fixture)
+    key = name.replace("@", "_")
+    c = configs.build(name)
+    psi = c_oracle.execute_parts(c, parts_of(doc["partition"]))
+    assert np.max(np.abs(psi[arr[key + "_idx"]] - arr[key + "_amp"])) < 1e-12
+    p2 = psi.real ** 2 + psi.imag ** 2
+    assert abs(np.sqrt(p2.sum()) - doc["norm"]) < 1e-12
+    assert abs(float(np.sum(p2 * (np.arange(p2.size) % 7))) - doc["checksum_abs2_weighted"]) < 1e-10
+
+
 def test_c_oracle_matches_corpus_and_flat(golden):
     docs, states = golden.json("corpus"), golden.npz("corpus")
     for i, doc in enumerate(docs[:30]):
