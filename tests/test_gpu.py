@@ -152,8 +152,8 @@ def test_24_qubit_programs_match_the_reference_itself(golden, name, fixture):
     24-qubit c2 / c3 and 22-qubit c4 (tests/golden/make_golden_large.py ran hier.py:342-368
     there; 4096 sampled amplitudes, the norm and a weighted checksum of every
     |amp|^2). Checked: execute_hierarchical, the program bench.py times
-    (|0..0> in its own initial layout, ping-pong passes, one CUDA graph) and
-    the one-pass-per-part program."""
+    (|0..0> in its own initial layout, ping-pong passes, one CUDA graph), the
+    one-pass-per-part program and simulate_distributed over 2 and 8 ranks."""
     from paper_2205_06973_b200.statevec import StateVector, allocate
 
     doc = golden.json(fixture)[name + ":sample"]
@@ -186,6 +186,10 @@ def test_24_qubit_programs_match_the_reference_itself(golden, name, fixture):
     literal.program.init_basis(buf, 0)
     literal.program.run_graph(buf)
     check(StateVector(n, buf).data)
+    del buf, timed, literal
+    # the sharded path (emulated ranks on this GPU, dist.py:485-529) ends in the same state
+    for p_bits in (1, 3):
+        check(simulate_distributed(c, part, p_bits).state.data)
 
 
 @pytest.mark.parametrize("name,strategy", [("c2", "dfs"), ("c2", "dagp"), ("c3@26", "dfs")])
