@@ -177,6 +177,9 @@ def test_24_qubit_programs_match_the_reference_itself(golden, name, fixture):
     # any valid partition ends in the same state: this repo's dagP parts, and complex64 at the north star's 1e-4
     check(execute_hierarchical(c, partition_dagp(build_dag(c), doc["limit"])).data)
     check(execute_hierarchical(c, part, dtype="complex64").data, TOL["complex64"])
+    # parts wider than one 12-qubit tile (k = 14, the c5 path) and the two-level run (hier.py:371-419)
+    check(execute_hierarchical(c, partition_dfs(build_dag(c), 14)).data)
+    check(execute_multilevel(c, partition_multilevel(build_dag(c), doc["limit"], 8)).data)
     buf = allocate(n)
     timed = HierarchicalRun(c, part, basis_start=True)
     assert all(timed.program.info(j)["compiled"] for j in range(timed.program.num_launches))
