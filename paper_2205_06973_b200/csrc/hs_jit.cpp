@@ -74,6 +74,13 @@ std::string lit_raw(double v, bool c128) {
 struct Gen {
   std::ostringstream o;
   bool c128;
+  // two teams take turns on the FP64 pipe (HISVSIM_FP64_TOKEN=1): a team's
+  // gates run between PP_ACQUIRE (after the phase's shared-memory loads) and
+  // PP_RELEASE (before its stores), so one team exchanges while the other
+  // computes instead of both doing the same thing at once
+  bool token = false;
+  int token_phases = 0;  // acquire / release pairs emitted per tile
+  int token_threads = 0;  // both teams' threads
   int RB, T, n_local;
   int nreg;
   std::vector<int> var;  // register slot i -> variable index
@@ -611,6 +618,20 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   o << "    " << g.R() << " ";
   for (int i = 0; i < g.nreg; ++i) o << (i ? ", " : "") << "r" << i << ", q" << i;
   o << ";\n    unsigned t, st;\n";
+  // the turns: a team takes its turn before a phase's shared-memory loads
+  // (memory operations stay behind the barrier) and passes it on once the
+  // phase's arithmetic is done. ptxas moves arithmetic freely across a
+  // barrier, so the passing barrier's id depends on every amplitude register
+  // through a value it cannot know is zero (zero_: high bits of ntiles)
+  auto take_turn = [&]() { o << "    PP_ACQUIRE();\n"; };
+  auto pass_turn = [&]() {
+    o << "    { unsigned h_ = 0u;";
+    for (int i = 0; i < g.nreg; ++i) {
+      if (g.c128) o << " h_ ^= (unsigned)__double2hiint(r" << i << ") ^ (unsigned)__double2hiint(q" << i << ");";
+      else o << " h_ ^= __float_as_uint(r" << i << ") ^ __float_as_uint(q" << i << ");";
+    }
+    o << "\n      asm volatile(\"bar.arrive %0, " << g.token_threads << ";\" :: \"r\"(3u + (team ^ 1u) + (h_ & zero_)) : \"memory\"); }\n";
+  };
   const Instr* cur = nullptr;
   g.reset_pending();
   for (const Instr& in : pl.prog) {
@@ -619,11 +640,16 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
     if (in.op != I_DIAG) g.flush(false, in.op == I_DENSE || in.op == I_PERM);  // apply the pending run first
     if (in.op == I_PHASE) {
       if (cur) {
+        if (g.token) pass_turn();
         g.store_regs(cur->rpos, cur->npos);
         o << "    " << xsync(cur->rpos, cur->npos, in.rpos, in.npos) << "\n";
       }
       g.emit_tdep("t", in.npos);
       o << "    st = swz(t);\n";
+      if (g.token) {
+        take_turn();
+        ++g.token_phases;
+      }
       g.load_regs(in.rpos, in.npos);
       if (&in == last_phase && after_last_load) o << "    " << after_last_load << "\n";
       cur = &in;
@@ -643,6 +669,7 @@ void emit_program(Gen& g, const PartPlan& pl, const char* sync, double* fp64_per
   // carried to the program's last launch unless it grows large
   const bool apply = !g.carry || std::fabs(std::log2(std::hypot(g.Sr, g.Si))) > (g.c128 ? 200 : 24);
   g.flush(apply);
+  if (g.token && cur) pass_turn();
   if (fp64_per_amp) *fp64_per_amp = g.ops / g.nreg;
   o << "    // fp64_instr_per_amp " << g.ops / g.nreg << " (dense " << g.cat[0] / g.nreg << ", diagonal apply "
     << g.cat[1] / g.nreg << ", constants " << g.cat[2] / g.nreg << ", mixed groups " << g.cat[3] / g.nreg
@@ -871,6 +898,28 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
     o << "      } }\n";
   }
   o << "  };\n";
+  // HISVSIM_FP64_TOKEN: "1" every two-team launch, "auto" only launches with
+  // little arithmetic (at most TOKEN_AUTO_GATES gate instructions per tile:
+  // memory-bound passes and gate-free layout launches), else off. Measured on
+  // c3 (ms per launch, turns / no turns): FP64-heavy launches 10.6 / 8.7,
+  // 14.6 / 12.5 (the turn serialises the loads of one team with the
+  // arithmetic of the other); the memory-bound last launch 5.43 / 6.20
+  int gate_instrs = 0;
+  for (const Instr& in : pl.prog) gate_instrs += in.op == I_DENSE || in.op == I_PERM || in.op == I_DIAG;
+  constexpr int TOKEN_AUTO_GATES = 10;
+  g.token = TEAMS == 2 && cl == 0 && NT >= 32 &&
+            (env_on("HISVSIM_FP64_TOKEN", "1") ||
+             (env_on("HISVSIM_FP64_TOKEN", "auto") && gate_instrs <= TOKEN_AUTO_GATES));
+  g.token_threads = 2 * NT;
+  if (g.token) {
+    // named barriers 3 + team: a team waits on its own, the other team's
+    // release arrives on it (2 * NT participants); team 1 hands team 0 the
+    // first turn
+    o << "#define PP_ACQUIRE() asm volatile(\"bar.sync %0, " << 2 * NT << ";\" :: \"r\"(3u + team) : \"memory\")\n";
+    o << "#define PP_RELEASE() asm volatile(\"bar.arrive %0, " << 2 * NT << ";\" :: \"r\"(3u + (team ^ 1u)) : \"memory\")\n";
+    o << "  const unsigned zero_ = (unsigned)((unsigned long long)ntiles >> 62);\n";
+    o << "  if (team == 1) PP_RELEASE();\n";
+  }
   if (TEAMS == 2) {
     o << "  issue(team);\n  if (team == 0) issue(2);\n";
     o << "  for (long long i = team;; i += 2) {\n";
@@ -966,7 +1015,16 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
       o << "    { C v; v.x = " << g.re(i) << "; v.y = " << g.im(i) << "; " << (oop ? "psi_out" : "psi") << "[dbase | "
         << off << "ull] = v; }\n";
     }
-    o << "  }\n}\n";
+    o << "  }\n";
+    if (g.token) {
+      // the turns alternate strictly: the team that runs out of tiles first
+      // keeps passing the turn while the other finishes its extra tile
+      o << "  { long long cnt = 0; while (TILE_OK(cnt, TILE(cnt))) ++cnt;\n"
+        << "    const long long mine = (cnt + 1 - (long long)team) / 2, other = (cnt + (long long)team) / 2;\n"
+        << "    for (long long x = mine; x < other; ++x)\n"
+        << "      for (int ph = 0; ph < " << g.token_phases << "; ++ph) { PP_ACQUIRE(); PP_RELEASE(); } }\n";
+    }
+    o << "}\n";
   } else {
     for (int j = 0; j < g.nreg; ++j) {
       const uint32_t sx = swz_host(uint32_t(j) << low, g.c128) & lmask;
@@ -980,7 +1038,16 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
     }
     o << "    TEAM_SYNC();\n";  // the buffer is free: refill it with tile i + 3
     o << "    issue(i + 3);\n";
-    o << "  }\n}\n";
+    o << "  }\n";
+    if (g.token) {
+      // the turns alternate strictly: the team that runs out of tiles first
+      // keeps passing the turn while the other finishes its extra tile
+      o << "  { long long cnt = 0; while (TILE_OK(cnt, TILE(cnt))) ++cnt;\n"
+        << "    const long long mine = (cnt + 1 - (long long)team) / 2, other = (cnt + (long long)team) / 2;\n"
+        << "    for (long long x = mine; x < other; ++x)\n"
+        << "      for (int ph = 0; ph < " << g.token_phases << "; ++ph) { PP_ACQUIRE(); PP_RELEASE(); } }\n";
+    }
+    o << "}\n";
   }
   if (carry_scale) {
     carry_scale[0] = g.Sr;
