@@ -907,9 +907,10 @@ std::string jit_source(const PartPlan& pl, int dtype, int n_local, double* fp64_
   int gate_instrs = 0;
   for (const Instr& in : pl.prog) gate_instrs += in.op == I_DENSE || in.op == I_PERM || in.op == I_DIAG;
   constexpr int TOKEN_AUTO_GATES = 10;
+  const char* tok_env = std::getenv("HISVSIM_FP64_TOKEN");
+  const std::string tok = tok_env && *tok_env ? tok_env : "auto";  // default: auto; "0" off; "1" every launch
   g.token = TEAMS == 2 && cl == 0 && NT >= 32 &&
-            (env_on("HISVSIM_FP64_TOKEN", "1") ||
-             (env_on("HISVSIM_FP64_TOKEN", "auto") && gate_instrs <= TOKEN_AUTO_GATES));
+            (tok == "1" || (tok == "auto" && gate_instrs <= TOKEN_AUTO_GATES));
   g.token_threads = 2 * NT;
   if (g.token) {
     // named barriers 3 + team: a team waits on its own, the other team's
